@@ -1,0 +1,412 @@
+#!/usr/bin/env python3
+"""Benchmark of the filter hot path (BASELINE.json metric) -> ONE JSON line on rank 0.
+
+A step = one pass of the whole hot path over the workload:
+  tf_build_filter (bbox, keys, radix sort, cell start, count, scan, fill with Hs)
+  + APPLIES x (tf_sensitivity_filter + tf_density_filter)
+on config 5 by default (12M Kuhn-tet centroids, rmin 1.5, 20 applies; BASELINE.json
+configs[4] -- the configuration the north-star targets are quoted on), inputs resident in
+HBM. value = algorithmic bytes of the step / step time (GB/s; bytes model SURVEY.md 8(d)).
+
+Multi-GPU (`torchrun --nproc-per-node N bench.py --gpus N`): the filter does not shard in
+the 1-GPU scope, so every rank runs an independent
+replica (weak scaling); time = max over ranks; value = all ranks' bytes / that time.
+
+`--impl reference` times the CPU oracle (test infrastructure, oracle/) on a bounded
+sample of the same workload instead (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+HBM_NOMINAL_GBS = 8000.0
+METRIC = "filter build nnz/s and apply GB/s (fraction of 8 TB/s HBM) at 1 B200"
+
+
+# ------------------------------------------------------------------ bytes model
+
+def sens_bytes(n, nnz):
+    return 12 * nnz + 8 * (n + 1) + 32 * n
+
+
+def dens_bytes(n, nnz):
+    return 12 * nnz + 8 * (n + 1) + 24 * n
+
+
+def build_bytes(n, nnz, dim):
+    return 8 * dim * n + 12 * nnz + 8 * (n + 1) + 8 * n
+
+
+def step_bytes(n, nnz, dim, applies):
+    return build_bytes(n, nnz, dim) + applies * (sens_bytes(n, nnz) + dens_bytes(n, nnz))
+
+
+# ------------------------------------------------------------------ distributed plumbing
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def init_dist(backend):
+    import torch.distributed as dist
+    ws, rank, _ = dist_env()
+    if ws > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend, rank=rank, world_size=ws)
+    return dist if ws > 1 else None
+
+
+def reduce_max(value: float, dist=None, device=None) -> float:
+    """Max over ranks (timing rule: the job is as slow as its slowest rank)."""
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate(per_rank_units: float, world: int, max_seconds: float) -> float:
+    """Whole-job throughput: units processed by all ranks / slowest rank's time."""
+    return per_rank_units * world / max_seconds
+
+
+# ------------------------------------------------------------------ clocks (NVML, sampled during timing)
+
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index=0, period=0.1):
+        self.samples, self.reasons = [], 0
+        self.period = period
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy, read+write bytes)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get("k_spmv_sens_bytes_per_launch"), d.get("source")
+    except Exception:
+        return None, None
+
+
+# ------------------------------------------------------------------ workload
+
+def load_workload(cfg):
+    c, x, dc, rmin = synth.workload(cfg)
+    return c, x, dc, rmin, synth.CONFIGS[cfg]
+
+
+# ------------------------------------------------------------------ CPU oracle baseline
+
+def oracle_sample(c, x, dc, rmin, applies, rows_per_step, steps, seed_cfg):
+    """Time the oracle (as it stands, single thread) on a bounded sample of the workload:
+    the cell list over all N points (setup, charged pro rata), then for `rows_per_step`
+    seeded rows: the row build (count + fill) and `applies` sensitivity + density applies.
+    Returns (GB/s of the sample's algorithmic bytes, per-step seconds list, description)."""
+    import oracle
+    n, dim = c.shape
+    t0 = time.perf_counter()
+    cl = oracle.CellList(c, rmin)
+    t_setup = time.perf_counter() - t0
+    all_rows = synth.sample_rows(seed_cfg, n, rows_per_step * steps)
+    vals, times = [], []
+    for s in range(steps):
+        rows = np.sort(all_rows[s * rows_per_step:(s + 1) * rows_per_step])
+        t0 = time.perf_counter()
+        H = cl.rows(rows)
+        for _ in range(applies):
+            oracle.apply_sensitivity(H, x, dc)
+            oracle.apply_density(H, x)
+        dt = time.perf_counter() - t0 + t_setup * len(rows) / n
+        m = len(rows)
+        nnz = H.nnz
+        b = (8 * dim * m + 12 * nnz + 8 * m + 8 * m) + applies * (
+            (12 * nnz + 8 * m + 32 * m) + (12 * nnz + 8 * m + 24 * m))
+        vals.append(b / dt / 1e9)
+        times.append(dt)
+    cl.close()
+    desc = (f"{rows_per_step} seeded rows per step (stream S(c,5,0)) of the same workload: row build "
+            f"+ {applies}x(sensitivity+density) on those rows; cell-list setup over all {n} points "
+            f"({t_setup:.2f} s) charged pro rata; single-threaded C oracle (-O2 -ffp-contract=off)")
+    return statistics.median(vals), times, desc
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def run_ours(args):
+    import torch
+    dist = init_dist("nccl")
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    import paper_2012_08208_b200 as tf
+
+    c, x, dc, rmin, meta = load_workload(args.config)
+    n, dim = c.shape
+    applies = args.applies if args.applies is not None else meta["applies"]
+    cd = torch.from_numpy(c).to(device)
+    xd = torch.from_numpy(x).to(device)
+    dcd = torch.from_numpy(dc).to(device)
+    out_s = torch.empty_like(xd)
+    out_d = torch.empty_like(xd)
+    stream = torch.cuda.current_stream()
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    rec = {"build": [], "sens": [], "dens": []}
+
+    def step(record):
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        f = tf.tf_build_filter(cd, rmin)
+        e1.record(stream)
+        pairs = []
+        for _ in range(applies):
+            a, b, d = ev(), ev(), ev()
+            a.record(stream)
+            f.sensitivity(xd, dcd, out=out_s)
+            b.record(stream)
+            f.density(xd, out=out_d)
+            d.record(stream)
+            pairs.append((a, b, d))
+        if record:
+            rec["_pending"] = (e0, e1, pairs)
+        return f
+
+    # warm-up (untimed)
+    nnz = None
+    for _ in range(args.warmup):
+        f = step(False)
+        nnz = f.nnz
+        f.close()
+    torch.cuda.synchronize()
+
+    # timed: K steps bracketed by barrier + synchronize; events on the launching stream
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    k0 = tf.kernel_launches()
+    filters_launches = 0
+    with ClockSampler(local) as clk:
+        t_start, t_end = ev(), ev()
+        t_start.record(stream)
+        for _ in range(args.steps):
+            f = step(True)
+            nnz = f.nnz
+            f.close()  # frees on the device (stream-ordered pool), inside the step
+            e0, e1, pairs = rec.pop("_pending")
+            rec.setdefault("_all", []).append((e0, e1, pairs))
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = tf.kernel_launches() - k0
+    if dist:
+        dist.barrier()
+    elapsed = t_start.elapsed_time(t_end) / 1e3
+    for e0, e1, pairs in rec["_all"]:
+        rec["build"].append(e0.elapsed_time(e1) / 1e3)
+        for a, b, d in pairs:
+            rec["sens"].append(a.elapsed_time(b) / 1e3)
+            rec["dens"].append(b.elapsed_time(d) / 1e3)
+    t_max = reduce_max(elapsed, dist, device)
+
+    sb = step_bytes(n, nnz, dim, applies)
+    value = aggregate(sb * args.steps, ws, t_max) / 1e9
+    t_sens = statistics.mean(rec["sens"])
+    t_dens = statistics.mean(rec["dens"])
+    t_build = statistics.mean(rec["build"])
+    peak, peak_src = measured_peak()
+    sens_gbs = sens_bytes(n, nnz) / t_sens / 1e9
+    traffic, traffic_src = ncu_traffic()
+
+    # correctness guard on the timed path (one row sample, cheap)
+    res = {}
+    if not args.no_e2e and rank == 0:
+        res["e2e"] = run_e2e(tf, c, x, dc, rmin, applies, n, nnz, dim, args)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        v, times, desc = oracle_sample(c, x, dc, rmin, applies, args.cpu_rows, 1, args.config)
+        cpu = {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc,
+               "seconds": times}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": meta["name"], "config_index": args.config, "n": n, "dim": dim,
+                       "rmin": rmin, "nnz": nnz, "applies_per_step": applies,
+                       "step": "build + applies x (sensitivity + density)",
+                       "l2": "inputs larger than L2 (CSR %.1f GB >> 126 MB L2); no flush" % (12 * nnz / 1e9),
+                       "parallelism": f"replicas{ws}"},
+            "build": {"ms": t_build * 1e3, "nnz_per_s": nnz / t_build,
+                      "gbs": build_bytes(n, nnz, dim) / t_build / 1e9,
+                      "frac_of_8tbs": build_bytes(n, nnz, dim) / t_build / 1e9 / HBM_NOMINAL_GBS},
+            "apply": {"sensitivity_us": t_sens * 1e6, "sensitivity_gbs": sens_gbs,
+                      "sensitivity_frac_of_8tbs": sens_gbs / HBM_NOMINAL_GBS,
+                      "density_us": t_dens * 1e6, "density_gbs": dens_bytes(n, nnz) / t_dens / 1e9,
+                      "density_frac_of_8tbs": dens_bytes(n, nnz) / t_dens / 1e9 / HBM_NOMINAL_GBS,
+                      "iters_per_s": 1.0 / (t_sens + t_dens)},
+            "roofline": {"kernel": "k_spmv<sensitivity>", "bound": "hbm", "achieved": sens_gbs, "peak": peak,
+                         "unit": "GB/s", "frac": sens_gbs / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": sens_bytes(n, nnz), "peak_source": peak_src,
+                         "traffic_source": traffic_src},
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        line.update(res)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_e2e(tf, c, x, dc, rmin, applies, n, nnz, dim, args):
+    """Same step through the C ABI's host-buffer variants: H2D of centroids / x / dc from
+    pinned memory and D2H of every filtered field inside the timed region."""
+    import torch
+    cp = torch.from_numpy(c).pin_memory().numpy()
+    xp = torch.from_numpy(x).pin_memory().numpy()
+    dcp = torch.from_numpy(dc).pin_memory().numpy()
+    os_ = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+    od = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+
+    def step():
+        f = tf.tf_build_filter_host(cp, rmin)
+        for _ in range(applies):
+            f.sensitivity_host(xp, dcp, os_)
+            f.density_host(xp, od)
+        f.close()
+
+    step()  # warm-up
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        step()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    h2d = 8 * dim * n + applies * (16 * n + 8 * n)
+    d2h = applies * (8 * n + 8 * n)
+    return {"value": step_bytes(n, nnz, dim, applies) / t / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "seconds_per_step": t,
+            "timer": "host wall clock around the blocking C-ABI *_host calls"}
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    c, x, dc, rmin, meta = load_workload(args.config)
+    n, dim = c.shape
+    applies = args.applies if args.applies is not None else meta["applies"]
+    v, times, desc = oracle_sample(c, x, dc, rmin, applies, args.cpu_rows, args.warmup + args.steps, args.config)
+    timed = times[args.warmup:]
+    vals = v
+    line = {
+        "impl": "reference", "metric": METRIC, "value": vals, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": statistics.mean(timed) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": meta["name"], "config_index": args.config, "n": n, "dim": dim, "rmin": rmin,
+                   "applies_per_step": applies, "step": "bounded sample, see cpu_baseline.sample",
+                   "parallelism": "cpu single thread"},
+        "cpu_baseline": {"value": vals, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc},
+        "e2e": {"value": vals, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--applies", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=20000)
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: timing rules need --warmup >= 3", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

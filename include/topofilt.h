@@ -1,0 +1,155 @@
+/*
+ * topofilt.h -- C ABI of libtopofilt, the B200 (sm_100a) mesh-independency filter of
+ * Gupta et al., "A 55-line code for large-scale parallel topology optimization in
+ * 2D and 3D" (arXiv 2012.08208).
+ *
+ * The operations (PAPER.md = the paper's LaTeX source):
+ *   build   W_ij = max(0, rmin - |c_i - c_j|) over cell-midpoint pairs within rmin
+ *           (Eq. filter_cond; listing PAPER.md:442-444) and the
+ *           row sums Hs_i = sum_j W_ij. Built once, outside the
+ *           optimisation loop. Stored as CSR: pairs with d^2 < rmin^2,
+ *           d^2 = (dx*dx + dy*dy) + dz*dz in fp64, no FMA contraction; columns
+ *           ascending; weights fp64 (readings R1-R4).
+ *   sensitivity filter   dc~_i = (sum_j W_ij x_j dc_j) / (Hs_i * max(1e-3, x_i))
+ *           (Eq. filter, Eq. filter_mat PAPER.md:401-439,
+ *           listing PAPER.md:447; the max(1e-3, .) floor is BASELINE.json's).
+ *   density filter       x~_i = (sum_j W_ij x_j) / Hs_i   (BASELINE.json north_star;
+ *           not in the paper).
+ *
+ * Conventions for every call:
+ *   - Array arguments are CUDA DEVICE pointers unless the name ends in _host.
+ *     Device arrays are contiguous, 8-byte aligned, and owned by the caller.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Work is stream-ordered; apply calls are asynchronous (no host sync).
+ *   - Every call returns tf_status; nothing throws or aborts across the ABI.
+ *     On a non-OK status tf_last_error() returns a thread-local message.
+ *   - Sizes: 1 <= n < 2^31 - 1 (int32 column indices); nnz < 2^63.
+ */
+#ifndef TOPOFILT_H
+#define TOPOFILT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TOPOFILT_VERSION 1
+
+#if defined(__GNUC__)
+#define TF_API __attribute__((visibility("default")))
+#else
+#define TF_API
+#endif
+
+typedef struct tf_filter_s *tf_filter; /* opaque; owns rowptr/cols/vals/hs; immutable after build */
+
+typedef enum {
+    TF_OK = 0,
+    TF_ERR_INVALID = 1,  /* bad argument: dim not 2/3, n out of range, rmin <= 0 / NaN / Inf,
+                            NULL pointer, host pointer where a device pointer is required,
+                            non-finite centroid, out aliasing x or dc */
+    TF_ERR_NOMEM = 2,    /* device allocation failed (message states the bytes and nnz) */
+    TF_ERR_CUDA = 3,     /* any CUDA runtime error (message carries cudaGetErrorString) */
+    TF_ERR_OVERFLOW = 4  /* nnz does not fit the index types */
+} tf_status;
+
+/* Borrowed device views of a built filter; valid until tf_free(h). */
+typedef struct {
+    int64_t n;            /* rows = columns = number of cells */
+    int64_t nnz;          /* stored entries (pairs with d^2 < rmin^2, incl. the diagonal) */
+    int32_t dim;          /* 2 or 3 */
+    double rmin;          /* filter radius */
+    const int64_t *rowptr;/* [n+1], rowptr[0] = 0, rowptr[n] = nnz */
+    const int32_t *cols;  /* [nnz], strictly ascending inside each row */
+    const double *vals;   /* [nnz], W_ij in [0, rmin]; W_ii = rmin */
+    const double *hs;     /* [n], Hs_i = sum_j W_ij */
+} tf_view;
+
+/* Build statistics (diagnostics; all host values). */
+typedef struct {
+    double bin_side;      /* cell-list bin side s >= rmin*(1+1e-6) */
+    int64_t bins[3];      /* bins per dimension (bins[2] = 1 in 2D) */
+    int64_t nbins;
+    int64_t max_candidates; /* largest 3^dim neighbourhood (points) of any bin */
+    int64_t large_rows;   /* rows whose bin neighbourhood exceeded the shared-memory path
+                             (built unsorted, then sorted by the row-sort kernel) */
+    int32_t radix_passes;
+    int32_t reserved;
+} tf_build_info;
+
+/*
+ * tf_build_filter -- build W (CSR) and Hs from cell centroids.
+ *   centroids: device fp64, row-major [n x dim] (cell midpoints).
+ *   n:         number of cells, 1 <= n < 2^31 - 1.
+ *   dim:       2 or 3.
+ *   rmin:      filter radius, finite and > 0 (rmin <= 0 is invalid).
+ *   stream:    cudaStream_t; the call synchronises this stream twice (bounding box
+ *              and nnz readback) and returns a complete handle.
+ *   out:       receives the handle (set to NULL on failure).
+ * Errors: TF_ERR_INVALID (arguments, non-finite centroid), TF_ERR_NOMEM, TF_ERR_CUDA,
+ *         TF_ERR_OVERFLOW.
+ */
+TF_API tf_status tf_build_filter(const double *centroids, int64_t n, int dim, double rmin,
+                          void *stream, tf_filter *out);
+
+/* tf_filter_view -- borrowed device pointers of the CSR and Hs (no copy). */
+TF_API tf_status tf_filter_view(tf_filter h, tf_view *v);
+
+/* tf_build_stats -- diagnostics of the build that produced h (zeros for imported CSRs). */
+TF_API tf_status tf_build_stats(tf_filter h, tf_build_info *info);
+
+/*
+ * tf_sensitivity_filter -- out_i = (sum_j W_ij x_j dc_j) / (Hs_i * max(1e-3, x_i)).
+ *   x, dc: device fp64 [n]; out: device fp64 [n], must not overlap x or dc
+ *   (the gather reads other rows' inputs). One kernel launch on `stream`, no sync.
+ *   NaNs propagate, except max(1e-3, NaN) = 1e-3 (fmax semantics).
+ */
+TF_API tf_status tf_sensitivity_filter(tf_filter h, const double *x, const double *dc, double *out,
+                                void *stream);
+
+/* tf_density_filter -- out_i = (sum_j W_ij x_j) / Hs_i. Same conventions. */
+TF_API tf_status tf_density_filter(tf_filter h, const double *x, double *out, void *stream);
+
+/* tf_free -- release everything the handle owns (synchronises the device). NULL: no-op. */
+TF_API void tf_free(tf_filter h);
+
+/* tf_last_error -- thread-local message for the last non-OK status of this thread. */
+TF_API const char *tf_last_error(void);
+
+/* ------------------------------------------------------------------ host-buffer variants
+ * The same operations on HOST arrays (end-to-end path): inputs are copied to
+ * handle-owned device buffers on `stream`, the kernel runs, and the result is copied
+ * back; the call synchronises `stream` before returning so `*_host` outputs are valid.
+ * Pinned (page-locked) host memory gives full PCIe bandwidth; pageable also works. */
+TF_API tf_status tf_build_filter_host(const double *centroids_host, int64_t n, int dim, double rmin,
+                               void *stream, tf_filter *out);
+TF_API tf_status tf_sensitivity_filter_host(tf_filter h, const double *x_host, const double *dc_host,
+                                     double *out_host, void *stream);
+TF_API tf_status tf_density_filter_host(tf_filter h, const double *x_host, double *out_host,
+                                 void *stream);
+
+/* ------------------------------------------------------------------ test / diagnostics */
+
+/* tf_filter_from_csr -- TEST HOOK: wrap a host CSR (e.g. the oracle's) in a handle so the
+ * apply kernels can be tested independently of the GPU build. Arrays are copied; the
+ * caller keeps ownership. rowptr_host [n+1], cols_host [nnz], vals_host [nnz], hs_host [n].
+ * Validates rowptr monotone and 0 <= cols < n. dim/rmin are recorded as given (0 allowed). */
+TF_API tf_status tf_filter_from_csr(const int64_t *rowptr_host, const int32_t *cols_host,
+                             const double *vals_host, const double *hs_host, int64_t n,
+                             void *stream, tf_filter *out);
+
+/* Number of CUDA kernels this library has launched in this process (monotone counter). */
+TF_API uint64_t tf_kernel_launches(void);
+
+/* TEST HOOK: make every single device allocation larger than `bytes` fail with
+ * TF_ERR_NOMEM (0 = no limit). Exercises the out-of-memory paths. Process-wide. */
+TF_API void tf_debug_set_alloc_limit(uint64_t bytes);
+
+TF_API int tf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOPOFILT_H */

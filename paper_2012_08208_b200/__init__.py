@@ -1,0 +1,289 @@
+"""Python binding of libtopofilt (include/topofilt.h): argument marshalling only.
+
+Every step of the filter path runs in the CUDA kernels of libtopofilt.so (built in-tree
+for sm_100a by ``_build.py``); this module only passes device pointers, sizes and the
+current torch CUDA stream through ctypes. There is no CPU fallback: if the shared
+library is missing, importing this package raises.
+
+Names mirror the C ABI: ``tf_build_filter``, ``tf_sensitivity_filter``,
+``tf_density_filter``, ``tf_filter_view``, ``tf_free`` (+ ``*_host`` variants), and a
+convenience ``Filter`` object returned by ``tf_build_filter``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtopofilt.so")
+
+TF_OK, TF_ERR_INVALID, TF_ERR_NOMEM, TF_ERR_CUDA, TF_ERR_OVERFLOW = range(5)
+_STATUS = {0: "TF_OK", 1: "TF_ERR_INVALID", 2: "TF_ERR_NOMEM", 3: "TF_ERR_CUDA", 4: "TF_ERR_OVERFLOW"}
+
+# Every symbol include/topofilt.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "tf_build_filter", "tf_filter_view", "tf_build_stats", "tf_sensitivity_filter", "tf_density_filter",
+    "tf_free", "tf_last_error", "tf_build_filter_host", "tf_sensitivity_filter_host",
+    "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
+    "tf_version",
+]
+
+
+class TopofiltError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class tf_view(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("dim", ctypes.c_int32),
+                ("rmin", ctypes.c_double), ("rowptr", ctypes.c_void_p), ("cols", ctypes.c_void_p),
+                ("vals", ctypes.c_void_p), ("hs", ctypes.c_void_p)]
+
+
+class tf_build_info(ctypes.Structure):
+    _fields_ = [("bin_side", ctypes.c_double), ("bins", ctypes.c_int64 * 3), ("nbins", ctypes.c_int64),
+                ("max_candidates", ctypes.c_int64), ("large_rows", ctypes.c_int64),
+                ("radix_passes", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libtopofilt.so not built at {LIB_PATH}: run `python __graft_entry__.py build` "
+                          "(the CUDA path has no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    sig = {
+        "tf_build_filter": ([P, I64, I32, D, P, PP], I32),
+        "tf_build_filter_host": ([P, I64, I32, D, P, PP], I32),
+        "tf_filter_view": ([P, ctypes.POINTER(tf_view)], I32),
+        "tf_build_stats": ([P, ctypes.POINTER(tf_build_info)], I32),
+        "tf_sensitivity_filter": ([P, P, P, P, P], I32),
+        "tf_density_filter": ([P, P, P, P], I32),
+        "tf_sensitivity_filter_host": ([P, P, P, P, P], I32),
+        "tf_density_filter_host": ([P, P, P, P], I32),
+        "tf_filter_from_csr": ([P, P, P, P, I64, P, PP], I32),
+        "tf_free": ([P], None),
+        "tf_last_error": ([], ctypes.c_char_p),
+        "tf_kernel_launches": ([], ctypes.c_uint64),
+        "tf_debug_set_alloc_limit": ([ctypes.c_uint64], None),
+        "tf_version": ([], I32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _check(status: int):
+    if status != TF_OK:
+        raise TopofiltError(status, _lib.tf_last_error().decode(errors="replace"))
+
+
+def _stream_ptr(stream=None):
+    """None -> torch's current CUDA stream; 0 -> the legacy default stream; else a torch.cuda.Stream."""
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dptr(t, name, dtype=None, numel=None):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA torch.Tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements, got {t.numel()}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ wrapper for zero-copy torch views of handle memory."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, True),
+                                         "version": 3, "strides": None}
+
+
+class Filter:
+    """A built filter (owns a tf_filter handle). Immutable; applies are stream-ordered."""
+
+    def __init__(self, handle: ctypes.c_void_p, keepalive=None):
+        self._h = handle
+        self._keep = keepalive
+        v = tf_view()
+        _check(_lib.tf_filter_view(self._h, ctypes.byref(v)))
+        self.n, self.nnz, self.dim, self.rmin = v.n, v.nnz, v.dim, v.rmin
+        self._v = v
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("filter is closed")
+        return self._h
+
+    def sensitivity(self, x, dc, out=None, stream=None):
+        """dc~ = H(x∘dc) / (Hs∘max(1e-3, x)) (Eq. filter_mat)."""
+        import torch
+        if out is None:
+            out = torch.empty_like(x)
+        tf_sensitivity_filter(self, x, dc, out, stream)
+        return out
+
+    def density(self, x, out=None, stream=None):
+        """x~ = Hx / Hs (BASELINE.json north_star)."""
+        import torch
+        if out is None:
+            out = torch.empty_like(x)
+        tf_density_filter(self, x, out, stream)
+        return out
+
+    def csr(self):
+        """Zero-copy torch views (rowptr int64, cols int32, vals f64, hs f64) tied to this handle."""
+        import torch
+        v = self._v
+        mk = lambda p, n, t: torch.as_tensor(_CudaArray(p, (n,), t), device="cuda")
+        return (mk(v.rowptr, self.n + 1, "<i8"), mk(v.cols, self.nnz, "<i4"),
+                mk(v.vals, self.nnz, "<f8"), mk(v.hs, self.n, "<f8"))
+
+    def stats(self) -> dict:
+        info = tf_build_info()
+        _check(_lib.tf_build_stats(self.handle, ctypes.byref(info)))
+        return {"bin_side": info.bin_side, "bins": list(info.bins), "nbins": info.nbins,
+                "max_candidates": info.max_candidates, "large_rows": info.large_rows,
+                "radix_passes": info.radix_passes}
+
+    def sensitivity_host(self, x: np.ndarray, dc: np.ndarray, out: np.ndarray | None = None, stream=None):
+        return tf_sensitivity_filter_host(self, x, dc, out, stream)
+
+    def density_host(self, x: np.ndarray, out: np.ndarray | None = None, stream=None):
+        return tf_density_filter_host(self, x, out, stream)
+
+    def close(self):
+        if self._h is not None:
+            _lib.tf_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+# ------------------------------------------------------------------ C-ABI-named functions
+
+def tf_build_filter(centroids, rmin: float, stream=None) -> Filter:
+    """Build H (CSR) and Hs from device centroids [N, dim] float64."""
+    import torch
+    if centroids.dim() != 2:
+        raise ValueError("centroids must be [N, dim]")
+    n, dim = centroids.shape
+    h = ctypes.c_void_p()
+    _check(_lib.tf_build_filter(_dptr(centroids, "centroids", torch.float64), n, dim, float(rmin),
+                                _stream_ptr(stream), ctypes.byref(h)))
+    return Filter(h)
+
+
+def tf_build_filter_host(centroids: np.ndarray, rmin: float, stream=None) -> Filter:
+    c = np.ascontiguousarray(centroids, dtype=np.float64)
+    n, dim = c.shape
+    h = ctypes.c_void_p()
+    _check(_lib.tf_build_filter_host(c.ctypes.data_as(ctypes.c_void_p), n, dim, float(rmin),
+                                     _stream_ptr(stream), ctypes.byref(h)))
+    return Filter(h)
+
+
+def tf_sensitivity_filter(f: Filter, x, dc, out, stream=None):
+    import torch
+    _check(_lib.tf_sensitivity_filter(f.handle, _dptr(x, "x", torch.float64, f.n),
+                                      _dptr(dc, "dc", torch.float64, f.n),
+                                      _dptr(out, "out", torch.float64, f.n), _stream_ptr(stream)))
+    return out
+
+
+def tf_density_filter(f: Filter, x, out, stream=None):
+    import torch
+    _check(_lib.tf_density_filter(f.handle, _dptr(x, "x", torch.float64, f.n),
+                                  _dptr(out, "out", torch.float64, f.n), _stream_ptr(stream)))
+    return out
+
+
+def _host(a, n, name, writable=False):
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous or a.size != n:
+        raise TypeError(f"{name} must be a contiguous float64 numpy array of {n} elements")
+    if writable and not a.flags.writeable:
+        raise ValueError(f"{name} must be writable")
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def tf_sensitivity_filter_host(f: Filter, x, dc, out=None, stream=None):
+    if out is None:
+        out = np.empty(f.n, dtype=np.float64)
+    _check(_lib.tf_sensitivity_filter_host(f.handle, _host(x, f.n, "x"), _host(dc, f.n, "dc"),
+                                           _host(out, f.n, "out", True), _stream_ptr(stream)))
+    return out
+
+
+def tf_density_filter_host(f: Filter, x, out=None, stream=None):
+    if out is None:
+        out = np.empty(f.n, dtype=np.float64)
+    _check(_lib.tf_density_filter_host(f.handle, _host(x, f.n, "x"), _host(out, f.n, "out", True),
+                                       _stream_ptr(stream)))
+    return out
+
+
+def tf_filter_view(f: Filter):
+    return f.csr()
+
+
+def tf_free(f: Filter):
+    f.close()
+
+
+def tf_filter_from_csr(rowptr, cols, vals, hs, stream=None) -> Filter:
+    """TEST HOOK: wrap a host CSR (e.g. the oracle's) so the apply kernels can be tested alone."""
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    cols = np.ascontiguousarray(cols, dtype=np.int32)
+    vals = np.ascontiguousarray(vals, dtype=np.float64)
+    hs = np.ascontiguousarray(hs, dtype=np.float64)
+    n = rowptr.shape[0] - 1
+    h = ctypes.c_void_p()
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _check(_lib.tf_filter_from_csr(p(rowptr), p(cols), p(vals), p(hs), n, _stream_ptr(stream),
+                                   ctypes.byref(h)))
+    return Filter(h)
+
+
+def kernel_launches() -> int:
+    return int(_lib.tf_kernel_launches())
+
+
+def set_alloc_limit(nbytes: int):
+    _lib.tf_debug_set_alloc_limit(int(nbytes))
+
+
+def version() -> int:
+    return int(_lib.tf_version())

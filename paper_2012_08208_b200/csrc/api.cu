@@ -1,0 +1,357 @@
+// api.cu -- the C ABI of libtopofilt (include/topofilt.h): argument validation, handle
+// lifetime, stream-ordered allocation, host-buffer variants and diagnostics. All compute
+// is in build.cu / radix.cu / scan.cu / apply.cu; nothing here falls back to the CPU.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+#include <vector>
+
+#include "tf_internal.cuh"
+
+namespace tf {
+
+static thread_local char g_err[1024] = "";
+std::atomic<uint64_t> g_launches{0};
+static std::atomic<uint64_t> g_alloc_limit{0};
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+tf_status dev_alloc(void **p, size_t bytes, cudaStream_t s, const char *what) {
+    *p = nullptr;
+    const uint64_t lim = g_alloc_limit.load();
+    if (lim && bytes > lim) {
+        set_error("out of device memory: %s needs %zu bytes (test allocation limit %llu)", what, bytes,
+                  (unsigned long long)lim);
+        return TF_ERR_NOMEM;
+    }
+    cudaError_t e = cudaMallocAsync(p, bytes, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // clear the sticky-free allocation error
+        *p = nullptr;
+        set_error("out of device memory: %s needs %zu bytes (%s)", what, bytes, cudaGetErrorString(e));
+        return (e == cudaErrorMemoryAllocation) ? TF_ERR_NOMEM : TF_ERR_CUDA;
+    }
+    return TF_OK;
+}
+
+void dev_free(void *p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+tf_status device_info(DeviceInfo *di) {
+    TF_CUDA_TRY(cudaGetDevice(&di->device));
+    // Keep freed stream-ordered allocations cached in the device's default pool (like a
+    // caching allocator) so rebuilding a filter does not go back to the driver each time.
+    static thread_local int pool_set_for = -1;
+    if (pool_set_for != di->device) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, di->device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+        pool_set_for = di->device;
+    }
+    TF_CUDA_TRY(cudaDeviceGetAttribute(&di->sms, cudaDevAttrMultiProcessorCount, di->device));
+    int optin = 0;
+    TF_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, di->device));
+    di->smem_optin = (size_t)optin;
+    return TF_OK;
+}
+
+// Device (or managed) memory check: host pointers are rejected with TF_ERR_INVALID.
+static tf_status require_device(const void *p, const char *name) {
+    if (!p) {
+        set_error("%s is NULL", name);
+        return TF_ERR_INVALID;
+    }
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("%s: cudaPointerGetAttributes failed: %s", name, cudaGetErrorString(e));
+        return TF_ERR_INVALID;
+    }
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) {
+        set_error("%s is not a device pointer (use the *_host variant for host buffers)", name);
+        return TF_ERR_INVALID;
+    }
+    return TF_OK;
+}
+
+static bool overlaps(const void *a, const void *b, size_t bytes) {
+    const char *x = (const char *)a, *y = (const char *)b;
+    return x < y + bytes && y < x + bytes;
+}
+
+static void destroy(tf_filter_s *h) {
+    if (!h) return;
+    cudaDeviceSynchronize();
+    // stream-ordered allocations go back to the pool; the device is idle after the sync
+    if (h->rowptr) cudaFreeAsync(h->rowptr, 0);
+    if (h->cols) cudaFreeAsync(h->cols, 0);
+    if (h->vals) cudaFreeAsync(h->vals, 0);
+    if (h->hs) cudaFreeAsync(h->hs, 0);
+    if (h->plan.rb) cudaFreeAsync(h->plan.rb, 0);
+    cudaFree(h->hx);
+    cudaFree(h->hdc);
+    cudaFree(h->hout);
+    delete h;
+}
+
+static tf_status check_build_args(int64_t n, int dim, double rmin, tf_filter *out) {
+    if (!out) {
+        set_error("out is NULL");
+        return TF_ERR_INVALID;
+    }
+    *out = nullptr;
+    if (dim != 2 && dim != 3) {
+        set_error("dim must be 2 or 3 (got %d)", dim);
+        return TF_ERR_INVALID;
+    }
+    if (n < 1 || n >= (int64_t)0x7fffffff) {
+        set_error("n must satisfy 1 <= n < 2^31-1 (got %lld)", (long long)n);
+        return TF_ERR_INVALID;
+    }
+    if (!isfinite(rmin) || !(rmin > 0.0)) {
+        set_error("rmin must be finite and > 0 (got %g)", rmin);
+        return TF_ERR_INVALID;
+    }
+    return TF_OK;
+}
+
+static tf_status build_common(const double *c, int64_t n, int dim, double rmin, cudaStream_t s,
+                              tf_filter *out) {
+    tf_filter_s *h = new (std::nothrow) tf_filter_s();
+    if (!h) {
+        set_error("host allocation failed");
+        return TF_ERR_NOMEM;
+    }
+    h->n = n;
+    h->dim = dim;
+    h->rmin = rmin;
+    tf_status st = build_filter_device(c, n, dim, rmin, s, h);
+    if (st == TF_OK) st = make_apply_plan(h, s);
+    if (st == TF_OK) {
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            set_error("tf_build_filter: %s", cudaGetErrorString(e));
+            st = TF_ERR_CUDA;
+        }
+    }
+    if (st != TF_OK) {
+        destroy(h);
+        return st;
+    }
+    *out = h;
+    return TF_OK;
+}
+
+}  // namespace tf
+
+using namespace tf;
+
+extern "C" {
+
+int tf_version(void) { return TOPOFILT_VERSION; }
+
+const char *tf_last_error(void) { return g_err; }
+
+uint64_t tf_kernel_launches(void) { return g_launches.load(); }
+
+void tf_debug_set_alloc_limit(uint64_t bytes) { g_alloc_limit.store(bytes); }
+
+tf_status tf_build_filter(const double *centroids, int64_t n, int dim, double rmin, void *stream,
+                          tf_filter *out) {
+    try {
+        TF_TRY(check_build_args(n, dim, rmin, out));
+        TF_TRY(require_device(centroids, "centroids"));
+        return build_common(centroids, n, dim, rmin, (cudaStream_t)stream, out);
+    } catch (...) {
+        set_error("tf_build_filter: unexpected host exception");
+        return TF_ERR_NOMEM;
+    }
+}
+
+tf_status tf_build_filter_host(const double *centroids_host, int64_t n, int dim, double rmin, void *stream,
+                               tf_filter *out) {
+    try {
+        TF_TRY(check_build_args(n, dim, rmin, out));
+        if (!centroids_host) {
+            set_error("centroids_host is NULL");
+            return TF_ERR_INVALID;
+        }
+        cudaStream_t s = (cudaStream_t)stream;
+        DevBuf<double> dc;
+        TF_TRY(dc.alloc((size_t)n * dim, s, "centroids (device copy)"));
+        TF_CUDA_TRY(cudaMemcpyAsync(dc.p, centroids_host, (size_t)n * dim * sizeof(double),
+                                    cudaMemcpyHostToDevice, s));
+        return build_common(dc.p, n, dim, rmin, s, out);
+    } catch (...) {
+        set_error("tf_build_filter_host: unexpected host exception");
+        return TF_ERR_NOMEM;
+    }
+}
+
+tf_status tf_filter_view(tf_filter h, tf_view *v) {
+    if (!h || !v) {
+        set_error("tf_filter_view: NULL argument");
+        return TF_ERR_INVALID;
+    }
+    v->n = h->n;
+    v->nnz = h->nnz;
+    v->dim = h->dim;
+    v->rmin = h->rmin;
+    v->rowptr = h->rowptr;
+    v->cols = h->cols;
+    v->vals = h->vals;
+    v->hs = h->hs;
+    return TF_OK;
+}
+
+tf_status tf_build_stats(tf_filter h, tf_build_info *info) {
+    if (!h || !info) {
+        set_error("tf_build_stats: NULL argument");
+        return TF_ERR_INVALID;
+    }
+    *info = h->info;
+    return TF_OK;
+}
+
+static tf_status check_apply(tf_filter h, const double *x, const double *dc, double *out, bool sens) {
+    if (!h) {
+        set_error("filter handle is NULL");
+        return TF_ERR_INVALID;
+    }
+    TF_TRY(require_device(x, "x"));
+    if (sens) TF_TRY(require_device(dc, "dc"));
+    TF_TRY(require_device(out, "out"));
+    const size_t bytes = (size_t)h->n * sizeof(double);
+    if (overlaps(out, x, bytes) || (sens && overlaps(out, dc, bytes))) {
+        set_error("out must not overlap x or dc");
+        return TF_ERR_INVALID;
+    }
+    return TF_OK;
+}
+
+tf_status tf_sensitivity_filter(tf_filter h, const double *x, const double *dc, double *out, void *stream) {
+    TF_TRY(check_apply(h, x, dc, out, true));
+    return launch_sensitivity(h, x, dc, out, (cudaStream_t)stream);
+}
+
+tf_status tf_density_filter(tf_filter h, const double *x, double *out, void *stream) {
+    TF_TRY(check_apply(h, x, nullptr, out, false));
+    return launch_density(h, x, out, (cudaStream_t)stream);
+}
+
+static tf_status ensure_host_scratch(tf_filter h) {
+    if (h->hx) return TF_OK;
+    const size_t bytes = (size_t)h->n * sizeof(double);
+    TF_CUDA_TRY(cudaMalloc(&h->hx, bytes));
+    TF_CUDA_TRY(cudaMalloc(&h->hdc, bytes));
+    TF_CUDA_TRY(cudaMalloc(&h->hout, bytes));
+    return TF_OK;
+}
+
+tf_status tf_sensitivity_filter_host(tf_filter h, const double *x_host, const double *dc_host, double *out_host,
+                                     void *stream) {
+    if (!h || !x_host || !dc_host || !out_host) {
+        set_error("tf_sensitivity_filter_host: NULL argument");
+        return TF_ERR_INVALID;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    TF_TRY(ensure_host_scratch(h));
+    const size_t bytes = (size_t)h->n * sizeof(double);
+    TF_CUDA_TRY(cudaMemcpyAsync(h->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
+    TF_CUDA_TRY(cudaMemcpyAsync(h->hdc, dc_host, bytes, cudaMemcpyHostToDevice, s));
+    TF_TRY(launch_sensitivity(h, h->hx, h->hdc, h->hout, s));
+    TF_CUDA_TRY(cudaMemcpyAsync(out_host, h->hout, bytes, cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    return TF_OK;
+}
+
+tf_status tf_density_filter_host(tf_filter h, const double *x_host, double *out_host, void *stream) {
+    if (!h || !x_host || !out_host) {
+        set_error("tf_density_filter_host: NULL argument");
+        return TF_ERR_INVALID;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    TF_TRY(ensure_host_scratch(h));
+    const size_t bytes = (size_t)h->n * sizeof(double);
+    TF_CUDA_TRY(cudaMemcpyAsync(h->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
+    TF_TRY(launch_density(h, h->hx, h->hout, s));
+    TF_CUDA_TRY(cudaMemcpyAsync(out_host, h->hout, bytes, cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    return TF_OK;
+}
+
+tf_status tf_filter_from_csr(const int64_t *rowptr_host, const int32_t *cols_host, const double *vals_host,
+                             const double *hs_host, int64_t n, void *stream, tf_filter *out) {
+    if (!out) {
+        set_error("out is NULL");
+        return TF_ERR_INVALID;
+    }
+    *out = nullptr;
+    if (!rowptr_host || !cols_host || !vals_host || !hs_host || n < 1 || n >= (int64_t)0x7fffffff) {
+        set_error("tf_filter_from_csr: NULL array or n out of range");
+        return TF_ERR_INVALID;
+    }
+    if (rowptr_host[0] != 0) {
+        set_error("tf_filter_from_csr: rowptr[0] != 0");
+        return TF_ERR_INVALID;
+    }
+    for (int64_t i = 0; i < n; ++i)
+        if (rowptr_host[i + 1] < rowptr_host[i]) {
+            set_error("tf_filter_from_csr: rowptr not monotone at %lld", (long long)i);
+            return TF_ERR_INVALID;
+        }
+    const int64_t nnz = rowptr_host[n];
+    for (int64_t k = 0; k < nnz; ++k)
+        if (cols_host[k] < 0 || cols_host[k] >= n) {
+            set_error("tf_filter_from_csr: column out of range at %lld", (long long)k);
+            return TF_ERR_INVALID;
+        }
+    cudaStream_t s = (cudaStream_t)stream;
+    tf_filter_s *h = new (std::nothrow) tf_filter_s();
+    if (!h) return TF_ERR_NOMEM;
+    h->n = n;
+    h->nnz = nnz;
+    tf_status st = TF_OK;
+    auto fail = [&](tf_status e) {
+        destroy(h);
+        return e;
+    };
+    if ((st = dalloc(&h->rowptr, n + 1, s, "rowptr")) != TF_OK) return fail(st);
+    if ((st = dalloc(&h->cols, nnz ? nnz : 1, s, "cols")) != TF_OK) return fail(st);
+    if ((st = dalloc(&h->vals, nnz ? nnz : 1, s, "vals")) != TF_OK) return fail(st);
+    if ((st = dalloc(&h->hs, n, s, "hs")) != TF_OK) return fail(st);
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h->rowptr, rowptr_host, (n + 1) * 8, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(h->cols, cols_host, nnz * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(h->vals, vals_host, nnz * 8, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h->hs, hs_host, n * 8, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+        set_error("tf_filter_from_csr: %s", cudaGetErrorString(e));
+        return fail(TF_ERR_CUDA);
+    }
+    if ((st = make_apply_plan(h, s)) != TF_OK) return fail(st);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        set_error("tf_filter_from_csr: %s", cudaGetErrorString(e));
+        return fail(TF_ERR_CUDA);
+    }
+    *out = h;
+    return TF_OK;
+}
+
+void tf_free(tf_filter h) { destroy(h); }
+
+}  // extern "C"

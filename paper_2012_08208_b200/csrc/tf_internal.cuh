@@ -1,0 +1,154 @@
+// tf_internal.cuh -- internal declarations shared by the libtopofilt translation units.
+// Product code only: nothing here is shared with oracle/ (see DESIGN.md "Independence").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/topofilt.h"
+
+namespace tf {
+
+// ------------------------------------------------------------------ errors
+void set_error(const char *fmt, ...);
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+struct Status {  // lightweight status carrier for host orchestration
+    tf_status code = TF_OK;
+    bool ok() const { return code == TF_OK; }
+};
+
+#define TF_CUDA_TRY(expr)                                                                 \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess) {                                                          \
+            ::tf::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),       \
+                            __FILE__, __LINE__);                                          \
+            return TF_ERR_CUDA;                                                           \
+        }                                                                                 \
+    } while (0)
+
+#define TF_LAUNCH_CHECK()                                                                 \
+    do {                                                                                  \
+        ::tf::count_launch();                                                             \
+        cudaError_t _e = cudaGetLastError();                                              \
+        if (_e != cudaSuccess) {                                                          \
+            ::tf::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e),   \
+                            __FILE__, __LINE__);                                          \
+            return TF_ERR_CUDA;                                                           \
+        }                                                                                 \
+    } while (0)
+
+#define TF_TRY(expr)                                                                      \
+    do {                                                                                  \
+        tf_status _s = (expr);                                                            \
+        if (_s != TF_OK) return _s;                                                       \
+    } while (0)
+
+// ------------------------------------------------------------------ memory
+// Stream-ordered device allocation with the test-only allocation limit.
+tf_status dev_alloc(void **p, size_t bytes, cudaStream_t s, const char *what);
+void dev_free(void *p, cudaStream_t s);
+void reset_alloc_budget();
+
+template <class T>
+inline tf_status dalloc(T **p, size_t count, cudaStream_t s, const char *what) {
+    return dev_alloc(reinterpret_cast<void **>(p), count * sizeof(T), s, what);
+}
+
+// Scoped temporary device buffer (freed stream-ordered on scope exit).
+template <class T>
+struct DevBuf {
+    T *p = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { reset(); }
+    tf_status alloc(size_t count, cudaStream_t st, const char *what) {
+        reset();
+        s = st;
+        return dalloc(&p, count ? count : 1, st, what);
+    }
+    void reset() {
+        if (p) dev_free(p, s);
+        p = nullptr;
+    }
+    T *release() {
+        T *q = p;
+        p = nullptr;
+        return q;
+    }
+};
+
+// ------------------------------------------------------------------ device info
+struct DeviceInfo {
+    int device = -1;
+    int sms = 148;
+    size_t smem_optin = 227 * 1024;
+};
+tf_status device_info(DeviceInfo *di);
+
+// ------------------------------------------------------------------ grid of the cell list
+struct Grid {
+    int dim;
+    double lo[3];
+    double inv_s;   // 1/s, s = bin side
+    double s;
+    int nb[3];      // bins per dimension (nb[2] = 1 in 2D)
+    int64_t nbins;
+    double rmin, r2;
+};
+
+// ------------------------------------------------------------------ apply plan
+struct ApplyPlan {
+    int64_t nblocks = 0;      // row blocks
+    int32_t *rb = nullptr;    // [nblocks+1] first row of each block
+    int block_nnz = 0;        // target nnz per block (window)
+    int stage_cap = 0;        // staged-path capacity (nnz)
+};
+
+}  // namespace tf
+
+// ------------------------------------------------------------------ the handle
+struct tf_filter_s {
+    int64_t n = 0, nnz = 0;
+    int dim = 0;
+    double rmin = 0;
+    int64_t *rowptr = nullptr;
+    int32_t *cols = nullptr;
+    double *vals = nullptr;
+    double *hs = nullptr;
+    tf::ApplyPlan plan;
+    tf_build_info info{};
+    // host-API scratch (lazily allocated, owned)
+    double *hx = nullptr, *hdc = nullptr, *hout = nullptr;
+};
+
+namespace tf {
+
+// scan.cu
+tf_status exclusive_scan_i32_i64(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s);
+tf_status exclusive_scan_i32_i32(const int32_t *in, int32_t *out, int64_t n, cudaStream_t s);
+
+// radix.cu: stable LSD sort of (key, val) pairs by the low `bits` bits of key.
+// Results land in (keys_out, vals_out); the inputs are used as ping-pong scratch.
+tf_status radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys_alt, uint32_t *vals_alt,
+                           int64_t n, int bits, cudaStream_t s, uint32_t **keys_out,
+                           uint32_t **vals_out, int *passes);
+
+// build.cu
+tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, cudaStream_t s,
+                              tf_filter_s *h);
+
+// apply.cu
+tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s);
+tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double *dc, double *out,
+                             cudaStream_t s);
+tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s);
+
+}  // namespace tf
