@@ -117,7 +117,7 @@ class _CudaArray:
     """Minimal __cuda_array_interface__ wrapper for zero-copy torch views of handle memory."""
 
     def __init__(self, ptr, shape, typestr):
-        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, True),
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False),
                                          "version": 3, "strides": None}
 
 

@@ -101,6 +101,7 @@ static void destroy(tf_filter_s *h) {
     if (h->vals) cudaFreeAsync(h->vals, 0);
     if (h->hs) cudaFreeAsync(h->hs, 0);
     if (h->plan.rb) cudaFreeAsync(h->plan.rb, 0);
+    if (h->plan.wlo) cudaFreeAsync(h->plan.wlo, 0);
     cudaFree(h->hx);
     cudaFree(h->hdc);
     cudaFree(h->hout);
@@ -329,9 +330,9 @@ tf_status tf_filter_from_csr(const int64_t *rowptr_host, const int32_t *cols_hos
         destroy(h);
         return e;
     };
-    if ((st = dalloc(&h->rowptr, n + 1, s, "rowptr")) != TF_OK) return fail(st);
-    if ((st = dalloc(&h->cols, nnz ? nnz : 1, s, "cols")) != TF_OK) return fail(st);
-    if ((st = dalloc(&h->vals, nnz ? nnz : 1, s, "vals")) != TF_OK) return fail(st);
+    if ((st = dalloc(&h->rowptr, n + 3, s, "rowptr")) != TF_OK) return fail(st);
+    if ((st = dalloc(&h->cols, nnz + 4, s, "cols")) != TF_OK) return fail(st);
+    if ((st = dalloc(&h->vals, nnz + 4, s, "vals")) != TF_OK) return fail(st);
     if ((st = dalloc(&h->hs, n, s, "hs")) != TF_OK) return fail(st);
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = cudaMemcpyAsync(h->rowptr, rowptr_host, (n + 1) * 8, cudaMemcpyHostToDevice, s);

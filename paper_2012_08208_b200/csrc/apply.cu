@@ -6,12 +6,19 @@
 //                Hadamard product, the max floor and the division fused in)
 //   density      out_i = (sum_k vals[k] * x[cols[k]]) / Hs_i   (BASELINE.json north_star)
 //
-// Work split ("CSR-stream"): the nnz stream is cut into windows of kWindow entries; block b
-// owns the rows whose first entry falls in window b (row-block table rb[], built once per
-// filter by make_apply_plan). A block streams its contiguous nnz range with coalesced
-// loads, forms the products into shared memory, then one warp per row reduces its segment
-// (lane-strided partial sums + xor-shuffle tree: deterministic, no atomics). Rows that make
-// a block's range exceed the staging capacity are reduced one at a time by the whole block.
+// Work split: the nnz stream is cut into windows of kWindow entries; block b owns the rows
+// whose first entry falls in window b (row-block table rb[], built once per filter by
+// make_apply_plan). Per block:
+//   1. one thread issues two TMA bulk copies (cp.async.bulk, mbarrier completion) that
+//      stage the block's contiguous cols/vals range in shared memory -- the CSR stream never
+//      touches the LSU/L1 data pipe, which is left to the x/dc gathers (the measured
+//      bottleneck of an LDG-staged version);
+//   2. G lanes per row (G from the average row length) read their row's cols/vals from
+//      shared memory, gather x (and dc) through L1, and accumulate in registers; a
+//      G-lane xor-shuffle tree gives the row sum (deterministic, no atomics);
+//   3. one thread per row applies the elementwise epilogue with coalesced hs/x loads.
+// Rows that make a block's range exceed the staging capacity are reduced one at a time by
+// the whole block straight from global memory.
 //
 // Roofline: HBM. Algorithmic bytes per apply = 12*nnz + 8(N+1) + 32N (sensitivity) or
 // + 24N (density); gathers of x/dc hit L2/L1 (neighbour columns are index-local).
@@ -22,10 +29,13 @@
 namespace tf {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int kWindow = 2048;   // target nnz per block
-constexpr int kStage = 4096;    // shared-memory staging capacity (doubles)
+constexpr int kCW = 12;                   // consumer warps per block (+1 producer warp)
+constexpr int kThreads = kCW * 32;        // consumer threads
+constexpr int kWindow = 1792;             // target nnz per window (row block)
+constexpr int kStage = 2560;              // staged nnz capacity per stage (multiple of 4): 30 KB
+constexpr int kRowCap = 512;              // staged rowptr capacity per stage (int64, multiple of 2): 4 KB
+constexpr int kStages = 3;                // TMA ring depth per block
+constexpr int kBlocksPerSM = 2;           // persistent grid = kBlocksPerSM x SMs
 
 __global__ void k_plan(const int64_t *__restrict__ rowptr, int64_t n, int64_t nblocks, int32_t *__restrict__ rb) {
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nblocks;
@@ -51,57 +61,224 @@ __device__ __forceinline__ double finish(double acc, double hs_i, double x_i) {
     return acc / hs_i;
 }
 
-template <bool SENS>
-__global__ void __launch_bounds__(kThreads) k_spmv(const int64_t *__restrict__ rowptr,
-                                                   const int32_t *__restrict__ cols,
-                                                   const double *__restrict__ vals,
-                                                   const double *__restrict__ hs,
-                                                   const double *__restrict__ x,
-                                                   const double *__restrict__ dc,
-                                                   double *__restrict__ out,
-                                                   const int32_t *__restrict__ rb) {
-    __shared__ double prod[kStage];
-    __shared__ double red[kWarps];
-    const int r0 = rb[blockIdx.x], r1 = rb[blockIdx.x + 1];
-    if (r0 >= r1) return;
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// ---- TMA bulk copy (global -> shared) with mbarrier completion, evict-first in L2
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(phase)
+            : "memory");
+    }
+}
+
+// try_wait with a suspend-time hint: the producer sleeps instead of spinning on issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(phase), "r"(20000u)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// Persistent, warp-specialised SpMV. Warp kCW (the producer) streams the windows of this
+// block (w = blockIdx.x, + gridDim.x, ...) into a kStages-deep shared-memory ring with TMA
+// bulk copies; full[s] completes when a window's bytes have landed, empty[s] when all kCW
+// consumer warps have left it. Consumer warps claim groups of 32/G rows of the window from a
+// shared counter (dynamic balance, no block-wide barriers); each row is reduced by G lanes
+// that issue U predicated (col, val) shared loads and U x/dc gathers before accumulating,
+// and the group leader writes out[r] directly.
+template <bool SENS, int G, int U>
+__global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int64_t *__restrict__ rowptr,
+                                                                      const int32_t *__restrict__ cols,
+                                                                      const double *__restrict__ vals,
+                                                                      const double *__restrict__ hs,
+                                                                      const double *__restrict__ x,
+                                                                      const double *__restrict__ dc,
+                                                                      double *__restrict__ out,
+                                                                      const int32_t *__restrict__ rb,
+                                                                      const int64_t *__restrict__ wlo,
+                                                                      int64_t nwin) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *svals = reinterpret_cast<double *>(smem_raw);                           // [kStages][kStage]
+    int64_t *srow = reinterpret_cast<int64_t *>(svals + kStages * kStage);          // [kStages][kRowCap]
+    int32_t *scols = reinterpret_cast<int32_t *>(srow + kStages * kRowCap);         // [kStages][kStage]
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    __shared__ int next_row[kStages];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t k0 = rowptr[r0], k1 = rowptr[r1];
-    const int64_t L = k1 - k0;
-    if (L <= kStage) {
-        for (int i = tid; i < (int)L; i += kThreads) {
-            const int64_t k = k0 + i;
-            const int32_t j = __ldg(cols + k);
-            const double v = __ldg(vals + k);
-            const double t = SENS ? __ldg(x + j) * __ldg(dc + j) : __ldg(x + j);
-            prod[i] = v * t;
+    if (tid == 0) {
+        for (int st = 0; st < kStages; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], kCW);
+            next_row[st] = 0;
         }
-        __syncthreads();
-        for (int r = r0 + warp; r < r1; r += kWarps) {
-            const int s = (int)(rowptr[r] - k0), e = (int)(rowptr[r + 1] - k0);
-            double acc = 0.0;
-            for (int i = s + lane; i < e; i += 32) acc += prod[i];
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) out[r] = finish<SENS>(acc, hs[r], x[r]);
-        }
-    } else {
-        for (int r = r0; r < r1; ++r) {
-            const int64_t s = rowptr[r], e = rowptr[r + 1];
-            double acc = 0.0;
-            for (int64_t k = s + tid; k < e; k += kThreads) {
-                const int32_t j = cols[k];
-                const double t = SENS ? x[j] * dc[j] : x[j];
-                acc += vals[k] * t;
+    }
+    __syncthreads();
+
+    if (warp == kCW) {
+        // ---------------- producer
+        if (lane == 0) {
+            uint64_t pol;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+            int it = 0;
+            for (int64_t w = blockIdx.x; w < nwin; w += gridDim.x, ++it) {
+                const int st = it % kStages;
+                const int64_t a = wlo[w], n4 = wlo[w + 1 + nwin] - a;  // wlo[nwin+1+w] = aligned end
+                if (it >= kStages) mbar_wait_sleep(&empty[st], ((it / kStages) - 1) & 1);
+                next_row[st] = 0;  // published to the consumers by the full-barrier completion
+                const int r0 = rb[w], r1 = rb[w + 1];
+                const int r0a = r0 & ~1, nrow = ((r1 + 2) & ~1) - r0a;  // rowptr[r0a .. ), 16-byte aligned
+                if (n4 > 0 && n4 <= kStage && nrow <= kRowCap) {
+                    mbar_expect_tx(&full[st], (uint32_t)n4 * 12u + (uint32_t)nrow * 8u);
+                    bulk_g2s(svals + st * kStage, vals + a, (uint32_t)n4 * 8u, &full[st], pol);
+                    bulk_g2s(scols + st * kStage, cols + a, (uint32_t)n4 * 4u, &full[st], pol);
+                    bulk_g2s(srow + st * kRowCap, rowptr + r0a, (uint32_t)nrow * 8u, &full[st], pol);
+                } else {
+                    mbar_arrive(&full[st]);  // nothing staged: consumers read global memory
+                }
             }
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) red[warp] = acc;
-            __syncthreads();
-            if (tid == 0) {
-                double a = 0.0;
-                for (int w = 0; w < kWarps; ++w) a += red[w];
-                out[r] = finish<SENS>(a, hs[r], x[r]);
-            }
-            __syncthreads();
         }
+        return;
+    }
+
+    // ---------------- consumers
+    constexpr int RPW = 32 / G;  // rows per warp claim
+    const int sub = lane & (G - 1);
+    int it = 0;
+    for (int64_t w = blockIdx.x; w < nwin; w += gridDim.x, ++it) {
+        const int st = it % kStages;
+        const int r0 = rb[w], R = rb[w + 1] - r0;
+        const int64_t a = wlo[w], n4 = wlo[w + 1 + nwin] - a;
+        const int r0a = r0 & ~1, nrow = ((rb[w + 1] + 2) & ~1) - r0a;
+        const bool staged = n4 > 0 && n4 <= kStage && nrow <= kRowCap;
+        const double *sv = svals + st * kStage;
+        const int32_t *sc = scols + st * kStage;
+        const int64_t *sr = srow + st * kRowCap + (r0 - r0a);  // sr[rr] = rowptr[r0 + rr]
+        mbar_wait(&full[st], (it / kStages) & 1);
+        if (staged) {
+            for (;;) {
+                int rbase = 0;
+                if (lane == 0) rbase = atomicAdd(&next_row[st], RPW);
+                rbase = __shfl_sync(0xffffffffu, rbase, 0);
+                if (rbase >= R) break;
+                const int rr = rbase + lane / G;
+                double acc = 0.0, hs_r = 1.0, x_r = 1.0;
+                if (rr < R) {
+                    const int r = r0 + rr;
+                    if (sub == 0) hs_r = hs[r], x_r = x[r];  // epilogue operands, issued early
+                    const int s = (int)(sr[rr] - a), e = (int)(sr[rr + 1] - a);
+                    int32_t j[U];
+                    double v[U], t[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int i = s + sub + u * G;
+                        j[u] = (i < e) ? sc[i] : -1;
+                        v[u] = (i < e) ? sv[i] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        t[u] = (j[u] >= 0) ? (SENS ? __ldg(x + j[u]) * __ldg(dc + j[u]) : __ldg(x + j[u])) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) acc = fma(v[u], t[u], acc);
+                    for (int i = s + sub + U * G; i < e; i += G) {  // rows longer than U*G
+                        const int32_t jj = sc[i];
+                        const double tt = SENS ? __ldg(x + jj) * __ldg(dc + jj) : __ldg(x + jj);
+                        acc = fma(sv[i], tt, acc);
+                    }
+                }
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (sub == 0 && rr < R) out[r0 + rr] = finish<SENS>(acc, hs_r, x_r);
+            }
+        } else {
+            // window too large to stage (long rows): a whole warp per row, from global memory
+            for (;;) {
+                int rr = 0;
+                if (lane == 0) rr = atomicAdd(&next_row[st], 1);
+                rr = __shfl_sync(0xffffffffu, rr, 0);
+                if (rr >= R) break;
+                const int r = r0 + rr;
+                const int64_t s = rowptr[r], e = rowptr[r + 1];
+                double acc = 0.0;
+                for (int64_t k = s + lane; k < e; k += 32) {
+                    const int32_t jj = cols[k];
+                    const double tt = SENS ? x[jj] * dc[jj] : x[jj];
+                    acc = fma(vals[k], tt, acc);
+                }
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0) out[r] = finish<SENS>(acc, hs[r], x[r]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    }
+}
+
+template <bool SENS, int G, int U>
+tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s) {
+    const unsigned grid = (unsigned)std::min<int64_t>(h->plan.nblocks, (int64_t)h->plan.grid);
+    const size_t smem = (size_t)kStages * (kStage * (sizeof(double) + sizeof(int32_t)) + kRowCap * sizeof(int64_t));
+    // per-instantiation attribute (dynamic shared memory above 48 KB needs the opt-in)
+    static bool attr_set = false;
+    if (!attr_set) {
+        TF_CUDA_TRY(cudaFuncSetAttribute(k_spmv<SENS, G, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+    }
+    k_spmv<SENS, G, U><<<grid, kThreads + 32, smem, s>>>(h->rowptr, h->cols, h->vals, h->hs, x, dc, out,
+                                                          h->plan.rb, h->plan.wlo, h->plan.nblocks);
+    TF_LAUNCH_CHECK();
+    return TF_OK;
+}
+
+template <bool SENS, int G>
+tf_status launch_spmv_g(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s) {
+    if (h->plan.unroll >= 8) return launch_spmv_gu<SENS, G, 8>(h, x, dc, out, s);
+    return launch_spmv_gu<SENS, G, 4>(h, x, dc, out, s);
+}
+
+template <bool SENS>
+tf_status launch_spmv(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s) {
+    switch (h->plan.group) {
+        case 1: return launch_spmv_g<SENS, 1>(h, x, dc, out, s);
+        case 2: return launch_spmv_g<SENS, 2>(h, x, dc, out, s);
+        case 4: return launch_spmv_g<SENS, 4>(h, x, dc, out, s);
+        case 8: return launch_spmv_g<SENS, 8>(h, x, dc, out, s);
+        case 16: return launch_spmv_g<SENS, 16>(h, x, dc, out, s);
+        default: return launch_spmv_g<SENS, 32>(h, x, dc, out, s);
+    }
+}
+
+// Aligned staging window of each row block: wlo[w] = rowptr[rb[w]] & ~3 and
+// wlo[nwin + 1 + w] = (rowptr[rb[w+1]] + 3) & ~3 (16-byte aligned bulk copies).
+__global__ void k_plan_windows(const int64_t *__restrict__ rowptr, const int32_t *__restrict__ rb, int64_t nwin,
+                               int64_t *__restrict__ wlo) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
+        wlo[w] = rowptr[rb[w]] & ~(int64_t)3;
+        wlo[nwin + 1 + w] = (rowptr[rb[w + 1]] + 3) & ~(int64_t)3;
     }
 }
 
@@ -114,28 +291,37 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
         return TF_ERR_OVERFLOW;
     }
     TF_TRY(dalloc(&h->plan.rb, nblocks + 1, s, "apply row blocks"));
+    TF_TRY(dalloc(&h->plan.wlo, 2 * nblocks + 1, s, "apply windows"));
+    DeviceInfo di;
+    TF_TRY(device_info(&di));
+    h->plan.grid = di.sms * kBlocksPerSM;
     h->plan.nblocks = nblocks;
     h->plan.block_nnz = kWindow;
     h->plan.stage_cap = kStage;
+    // lanes per row in the reduction: about 3 entries per lane (wide groups keep the x/dc
+    // gathers of one warp instruction on few cache lines)
+    // lanes per row G ~ avg/6 (G lanes of a warp gather neighbouring columns of one row);
+    // unroll U so that U*G covers ~1.25x the average row in one batch of loads
+    const double avg = (double)h->nnz / (double)std::max<int64_t>(1, h->n);
+    int g = 1;
+    while (g < 32 && 6.0 * g < avg) g *= 2;
+    h->plan.group = g;
+    h->plan.unroll = (1.25 * avg > 4.0 * g) ? 8 : 4;
     const unsigned grid = (unsigned)std::min<int64_t>((nblocks + 256) / 256, 65535);
     k_plan<<<grid, 256, 0, s>>>(h->rowptr, h->n, nblocks, h->plan.rb);
+    TF_LAUNCH_CHECK();
+    k_plan_windows<<<grid, 256, 0, s>>>(h->rowptr, h->plan.rb, nblocks, h->plan.wlo);
     TF_LAUNCH_CHECK();
     return TF_OK;
 }
 
 tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double *dc, double *out,
                              cudaStream_t s) {
-    k_spmv<true><<<(unsigned)h->plan.nblocks, kThreads, 0, s>>>(h->rowptr, h->cols, h->vals, h->hs, x, dc, out,
-                                                                h->plan.rb);
-    TF_LAUNCH_CHECK();
-    return TF_OK;
+    return launch_spmv<true>(h, x, dc, out, s);
 }
 
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s) {
-    k_spmv<false><<<(unsigned)h->plan.nblocks, kThreads, 0, s>>>(h->rowptr, h->cols, h->vals, h->hs, x, nullptr,
-                                                                 out, h->plan.rb);
-    TF_LAUNCH_CHECK();
-    return TF_OK;
+    return launch_spmv<false>(h, x, nullptr, out, s);
 }
 
 }  // namespace tf

@@ -90,14 +90,32 @@ __global__ void __launch_bounds__(256) k_bbox_partial(const double *__restrict__
     }
 }
 
-__global__ void k_bbox_final(const double *__restrict__ part, int nparts, double *__restrict__ out) {
-    if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(256) k_bbox_final(const double *__restrict__ part, int nparts,
+                                                    double *__restrict__ out) {
     double r[7] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0};
-    for (int b = 0; b < nparts; ++b) {
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
         for (int d = 0; d < 3; ++d) r[d] = fmin(r[d], part[b * 7 + d]), r[3 + d] = fmax(r[3 + d], part[b * 7 + 3 + d]);
         r[6] = fmax(r[6], part[b * 7 + 6]);
     }
-    for (int k = 0; k < 7; ++k) out[k] = r[k];
+    for (int o = 16; o > 0; o >>= 1) {
+        for (int d = 0; d < 3; ++d) {
+            r[d] = fmin(r[d], __shfl_xor_sync(0xffffffffu, r[d], o));
+            r[3 + d] = fmax(r[3 + d], __shfl_xor_sync(0xffffffffu, r[3 + d], o));
+        }
+        r[6] = fmax(r[6], __shfl_xor_sync(0xffffffffu, r[6], o));
+    }
+    __shared__ double sr[8][7];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0)
+        for (int k = 0; k < 7; ++k) sr[warp][k] = r[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            for (int d = 0; d < 3; ++d) sr[0][d] = fmin(sr[0][d], sr[w][d]), sr[0][3 + d] = fmax(sr[0][3 + d], sr[w][3 + d]);
+            sr[0][6] = fmax(sr[0][6], sr[w][6]);
+        }
+        for (int k = 0; k < 7; ++k) out[k] = sr[0][k];
+    }
 }
 
 // ------------------------------------------------------------------ a3: bin keys
@@ -171,72 +189,292 @@ __device__ __forceinline__ void xtriple_range(int r, int bx, int by, int bz, con
     e = cs[row + xh + 1];
 }
 
-// ------------------------------------------------------------------ a5: count pass
-// One warp per query bin. For each query in the bin, lanes sweep the 3^(dim-1)
-// contiguous x-triple ranges 32 candidates at a time; the exact fp64 test feeds a
-// warp ballot and popc accumulates the row length. Also records the largest
-// neighbourhood (for sizing the fill pass's shared memory).
+// ------------------------------------------------------------------ a5/a7 shared machinery
+// fp32 bin-local prefilter (R4b). Candidates of a query bin are staged as
+// float offsets from the bin centre o: u = fl32(fl64(c - o)). With every staged point within
+// M = 1.5*s*(1+1e-4) of o per component, |d2_f32 - d2| <= E = 1e-5*M^2 (+1e-12*r2 for the
+// fp64 rounding of the reference test); derivation in DESIGN.md. Hence
+//   d2f <  t_in  => the exact fp64 test accepts,   d2f >= t_out => it rejects,
+// and only pairs in [t_in, t_out) -- plus every pair the fill pass keeps -- are decided or
+// weighted by the exact fp64 expression on the original centroid bytes.
+struct BinView {
+    int bx, by, bz;
+    double ox, oy, oz;  // bin centre (fp64)
+};
+
+__device__ __forceinline__ BinView bin_view(int64_t b, const Grid &g) {
+    BinView v;
+    decode_bin(b, g, v.bx, v.by, v.bz);
+    v.ox = g.lo[0] + ((double)v.bx + 0.5) * g.s;
+    v.oy = g.lo[1] + ((double)v.by + 0.5) * g.s;
+    v.oz = (g.dim == 3) ? g.lo[2] + ((double)v.bz + 0.5) * g.s : 0.0;
+    return v;
+}
+
+__device__ __forceinline__ float4 local_f32(double x, double y, double z, const BinView &v) {
+    return make_float4(__double2float_rn(x - v.ox), __double2float_rn(y - v.oy), __double2float_rn(z - v.oz), 0.f);
+}
+
 template <int DIM>
-__global__ void __launch_bounds__(256) k_count(SortedPts P, Grid g, int32_t *__restrict__ counts,
-                                               int32_t *__restrict__ stats) {
-    const int lane = threadIdx.x & 31;
-    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (b >= g.nbins) return;
+__device__ __forceinline__ float d2_f32(const float4 &a, const float4 &b) {
+    const float dx = a.x - b.x, dy = a.y - b.y;
+    float d2 = fmaf(dy, dy, dx * dx);
+    if (DIM == 3) {
+        const float dz = a.z - b.z;
+        d2 = fmaf(dz, dz, d2);
+    }
+    return d2;
+}
+
+// 3^(dim-1) contiguous x-triple ranges of a bin, computed by lanes 0..NR-1 into shared memory.
+template <int DIM>
+__device__ __forceinline__ void load_ranges(const BinView &v, const Grid &g, const int32_t *cs, int *rs, int *rp) {
+    constexpr int NR = (DIM == 3) ? 9 : 3;
+    if (threadIdx.x < NR) {
+        int s, e;
+        xtriple_range<DIM>(threadIdx.x, v.bx, v.by, v.bz, g, cs, s, e);
+        rs[threadIdx.x] = s;
+        rp[threadIdx.x + 1] = e - s;  // lengths, prefix-summed below
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        rp[0] = 0;
+        for (int r = 0; r < NR; ++r) rp[r + 1] += rp[r];
+    }
+    __syncthreads();
+}
+
+// Largest candidate set of any bin (sizes the shared-memory staging).
+template <int DIM>
+__global__ void __launch_bounds__(256) k_binstats(const int32_t *__restrict__ cs, Grid g, int32_t *__restrict__ stats) {
+    constexpr int NR = (DIM == 3) ? 9 : 3;
+    int best = 0;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < g.nbins; b += (int64_t)gridDim.x * blockDim.x) {
+        if (cs[b] == cs[b + 1]) continue;
+        int bx, by, bz;
+        decode_bin(b, g, bx, by, bz);
+        int C = 0;
+        for (int r = 0; r < NR; ++r) {
+            int s, e;
+            xtriple_range<DIM>(r, bx, by, bz, g, cs, s, e);
+            C += e - s;
+        }
+        best = max(best, C);
+    }
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&stats[0], best);
+}
+
+// ------------------------------------------------------------------ a5: count pass
+// Block per query bin, WARPS warps, one warp per query. The bin's candidates (the 3^(dim-1)
+// contiguous x-triples) are staged once as bin-local float4 (+ sorted position for the rare
+// exact re-test); each query sweeps them 32 at a time: surely-in pairs are counted by
+// ballot/popc, band pairs are decided by the exact fp64 test. Neighbourhoods over `cap`
+// fall back to exact fp64 tests straight from the sorted SoA.
+template <int DIM, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_count(SortedPts P, Grid g, int cap, int32_t *__restrict__ counts) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int NR = (DIM == 3) ? 9 : 3;
+    __shared__ int rs[NR], rp[NR + 1];
+    const int64_t b = blockIdx.x;
     const int q0 = P.cs[b], q1 = P.cs[b + 1];
     if (q0 == q1) return;
-    int bx, by, bz;
-    decode_bin(b, g, bx, by, bz);
-    constexpr int NR = (DIM == 3) ? 9 : 3;
-    int rs = 0, re = 0;
-    if (lane < NR) xtriple_range<DIM>(lane, bx, by, bz, g, P.cs, rs, re);
-    int total = re - rs;
-    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-    if (lane == 0) atomicMax(&stats[0], total);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const BinView v = bin_view(b, g);
+    load_ranges<DIM>(v, g, P.cs, rs, rp);
+    const int C = rp[NR];
     const double r2 = g.r2;
-    for (int q = q0; q < q1; ++q) {
-        const double qx = P.x[q], qy = P.y[q], qz = (DIM == 3) ? P.z[q] : 0.0;
-        int cnt = 0;
-#pragma unroll 1
-        for (int r = 0; r < NR; ++r) {
-            const int s = __shfl_sync(0xffffffffu, rs, r), e = __shfl_sync(0xffffffffu, re, r);
-            for (int base = s; base < e; base += 32) {
-                const int p = base + lane;
-                bool ok = false;
-                if (p < e) {
-                    const double d2 = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0);
-                    ok = d2 < r2;
-                }
-                cnt += __popc(__ballot_sync(0xffffffffu, ok));
+    if (C <= cap && g.use_f32) {
+        float4 *F = reinterpret_cast<float4 *>(smem_raw);
+        int32_t *POS = reinterpret_cast<int32_t *>(F + cap);
+        for (int r = warp; r < NR; r += WARPS) {
+            const int s = rs[r], off = rp[r], len = rp[r + 1] - rp[r];
+            for (int i = lane; i < len; i += 32) {
+                const int p = s + i;
+                F[off + i] = local_f32(P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0, v);
+                POS[off + i] = p;
             }
         }
-        if (lane == 0) counts[P.id[q]] = cnt;
+        __syncthreads();
+        const float t_in = g.t_in, t_out = g.t_out;
+        for (int q = q0 + warp; q < q1; q += WARPS) {
+            const double qx = P.x[q], qy = P.y[q], qz = (DIM == 3) ? P.z[q] : 0.0;
+            const float4 fq = local_f32(qx, qy, qz, v);
+            int cnt = 0;
+            for (int t0 = 0; t0 < C; t0 += 32) {
+                const int t = t0 + lane;
+                bool in = false, band = false;
+                if (t < C) {
+                    const float d2f = d2_f32<DIM>(fq, F[t]);
+                    in = d2f < t_in;
+                    band = !in && d2f < t_out;
+                }
+                cnt += __popc(__ballot_sync(0xffffffffu, in));
+                if (__any_sync(0xffffffffu, band)) {
+                    bool ok = false;
+                    if (band) {
+                        const int p = POS[t];
+                        ok = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0) < r2;
+                    }
+                    cnt += __popc(__ballot_sync(0xffffffffu, ok));
+                }
+            }
+            if (lane == 0) counts[P.id[q]] = cnt;
+        }
+    } else {
+        for (int q = q0 + warp; q < q1; q += WARPS) {
+            const double qx = P.x[q], qy = P.y[q], qz = (DIM == 3) ? P.z[q] : 0.0;
+            int cnt = 0;
+            for (int r = 0; r < NR; ++r) {
+                const int s = rs[r], e = rs[r] + rp[r + 1] - rp[r];
+                for (int base = s; base < e; base += 32) {
+                    const int p = base + lane;
+                    bool ok = false;
+                    if (p < e) ok = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0) < r2;
+                    cnt += __popc(__ballot_sync(0xffffffffu, ok));
+                }
+            }
+            if (lane == 0) counts[P.id[q]] = cnt;
+        }
     }
 }
 
 // ------------------------------------------------------------------ a7: fill pass
-template <int DIM>
-struct FillSmem {
-    double *x, *y, *z;
-    int32_t *id;
-    __device__ FillSmem(unsigned char *raw, int cap) {
-        x = reinterpret_cast<double *>(raw);
-        y = x + cap;
-        z = (DIM == 3) ? y + cap : y;
-        id = reinterpret_cast<int32_t *>((DIM == 3 ? z : y) + cap);
+// Block-wide stable LSD radix sort of C (key, val) pairs in shared memory, 8-bit digits.
+// Warp w owns the contiguous strip [w*Q, (w+1)*Q): per-warp digit histograms, a block scan
+// over (digit, warp) in digit-major order, then a stable scatter where the rank inside a
+// 32-element round comes from __match_any_sync peer groups. Returns 0 if the result is in
+// (ka, va), 1 if in (kb, vb).
+template <int WARPS>
+__device__ int block_radix_sort_smem(uint32_t *ka, uint32_t *va, uint32_t *kb, uint32_t *vb, int C, int bits,
+                                     int32_t (*wc)[256], int32_t *wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int Q = (((C + WARPS - 1) / WARPS) + 31) & ~31;
+    const int s0 = min(C, warp * Q), s1 = min(C, s0 + Q);
+    int which = 0;
+    for (int shift = 0; shift < bits; shift += 8) {
+        uint32_t *ki = which ? kb : ka, *vi = which ? vb : va, *ko = which ? ka : kb, *vo = which ? va : vb;
+        for (int i = lane; i < 256; i += 32) wc[warp][i] = 0;
+        __syncwarp();
+        for (int base = s0; base < s1; base += 32) {
+            const int i = base + lane;
+            const int d = (i < s1) ? (int)((ki[i] >> shift) & 255u) : 256;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            if (d < 256 && lane == __ffs(peers) - 1) wc[warp][d] += __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        // exclusive scan over (digit, warp), digit-major: each thread owns DPT consecutive digits
+        constexpr int DPT = 256 / (32 * WARPS);
+        int tot[DPT], run = 0;
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) {
+            const int d = tid * DPT + k;
+            int t = 0;
+#pragma unroll
+            for (int w = 0; w < WARPS; ++w) t += wc[w][d];
+            tot[k] = t;
+            run += t;
+        }
+        int inc = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        int ex = inc - run;
+        for (int w = 0; w < warp; ++w) ex += wsum[w];
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) {
+            const int d = tid * DPT + k;
+            int off = ex;
+#pragma unroll
+            for (int w = 0; w < WARPS; ++w) {
+                const int c = wc[w][d];
+                wc[w][d] = off;
+                off += c;
+            }
+            ex += tot[k];
+        }
+        __syncthreads();
+        for (int base = s0; base < s1; base += 32) {
+            const int i = base + lane;
+            const bool valid = i < s1;
+            const uint32_t key = valid ? ki[i] : 0u, val = valid ? vi[i] : 0u;
+            const int d = valid ? (int)((key >> shift) & 255u) : 256;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const int before = valid ? wc[warp][d] : 0;
+            __syncwarp();
+            if (valid && lane == __ffs(peers) - 1) wc[warp][d] = before + __popc(peers);
+            __syncwarp();
+            if (valid) {
+                const int dst = before + __popc(peers & lt);
+                ko[dst] = key;
+                vo[dst] = val;
+            }
+        }
+        __syncthreads();
+        which ^= 1;
     }
-};
-
-__device__ __forceinline__ int lower_bound_i32(const int32_t *a, int len, int32_t v) {
-    int lo = 0, hi = len;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (a[mid] < v) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
+    return which;
 }
 
-// Block per query bin, WARPS warps. See file header.
+// Shared-memory layout of the fill staging (36 B per candidate).
+struct FillSmem {
+    float4 *f;                      // bin-local fp32 coordinates, SORTED by id
+    int32_t *pos;                   // staged sorted-SoA position (run order)
+    uint32_t *ka, *va, *kb, *vb;    // sort buffers: key = id - lo, val = staging index
+    __device__ FillSmem(unsigned char *raw, int cap) {
+        f = reinterpret_cast<float4 *>(raw);
+        pos = reinterpret_cast<int32_t *>(f + cap);
+        ka = reinterpret_cast<uint32_t *>(pos + cap);
+        va = ka + cap;
+        kb = va + cap;
+        vb = kb + cap;
+    }
+    static constexpr size_t bytes_per() { return 16 + 4 + 16; }
+};
+
+constexpr int kListCap = 256;  // per-warp compacted candidate list (phase A -> phase B)
+
+template <int DIM>
+__device__ __forceinline__ void fill_flush(const SortedPts &P, const uint32_t *skey, const uint32_t *perm,
+                                           const int32_t *pos, const int32_t *list, int nl, int lo,
+                                           double qx, double qy, double qz, double r2, double rmin,
+                                           int64_t base, int &wpos, double &hsum, int32_t *__restrict__ cols,
+                                           double *__restrict__ vals) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int e0 = 0; e0 < nl; e0 += 32) {
+        const int e = e0 + lane;
+        bool ok = false;
+        double d2 = 0.0;
+        int t = 0;
+        if (e < nl) {
+            t = list[e];
+            const int p = pos[perm[t]];
+            d2 = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0);
+            ok = d2 < r2;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+            const double w = weight_of(rmin, d2);
+            const int64_t k = base + wpos + __popc(bal & lt);
+            cols[k] = (int32_t)skey[t] + lo;
+            vals[k] = w;
+            hsum += w;
+        }
+        wpos += __popc(bal);
+    }
+}
+
+// Block per query bin. Stage the candidates, sort them by id with the whole block (so
+// ballot compaction emits every row's columns ascending); phase A: fp32 prefilter -> per-
+// warp list of candidates that may lie inside rmin; phase B: exact fp64 test on the original
+// centroid bytes, weight, CSR write, Hs.
 template <int DIM, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const int64_t *__restrict__ rowptr,
                                                      int32_t *__restrict__ cols, double *__restrict__ vals,
@@ -244,107 +482,103 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
                                                      int32_t *__restrict__ large_rows,
                                                      int32_t *__restrict__ stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int NRUN = (DIM == 3) ? 27 : 9;
-    __shared__ int run_s[NRUN], run_l[NRUN], run_p[NRUN + 1], run_min[NRUN], run_max[NRUN];
+    constexpr int NR = (DIM == 3) ? 9 : 3;
+    __shared__ int rs[NR], rp[NR + 1];
+    __shared__ int32_t wc[WARPS][256];
+    __shared__ int32_t wsum[WARPS];
+    __shared__ int32_t lists[WARPS][kListCap];
+    __shared__ int s_lo, s_hi;
     const int64_t b = blockIdx.x;
     const int q0 = P.cs[b], q1 = P.cs[b + 1];
     if (q0 == q1) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int bx, by, bz;
-    decode_bin(b, g, bx, by, bz);
-    if (tid < NRUN) {
-        const int dz = (DIM == 3) ? (tid / 9 - 1) : 0;
-        const int dy = (tid / 3) % 3 - 1;
-        const int dx = tid % 3 - 1;
-        const int xx = bx + dx, yy = by + dy, zz = bz + dz;
-        int s = 0, l = 0;
-        if (xx >= 0 && xx < g.nb[0] && yy >= 0 && yy < g.nb[1] && zz >= 0 && zz < g.nb[2]) {
-            const int64_t key = ((int64_t)zz * g.nb[1] + yy) * g.nb[0] + xx;
-            s = P.cs[key];
-            l = P.cs[key + 1] - s;
-        }
-        run_s[tid] = s;
-        run_l[tid] = l;
-        run_min[tid] = l ? P.id[s] : 0;
-        run_max[tid] = l ? P.id[s + l - 1] : -1;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        int acc = 0;
-        for (int r = 0; r < NRUN; ++r) run_p[r] = acc, acc += run_l[r];
-        run_p[NRUN] = acc;
-    }
-    __syncthreads();
-    const int C = run_p[NRUN];
-    const double r2 = g.r2, rmin = g.rmin;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    const BinView v = bin_view(b, g);
+    load_ranges<DIM>(v, g, P.cs, rs, rp);
+    const int C = rp[NR];
+    const double r2 = g.r2, rmin = g.rmin;
 
     if (C <= cap) {
-        // ---- stage the candidates in ascending id order (merge-rank of the sorted runs)
-        FillSmem<DIM> S(smem_raw, cap);
-        for (int t = tid; t < C; t += WARPS * 32) {
-            int r = 0;
-            while (t >= run_p[r + 1]) ++r;
-            const int off = t - run_p[r];
-            const int p = run_s[r] + off;
-            const int32_t id = P.id[p];
-            int rank = off;
-#pragma unroll 1
-            for (int r2i = 0; r2i < NRUN; ++r2i) {
-                if (r2i == r) continue;
-                const int l = run_l[r2i];
-                if (l == 0 || id < run_min[r2i]) continue;
-                if (id > run_max[r2i]) {
-                    rank += l;
-                    continue;
-                }
-                rank += lower_bound_i32(P.id + run_s[r2i], l, id);
+        FillSmem S(smem_raw, cap);
+        // ---- stage (run order) + id range
+        int lo = 0x7fffffff, hi = 0;
+        for (int r = warp; r < NR; r += WARPS) {
+            const int s = rs[r], off = rp[r], len = rp[r + 1] - rp[r];
+            for (int i = lane; i < len; i += 32) {
+                const int p = s + i;
+                const int32_t id = P.id[p];
+                S.pos[off + i] = p;
+                S.ka[off + i] = (uint32_t)id;
+                S.va[off + i] = (uint32_t)(off + i);
+                lo = min(lo, id);
+                hi = max(hi, id);
             }
-            S.id[rank] = id;
-            S.x[rank] = P.x[p];
-            S.y[rank] = P.y[p];
-            if (DIM == 3) S.z[rank] = P.z[p];
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (tid == 0) s_lo = 0x7fffffff, s_hi = 0;
+        __syncthreads();
+        if (lane == 0) atomicMin(&s_lo, lo), atomicMax(&s_hi, hi);
+        __syncthreads();
+        lo = s_lo;
+        hi = s_hi;
+        for (int t = tid; t < C; t += WARPS * 32) S.ka[t] -= (uint32_t)lo;
+        __syncthreads();
+        // ---- sort by id (whole block)
+        const int bits = (hi > lo) ? 32 - __clz((unsigned)(hi - lo)) : 0;
+        const int which = block_radix_sort_smem<WARPS>(S.ka, S.va, S.kb, S.vb, C, bits, wc, wsum);
+        const uint32_t *skey = which ? S.kb : S.ka;
+        const uint32_t *perm = which ? S.vb : S.va;
+        for (int t = tid; t < C; t += WARPS * 32) {
+            const int p = S.pos[perm[t]];
+            S.f[t] = local_f32(P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0, v);
         }
         __syncthreads();
-        // ---- one warp per query; candidates in ascending id -> columns ascending
+        // ---- queries: one warp each
+        int32_t *list = lists[warp];
+        const float t_out = g.use_f32 ? g.t_out : INFINITY;
         for (int q = q0 + warp; q < q1; q += WARPS) {
             const double qx = P.x[q], qy = P.y[q], qz = (DIM == 3) ? P.z[q] : 0.0;
+            const float4 fq = local_f32(qx, qy, qz, v);
             const int32_t qid = P.id[q];
             const int64_t base = rowptr[qid];
-            int pos = 0;
+            int wpos = 0, nl = 0;
             double hsum = 0.0;
             for (int t0 = 0; t0 < C; t0 += 32) {
                 const int t = t0 + lane;
-                bool ok = false;
-                double d2 = 0.0;
-                if (t < C) {
-                    d2 = pair_d2<DIM>(qx, qy, qz, S.x[t], S.y[t], (DIM == 3) ? S.z[t] : 0.0);
-                    ok = d2 < r2;
+                bool maybe = false;
+                if (t < C) maybe = d2_f32<DIM>(fq, S.f[t]) < t_out;
+                const uint32_t bal = __ballot_sync(0xffffffffu, maybe);
+                if (maybe) list[nl + __popc(bal & lt_mask)] = t;
+                nl += __popc(bal);
+                if (nl > kListCap - 32) {
+                    __syncwarp();
+                    fill_flush<DIM>(P, skey, perm, S.pos, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum,
+                                    cols, vals);
+                    __syncwarp();
+                    nl = 0;
                 }
-                const uint32_t bal = __ballot_sync(0xffffffffu, ok);
-                if (ok) {
-                    const double w = weight_of(rmin, d2);
-                    const int64_t k = base + pos + __popc(bal & lt_mask);
-                    cols[k] = S.id[t];
-                    vals[k] = w;
-                    hsum += w;
-                }
-                pos += __popc(bal);
             }
+            __syncwarp();
+            fill_flush<DIM>(P, skey, perm, S.pos, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum, cols,
+                            vals);
+            __syncwarp();
             for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
             if (lane == 0) hs[qid] = hsum;
         }
     } else {
-        // ---- large neighbourhood: candidates from global memory in run order; the rows
-        // are recorded and sorted afterwards by k_rowsort.
+        // ---- large neighbourhood: exact tests straight from the sorted SoA, written in
+        // candidate order; the rows are listed and sorted afterwards by k_rowsort.
         for (int q = q0 + warp; q < q1; q += WARPS) {
             const double qx = P.x[q], qy = P.y[q], qz = (DIM == 3) ? P.z[q] : 0.0;
             const int32_t qid = P.id[q];
             const int64_t base = rowptr[qid];
-            int pos = 0;
+            int wpos = 0;
             double hsum = 0.0;
-            for (int r = 0; r < NRUN; ++r) {
-                const int s = run_s[r], e = run_s[r] + run_l[r];
+            for (int r = 0; r < NR; ++r) {
+                const int s = rs[r], e = rs[r] + rp[r + 1] - rp[r];
                 for (int b0 = s; b0 < e; b0 += 32) {
                     const int p = b0 + lane;
                     bool ok = false;
@@ -356,12 +590,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
                     const uint32_t bal = __ballot_sync(0xffffffffu, ok);
                     if (ok) {
                         const double w = weight_of(rmin, d2);
-                        const int64_t k = base + pos + __popc(bal & lt_mask);
+                        const int64_t k = base + wpos + __popc(bal & lt_mask);
                         cols[k] = P.id[p];
                         vals[k] = w;
                         hsum += w;
                     }
-                    pos += __popc(bal);
+                    wpos += __popc(bal);
                 }
             }
             for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
@@ -442,6 +676,18 @@ int ceil_log2(int64_t v) {
     return b;
 }
 
+// Round a double to float toward -inf / +inf (conservative prefilter thresholds).
+float f32_down(double v) {
+    float f = (float)v;
+    if ((double)f > v) f = nextafterf(f, -INFINITY);
+    return f;
+}
+float f32_up(double v) {
+    float f = (float)v;
+    if ((double)f < v) f = nextafterf(f, INFINITY);
+    return f;
+}
+
 tf_status make_grid(const double *bb, int64_t n, int dim, double rmin, Grid *g) {
     g->dim = dim;
     g->rmin = rmin;
@@ -475,16 +721,31 @@ tf_status make_grid(const double *bb, int64_t n, int dim, double rmin, Grid *g) 
         nbins *= g->nb[d];
     }
     g->nbins = nbins;
+    // fp32 prefilter band (R4b): staged offsets from the bin centre are within
+    // M per component; |d2_f32 - d2| <= 1e-5 M^2; 1e-12 r2 covers the fp64 reference rounding.
+    const double M = 1.5 * s * (1.0 + 1e-4);
+    const double E = 1e-5 * M * M + 1e-12 * g->r2;
+    g->use_f32 = (s > 1e-15 && s < 1e15) ? 1 : 0;
+    g->t_in = (g->r2 - E > 0) ? f32_down(g->r2 - E) : -1.0f;
+    g->t_out = f32_up(g->r2 + E);
+    return TF_OK;
+}
+
+template <int DIM, int WARPS>
+tf_status launch_count(const SortedPts &P, const Grid &g, int cap, int32_t *counts, cudaStream_t s) {
+    const size_t smem = (size_t)cap * (sizeof(float4) + sizeof(int32_t));
+    // always set: dynamic + static shared memory above 48 KB needs the opt-in attribute
+    TF_CUDA_TRY(cudaFuncSetAttribute(k_count<DIM, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_count<DIM, WARPS><<<(unsigned)g.nbins, WARPS * 32, smem, s>>>(P, g, cap, counts);
+    TF_LAUNCH_CHECK();
     return TF_OK;
 }
 
 template <int DIM, int WARPS>
 tf_status launch_fill(const SortedPts &P, const Grid &g, tf_filter_s *h, int cap, int32_t *large_rows,
                       int32_t *stats, cudaStream_t s) {
-    const size_t smem = (size_t)cap * (DIM * sizeof(double) + sizeof(int32_t));
-    if (smem > 48 * 1024)
-        TF_CUDA_TRY(cudaFuncSetAttribute(k_fill<DIM, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
+    const size_t smem = (size_t)cap * FillSmem::bytes_per();
+    TF_CUDA_TRY(cudaFuncSetAttribute(k_fill<DIM, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_fill<DIM, WARPS><<<(unsigned)g.nbins, WARPS * 32, smem, s>>>(P, g, h->rowptr, h->cols, h->vals, h->hs,
                                                                    cap, large_rows, stats);
     TF_LAUNCH_CHECK();
@@ -506,7 +767,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     TF_TRY(bbd.alloc(8, s, "bbox"));
     k_bbox_partial<<<grid_n, threads, 0, s>>>(c, n, dim, part.p);
     TF_LAUNCH_CHECK();
-    k_bbox_final<<<1, 32, 0, s>>>(part.p, (int)grid_n, bbd.p);
+    k_bbox_final<<<1, 256, 0, s>>>(part.p, (int)grid_n, bbd.p);
     TF_LAUNCH_CHECK();
     double bb[7];
     TF_CUDA_TRY(cudaMemcpyAsync(bb, bbd.p, 7 * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -551,49 +812,53 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     P.id = reinterpret_cast<const int32_t *>(vs);
     P.cs = cs.p;
 
-    // a5 count
+    // largest neighbourhood -> shared-memory capacity of the count / fill passes
     DevBuf<int32_t> counts, stats;
     TF_TRY(counts.alloc(n, s, "row counts"));
     TF_TRY(stats.alloc(4, s, "build stats"));
     TF_CUDA_TRY(cudaMemsetAsync(stats.p, 0, 4 * sizeof(int32_t), s));
     {
-        const int64_t warps = g.nbins;
-        const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
-        if (dim == 3) k_count<3><<<blocks, 256, 0, s>>>(P, g, counts.p, stats.p);
-        else k_count<2><<<blocks, 256, 0, s>>>(P, g, counts.p, stats.p);
+        const unsigned blocks = (unsigned)std::min<int64_t>((g.nbins + 255) / 256, (int64_t)di.sms * 8);
+        if (dim == 3) k_binstats<3><<<blocks, 256, 0, s>>>(cs.p, g, stats.p);
+        else k_binstats<2><<<blocks, 256, 0, s>>>(cs.p, g, stats.p);
         TF_LAUNCH_CHECK();
     }
+    int32_t hstats[4];
+    TF_CUDA_TRY(cudaMemcpyAsync(hstats, stats.p, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    const int maxC = hstats[0];
+    h->info.max_candidates = maxC;
+    const int hard_cap = 3072;  // fill staging <= ~110 KB of shared memory
+    const int cap = (std::max(1, std::min(maxC, hard_cap)) + 3) & ~3;
+    const bool wide = (double)n / (double)g.nbins >= 12.0;
+
+    // a5 count
+    if (dim == 3) TF_TRY(wide ? (launch_count<3, 4>(P, g, cap, counts.p, s)) : (launch_count<3, 2>(P, g, cap, counts.p, s)));
+    else TF_TRY(wide ? (launch_count<2, 4>(P, g, cap, counts.p, s)) : (launch_count<2, 2>(P, g, cap, counts.p, s)));
 
     // a6 row pointers + nnz readback
-    TF_TRY(dalloc(&h->rowptr, n + 1, s, "rowptr"));
+    TF_TRY(dalloc(&h->rowptr, n + 3, s, "rowptr (+2 padding for 16-byte bulk copies)"));
     TF_TRY(exclusive_scan_i32_i64(counts.p, h->rowptr, n, s));
     int64_t nnz = 0;
-    int32_t hstats[4];
     TF_CUDA_TRY(cudaMemcpyAsync(&nnz, h->rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    TF_CUDA_TRY(cudaMemcpyAsync(hstats, stats.p, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     TF_CUDA_TRY(cudaStreamSynchronize(s));
     if (nnz < n || nnz < 0) {
         set_error("internal: nnz %lld < n %lld", (long long)nnz, (long long)n);
         return TF_ERR_CUDA;
     }
     h->nnz = nnz;
-    const int maxC = hstats[0];
-    h->info.max_candidates = maxC;
 
     // a7 fill
-    TF_TRY(dalloc(&h->cols, nnz, s, "cols (nnz int32)"));
-    TF_TRY(dalloc(&h->vals, nnz, s, "vals (nnz fp64)"));
+    TF_TRY(dalloc(&h->cols, nnz + 4, s, "cols (nnz int32, +4 padding for 16-byte bulk copies)"));
+    TF_TRY(dalloc(&h->vals, nnz + 4, s, "vals (nnz fp64, +4 padding)"));
     TF_TRY(dalloc(&h->hs, n, s, "Hs"));
-    const int hard_cap = (dim == 3) ? 4096 : 5632;  // <= ~112 KB of shared memory
-    const int cap = std::max(1, std::min(maxC, hard_cap));
     DevBuf<int32_t> large_rows;
     if (maxC > cap) TF_TRY(large_rows.alloc(n, s, "large-neighbourhood rows"));
-    const double avg = (double)n / (double)g.nbins;
     if (dim == 3) {
-        if (avg >= 12) TF_TRY((launch_fill<3, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
+        if (wide) TF_TRY((launch_fill<3, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
         else TF_TRY((launch_fill<3, 2>(P, g, h, cap, large_rows.p, stats.p, s)));
     } else {
-        if (avg >= 12) TF_TRY((launch_fill<2, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
+        if (wide) TF_TRY((launch_fill<2, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
         else TF_TRY((launch_fill<2, 2>(P, g, h, cap, large_rows.p, stats.p, s)));
     }
     if (maxC > cap) {

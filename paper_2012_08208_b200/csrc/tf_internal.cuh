@@ -102,6 +102,9 @@ struct Grid {
     int nb[3];      // bins per dimension (nb[2] = 1 in 2D)
     int64_t nbins;
     double rmin, r2;
+    // fp32 prefilter (R4b): d2_f32 < t_in => exact test accepts; >= t_out => rejects
+    int use_f32;
+    float t_in, t_out;
 };
 
 // ------------------------------------------------------------------ apply plan
@@ -110,6 +113,10 @@ struct ApplyPlan {
     int32_t *rb = nullptr;    // [nblocks+1] first row of each block
     int block_nnz = 0;        // target nnz per block (window)
     int stage_cap = 0;        // staged-path capacity (nnz)
+    int group = 1;            // lanes per row in the reduction phase (power of two <= 32)
+    int64_t *wlo = nullptr;   // [2*nblocks+1] aligned staging window start / end per row block
+    int grid = 0;             // persistent grid size
+    int unroll = 4;           // loads in flight per lane in the row loop (4 or 8)
 };
 
 }  // namespace tf
