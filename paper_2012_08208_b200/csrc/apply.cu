@@ -22,6 +22,8 @@
 //
 // Roofline: HBM. Algorithmic bytes per apply = 12*nnz + 8(N+1) + 32N (sensitivity) or
 // + 24N (density); gathers of x/dc hit L2/L1 (neighbour columns are index-local).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "tf_internal.cuh"
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                                                                       double *__restrict__ out,
                                                                       const int32_t *__restrict__ rb,
                                                                       const int64_t *__restrict__ wlo,
-                                                                      int64_t nwin) {
+                                                                      int64_t nwin, double *tbuf, int64_t n) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *svals = reinterpret_cast<double *>(smem_raw);                           // [kStages][kStage]
     int64_t *srow = reinterpret_cast<int64_t *>(svals + kStages * kStage);          // [kStages][kRowCap]
@@ -141,31 +143,50 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
 
     if (warp == kCW) {
         // ---------------- producer
-        if (lane == 0) {
-            uint64_t pol;
-            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-            int it = 0;
-            for (int64_t w = blockIdx.x; w < nwin; w += gridDim.x, ++it) {
-                const int st = it % kStages;
-                const int64_t a = wlo[w], n4 = wlo[w + 1 + nwin] - a;  // wlo[nwin+1+w] = aligned end
-                if (it >= kStages) mbar_wait_sleep(&empty[st], ((it / kStages) - 1) & 1);
-                next_row[st] = 0;  // published to the consumers by the full-barrier completion
-                const int r0 = rb[w], r1 = rb[w + 1];
-                const int r0a = r0 & ~1, nrow = ((r1 + 2) & ~1) - r0a;  // rowptr[r0a .. ), 16-byte aligned
-                if (n4 > 0 && n4 <= kStage && nrow <= kRowCap) {
-                    mbar_expect_tx(&full[st], (uint32_t)n4 * 12u + (uint32_t)nrow * 8u);
-                    bulk_g2s(svals + st * kStage, vals + a, (uint32_t)n4 * 8u, &full[st], pol);
-                    bulk_g2s(scols + st * kStage, cols + a, (uint32_t)n4 * 4u, &full[st], pol);
-                    bulk_g2s(srow + st * kRowCap, rowptr + r0a, (uint32_t)nrow * 8u, &full[st], pol);
-                } else {
-                    mbar_arrive(&full[st]);  // nothing staged: consumers read global memory
-                }
+        uint64_t pol = 0;
+        if (lane == 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        int it = 0;
+        int64_t w = blockIdx.x;
+        auto issue = [&](int st) {
+            const int64_t a = wlo[w], n4 = wlo[w + 1 + nwin] - a;  // wlo[nwin+1+w] = aligned end
+            next_row[st] = 0;  // published to the consumers by the full-barrier completion
+            const int r0 = rb[w], r1 = rb[w + 1];
+            const int r0a = r0 & ~1, nrow = ((r1 + 2) & ~1) - r0a;  // rowptr[r0a .. ), 16-byte aligned
+            if (n4 > 0 && n4 <= kStage && nrow <= kRowCap) {
+                mbar_expect_tx(&full[st], (uint32_t)n4 * 12u + (uint32_t)nrow * 8u);
+                bulk_g2s(svals + st * kStage, vals + a, (uint32_t)n4 * 8u, &full[st], pol);
+                bulk_g2s(scols + st * kStage, cols + a, (uint32_t)n4 * 4u, &full[st], pol);
+                bulk_g2s(srow + st * kRowCap, rowptr + r0a, (uint32_t)nrow * 8u, &full[st], pol);
+            } else {
+                mbar_arrive(&full[st]);  // nothing staged: consumers read global memory
             }
+        };
+        // prologue: the first kStages windows need no empty-wait (overlaps the t pass)
+        if (lane == 0)
+            for (; w < nwin && it < kStages; w += gridDim.x, ++it) issue(it);
+        if (SENS) {
+            __syncwarp();
+            cooperative_groups::this_grid().sync();
         }
+        if (lane == 0)
+            for (; w < nwin; w += gridDim.x, ++it) {
+                const int st = it % kStages;
+                mbar_wait_sleep(&empty[st], ((it / kStages) - 1) & 1);
+                issue(st);
+            }
         return;
     }
 
     // ---------------- consumers
+    if (SENS) {
+        // fused Hadamard pass t = x o dc (PAPER.md:447 np.multiply(density, sensitivity)),
+        // then a grid-wide barrier: the SpMV gathers one array instead of two
+        for (int64_t i = (int64_t)blockIdx.x * kThreads + tid; i < n; i += (int64_t)gridDim.x * kThreads)
+            tbuf[i] = __ldg(x + i) * __ldg(dc + i);
+        cooperative_groups::this_grid().sync();
+    }
+    // t was written in this launch: read it with plain cached loads, never the read-only path
+    const double *gsrc = SENS ? tbuf : x;
     constexpr int RPW = 32 / G;  // rows per warp claim
     const int sub = lane & (G - 1);
     int it = 0;
@@ -201,12 +222,12 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u)
-                        t[u] = (j[u] >= 0) ? (SENS ? __ldg(x + j[u]) * __ldg(dc + j[u]) : __ldg(x + j[u])) : 0.0;
+                        t[u] = (j[u] >= 0) ? __ldca(gsrc + j[u]) : 0.0;
 #pragma unroll
                     for (int u = 0; u < U; ++u) acc = fma(v[u], t[u], acc);
                     for (int i = s + sub + U * G; i < e; i += G) {  // rows longer than U*G
                         const int32_t jj = sc[i];
-                        const double tt = SENS ? __ldg(x + jj) * __ldg(dc + jj) : __ldg(x + jj);
+                        const double tt = __ldca(gsrc + jj);
                         acc = fma(sv[i], tt, acc);
                     }
                 }
@@ -226,7 +247,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                 double acc = 0.0;
                 for (int64_t k = s + lane; k < e; k += 32) {
                     const int32_t jj = cols[k];
-                    const double tt = SENS ? x[jj] * dc[jj] : x[jj];
+                    const double tt = __ldca(gsrc + jj);
                     acc = fma(vals[k], tt, acc);
                 }
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -240,16 +261,42 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
 
 template <bool SENS, int G, int U>
 tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s) {
-    const unsigned grid = (unsigned)std::min<int64_t>(h->plan.nblocks, (int64_t)h->plan.grid);
     const size_t smem = (size_t)kStages * (kStage * (sizeof(double) + sizeof(int32_t)) + kRowCap * sizeof(int64_t));
+    auto kern = k_spmv<SENS, G, U>;
     // per-instantiation attribute (dynamic shared memory above 48 KB needs the opt-in)
-    static bool attr_set = false;
-    if (!attr_set) {
-        TF_CUDA_TRY(cudaFuncSetAttribute(k_spmv<SENS, G, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
+    static int occ = 0;  // co-resident blocks per SM (a cooperative grid must not exceed it)
+    if (!occ) {
+        TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads + 32, smem));
+        if (occ < 1) {
+            set_error("apply kernel does not fit on an SM");
+            return TF_ERR_CUDA;
+        }
     }
-    k_spmv<SENS, G, U><<<grid, kThreads + 32, smem, s>>>(h->rowptr, h->cols, h->vals, h->hs, x, dc, out,
-                                                          h->plan.rb, h->plan.wlo, h->plan.nblocks);
+    const unsigned grid = (unsigned)std::min<int64_t>(
+        std::min<int64_t>(h->plan.nblocks, (int64_t)h->plan.grid), (int64_t)occ * (h->plan.grid / kBlocksPerSM));
+    const int64_t *rowptr = h->rowptr;
+    const int32_t *cols = h->cols;
+    const double *vals = h->vals, *hs = h->hs;
+    const int32_t *rb = h->plan.rb;
+    const int64_t *wlo = h->plan.wlo;
+    int64_t nwin = h->plan.nblocks, n = h->n;
+    double *tbuf = nullptr;
+    if (SENS) {
+        // per-call scratch (stream-ordered): concurrent applies on different streams stay safe
+        TF_TRY(dalloc(&tbuf, (size_t)n, s, "sensitivity scratch t = x*dc"));
+        void *args[] = {(void *)&rowptr, (void *)&cols, (void *)&vals, (void *)&hs, (void *)&x, (void *)&dc,
+                        (void *)&out, (void *)&rb, (void *)&wlo, (void *)&nwin, (void *)&tbuf, (void *)&n};
+        cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads + 32), args, smem, s);
+        count_launch();
+        dev_free(tbuf, s);
+        if (e != cudaSuccess) {
+            set_error("cooperative launch failed: %s", cudaGetErrorString(e));
+            return TF_ERR_CUDA;
+        }
+        return TF_OK;
+    }
+    kern<<<grid, kThreads + 32, smem, s>>>(rowptr, cols, vals, hs, x, dc, out, rb, wlo, nwin, tbuf, n);
     TF_LAUNCH_CHECK();
     return TF_OK;
 }
