@@ -226,6 +226,44 @@ __device__ __forceinline__ float d2_f32(const float4 &a, const float4 &b) {
     return d2;
 }
 
+// ---- packed fp32x2 arithmetic (sm_100a FADD2 / FMUL2 / FFMA2): two candidates per lane
+typedef unsigned long long f2u;
+__device__ __forceinline__ f2u f2_pack(float a, float b) {
+    return ((f2u)__float_as_uint(b) << 32) | (f2u)__float_as_uint(a);
+}
+__device__ __forceinline__ float f2_lo(f2u v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
+__device__ __forceinline__ float f2_hi(f2u v) { return __uint_as_float((unsigned)(v >> 32)); }
+__device__ __forceinline__ f2u f2_sub(f2u a, f2u b) {
+    f2u r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2u f2_mul(f2u a, f2u b) {
+    f2u r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2u f2_fma(f2u a, f2u b, f2u c) {
+    f2u r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+// d2 of two staged candidates (SoA float pairs) against the query (q?2 = (q, q)).
+// Three roundings per result, like d2_f32: the R4b error bound applies unchanged.
+template <int DIM>
+__device__ __forceinline__ f2u d2_f32x2(f2u X, f2u Y, f2u Z, f2u qx2, f2u qy2, f2u qz2) {
+    const f2u dx = f2_sub(X, qx2), dy = f2_sub(Y, qy2);
+    f2u d2;
+    if (DIM == 3) {
+        const f2u dz = f2_sub(Z, qz2);
+        d2 = f2_fma(dy, dy, f2_mul(dz, dz));
+    } else {
+        d2 = f2_mul(dy, dy);
+    }
+    return f2_fma(dx, dx, d2);
+}
+constexpr float kFar = 1e30f;  // padding coordinate: d2 overflows to +inf, never "maybe"
+
 // 3^(dim-1) contiguous x-triple ranges of a bin, computed by lanes 0..NR-1 into shared memory.
 template <int DIM>
 __device__ __forceinline__ void load_ranges(const BinView &v, const Grid &g, const int32_t *cs, int *rs, int *rp) {
@@ -267,10 +305,11 @@ __global__ void __launch_bounds__(256) k_binstats(const int32_t *__restrict__ cs
 
 // ------------------------------------------------------------------ a5: count pass
 // Block per query bin, WARPS warps, one warp per query. The bin's candidates (the 3^(dim-1)
-// contiguous x-triples) are staged once as bin-local float4 (+ sorted position for the rare
-// exact re-test); each query sweeps them 32 at a time: surely-in pairs are counted by
+// contiguous x-triples) are staged once as bin-local fp32 SoA (padded with far sentinels to
+// a multiple of 64) plus their sorted position for the rare exact re-test; each query sweeps
+// them 64 at a time, two per lane with packed f32x2 math: surely-in pairs are counted by
 // ballot/popc, band pairs are decided by the exact fp64 test. Neighbourhoods over `cap`
-// fall back to exact fp64 tests straight from the sorted SoA.
+// (or inputs where the fp32 band is unusable) fall back to exact fp64 tests from the SoA.
 template <int DIM, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_count(SortedPts P, Grid g, int cap, int32_t *__restrict__ counts) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -285,38 +324,49 @@ __global__ void __launch_bounds__(WARPS * 32) k_count(SortedPts P, Grid g, int c
     const int C = rp[NR];
     const double r2 = g.r2;
     if (C <= cap && g.use_f32) {
-        float4 *F = reinterpret_cast<float4 *>(smem_raw);
-        int32_t *POS = reinterpret_cast<int32_t *>(F + cap);
+        const int CP = (C + 63) & ~63;  // padded length
+        float *FX = reinterpret_cast<float *>(smem_raw);
+        float *FY = FX + cap;
+        float *FZ = FY + cap;
+        int32_t *POS = reinterpret_cast<int32_t *>(FZ + cap);
         for (int r = warp; r < NR; r += WARPS) {
             const int s = rs[r], off = rp[r], len = rp[r + 1] - rp[r];
             for (int i = lane; i < len; i += 32) {
                 const int p = s + i;
-                F[off + i] = local_f32(P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0, v);
+                const float4 f = local_f32(P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0, v);
+                FX[off + i] = f.x;
+                FY[off + i] = f.y;
+                FZ[off + i] = f.z;
                 POS[off + i] = p;
             }
         }
+        for (int t = C + tid; t < CP; t += WARPS * 32) FX[t] = kFar, FY[t] = kFar, FZ[t] = kFar, POS[t] = 0;
         __syncthreads();
         const float t_in = g.t_in, t_out = g.t_out;
+        const f2u *X2 = reinterpret_cast<const f2u *>(FX), *Y2 = reinterpret_cast<const f2u *>(FY),
+                  *Z2 = reinterpret_cast<const f2u *>(FZ);
         for (int q = q0 + warp; q < q1; q += WARPS) {
             const double qx = P.x[q], qy = P.y[q], qz = (DIM == 3) ? P.z[q] : 0.0;
             const float4 fq = local_f32(qx, qy, qz, v);
+            const f2u qx2 = f2_pack(fq.x, fq.x), qy2 = f2_pack(fq.y, fq.y), qz2 = f2_pack(fq.z, fq.z);
             int cnt = 0;
-            for (int t0 = 0; t0 < C; t0 += 32) {
-                const int t = t0 + lane;
-                bool in = false, band = false;
-                if (t < C) {
-                    const float d2f = d2_f32<DIM>(fq, F[t]);
-                    in = d2f < t_in;
-                    band = !in && d2f < t_out;
-                }
-                cnt += __popc(__ballot_sync(0xffffffffu, in));
-                if (__any_sync(0xffffffffu, band)) {
-                    bool ok = false;
-                    if (band) {
-                        const int p = POS[t];
-                        ok = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0) < r2;
+            for (int k = lane; k < CP / 2; k += 32) {
+                const f2u d2 = d2_f32x2<DIM>(X2[k], Y2[k], (DIM == 3) ? Z2[k] : 0ull, qx2, qy2, qz2);
+                const float d0 = f2_lo(d2), d1 = f2_hi(d2);
+                const bool in0 = d0 < t_in, in1 = d1 < t_in;
+                cnt += __popc(__ballot_sync(0xffffffffu, in0)) + __popc(__ballot_sync(0xffffffffu, in1));
+                const bool b0 = !in0 && d0 < t_out, b1 = !in1 && d1 < t_out;
+                if (__any_sync(0xffffffffu, b0 || b1)) {
+                    bool ok0 = false, ok1 = false;
+                    if (b0) {
+                        const int p = POS[2 * k];
+                        ok0 = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0) < r2;
                     }
-                    cnt += __popc(__ballot_sync(0xffffffffu, ok));
+                    if (b1) {
+                        const int p = POS[2 * k + 1];
+                        ok1 = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0) < r2;
+                    }
+                    cnt += __popc(__ballot_sync(0xffffffffu, ok0)) + __popc(__ballot_sync(0xffffffffu, ok1));
                 }
             }
             if (lane == 0) counts[P.id[q]] = cnt;
@@ -424,18 +474,20 @@ __device__ int block_radix_sort_smem(uint32_t *ka, uint32_t *va, uint32_t *kb, u
 
 // Shared-memory layout of the fill staging (36 B per candidate).
 struct FillSmem {
-    float4 *f;                      // bin-local fp32 coordinates, SORTED by id
+    float *fx, *fy, *fz;            // bin-local fp32 coordinates, SORTED by id (SoA, padded to 64)
     int32_t *pos;                   // staged sorted-SoA position (run order)
     uint32_t *ka, *va, *kb, *vb;    // sort buffers: key = id - lo, val = staging index
     __device__ FillSmem(unsigned char *raw, int cap) {
-        f = reinterpret_cast<float4 *>(raw);
-        pos = reinterpret_cast<int32_t *>(f + cap);
+        fx = reinterpret_cast<float *>(raw);
+        fy = fx + cap;
+        fz = fy + cap;
+        pos = reinterpret_cast<int32_t *>(fz + cap);
         ka = reinterpret_cast<uint32_t *>(pos + cap);
         va = ka + cap;
         kb = va + cap;
         vb = kb + cap;
     }
-    static constexpr size_t bytes_per() { return 16 + 4 + 16; }
+    static constexpr size_t bytes_per() { return 12 + 4 + 16; }
 };
 
 constexpr int kListCap = 256;  // per-warp compacted candidate list (phase A -> phase B)
@@ -531,29 +583,40 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
         const int which = block_radix_sort_smem<WARPS>(S.ka, S.va, S.kb, S.vb, C, bits, wc, wsum);
         const uint32_t *skey = which ? S.kb : S.ka;
         const uint32_t *perm = which ? S.vb : S.va;
-        for (int t = tid; t < C; t += WARPS * 32) {
-            const int p = S.pos[perm[t]];
-            S.f[t] = local_f32(P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0, v);
+        const int CP = (C + 63) & ~63;
+        for (int t = tid; t < CP; t += WARPS * 32) {
+            if (t < C) {
+                const int p = S.pos[perm[t]];
+                const float4 f = local_f32(P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0, v);
+                S.fx[t] = f.x, S.fy[t] = f.y, S.fz[t] = f.z;
+            } else {
+                S.fx[t] = kFar, S.fy[t] = kFar, S.fz[t] = kFar;
+            }
         }
         __syncthreads();
         // ---- queries: one warp each
         int32_t *list = lists[warp];
         const float t_out = g.use_f32 ? g.t_out : INFINITY;
+        const f2u *X2 = reinterpret_cast<const f2u *>(S.fx), *Y2 = reinterpret_cast<const f2u *>(S.fy),
+                  *Z2 = reinterpret_cast<const f2u *>(S.fz);
         for (int q = q0 + warp; q < q1; q += WARPS) {
             const double qx = P.x[q], qy = P.y[q], qz = (DIM == 3) ? P.z[q] : 0.0;
             const float4 fq = local_f32(qx, qy, qz, v);
+            const f2u qx2 = f2_pack(fq.x, fq.x), qy2 = f2_pack(fq.y, fq.y), qz2 = f2_pack(fq.z, fq.z);
             const int32_t qid = P.id[q];
             const int64_t base = rowptr[qid];
             int wpos = 0, nl = 0;
             double hsum = 0.0;
-            for (int t0 = 0; t0 < C; t0 += 32) {
-                const int t = t0 + lane;
-                bool maybe = false;
-                if (t < C) maybe = d2_f32<DIM>(fq, S.f[t]) < t_out;
-                const uint32_t bal = __ballot_sync(0xffffffffu, maybe);
-                if (maybe) list[nl + __popc(bal & lt_mask)] = t;
-                nl += __popc(bal);
-                if (nl > kListCap - 32) {
+            for (int k = lane; k < CP / 2; k += 32) {
+                // candidates 2k and 2k+1 (sorted order): phase A keeps every "maybe" in order
+                const f2u d2 = d2_f32x2<DIM>(X2[k], Y2[k], (DIM == 3) ? Z2[k] : 0ull, qx2, qy2, qz2);
+                const bool m0 = f2_lo(d2) < t_out, m1 = f2_hi(d2) < t_out;
+                const uint32_t b0 = __ballot_sync(0xffffffffu, m0), b1 = __ballot_sync(0xffffffffu, m1);
+                const int pre = nl + __popc(b0 & lt_mask) + __popc(b1 & lt_mask);
+                if (m0) list[pre] = 2 * k;
+                if (m1) list[pre + (m0 ? 1 : 0)] = 2 * k + 1;
+                nl += __popc(b0) + __popc(b1);
+                if (nl > kListCap - 64) {
                     __syncwarp();
                     fill_flush<DIM>(P, skey, perm, S.pos, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum,
                                     cols, vals);
@@ -733,7 +796,7 @@ tf_status make_grid(const double *bb, int64_t n, int dim, double rmin, Grid *g) 
 
 template <int DIM, int WARPS>
 tf_status launch_count(const SortedPts &P, const Grid &g, int cap, int32_t *counts, cudaStream_t s) {
-    const size_t smem = (size_t)cap * (sizeof(float4) + sizeof(int32_t));
+    const size_t smem = (size_t)cap * (3 * sizeof(float) + sizeof(int32_t));
     // always set: dynamic + static shared memory above 48 KB needs the opt-in attribute
     TF_CUDA_TRY(cudaFuncSetAttribute(k_count<DIM, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_count<DIM, WARPS><<<(unsigned)g.nbins, WARPS * 32, smem, s>>>(P, g, cap, counts);
@@ -829,7 +892,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     const int maxC = hstats[0];
     h->info.max_candidates = maxC;
     const int hard_cap = 3072;  // fill staging <= ~110 KB of shared memory
-    const int cap = (std::max(1, std::min(maxC, hard_cap)) + 3) & ~3;
+    const int cap = (std::max(1, std::min(maxC, hard_cap)) + 63) & ~63;  // multiple of 64 (packed sweeps)
     const bool wide = (double)n / (double)g.nbins >= 12.0;
 
     // a5 count
