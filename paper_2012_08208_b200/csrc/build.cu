@@ -472,32 +472,27 @@ __device__ int block_radix_sort_smem(uint32_t *ka, uint32_t *va, uint32_t *kb, u
     return which;
 }
 
-// Shared-memory layout of the fill staging (36 B per candidate).
+// Shared-memory layout of the fill staging: five 4-byte arrays of `cap` entries (20 B per
+// candidate), reused across the phases of k_fill:
+//   staging:  b[0] = sorted-SoA position (run order), (b[1], b[2]) = (key = id - lo, staging index)
+//   sort:     ping-pong between (b[1], b[2]) and (b[3], b[4])
+//   sweeps:   skey (ids - lo, sorted), sp (sorted-SoA position of sorted candidate t, written in
+//             place over perm), fx/fy/fz (bin-local fp32, sorted) in the free sort pair and b[0].
 struct FillSmem {
-    float *fx, *fy, *fz;            // bin-local fp32 coordinates, SORTED by id (SoA, padded to 64)
-    int32_t *pos;                   // staged sorted-SoA position (run order)
-    uint32_t *ka, *va, *kb, *vb;    // sort buffers: key = id - lo, val = staging index
+    uint32_t *b[5];
     __device__ FillSmem(unsigned char *raw, int cap) {
-        fx = reinterpret_cast<float *>(raw);
-        fy = fx + cap;
-        fz = fy + cap;
-        pos = reinterpret_cast<int32_t *>(fz + cap);
-        ka = reinterpret_cast<uint32_t *>(pos + cap);
-        va = ka + cap;
-        kb = va + cap;
-        vb = kb + cap;
+        for (int k = 0; k < 5; ++k) b[k] = reinterpret_cast<uint32_t *>(raw) + (size_t)k * cap;
     }
-    static constexpr size_t bytes_per() { return 12 + 4 + 16; }
+    static constexpr size_t bytes_per() { return 5 * sizeof(uint32_t); }
 };
 
-constexpr int kListCap = 256;  // per-warp compacted candidate list (phase A -> phase B)
+constexpr int kListCap = 128;  // per-warp compacted candidate list (phase A -> phase B)
 
 template <int DIM>
-__device__ __forceinline__ void fill_flush(const SortedPts &P, const uint32_t *skey, const uint32_t *perm,
-                                           const int32_t *pos, const int32_t *list, int nl, int lo,
-                                           double qx, double qy, double qz, double r2, double rmin,
-                                           int64_t base, int &wpos, double &hsum, int32_t *__restrict__ cols,
-                                           double *__restrict__ vals) {
+__device__ __forceinline__ void fill_flush(const SortedPts &P, const uint32_t *skey, const uint32_t *sp,
+                                           const int32_t *list, int nl, int lo, double qx, double qy, double qz,
+                                           double r2, double rmin, int64_t base, int &wpos, double &hsum,
+                                           int32_t *__restrict__ cols, double *__restrict__ vals) {
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     for (int e0 = 0; e0 < nl; e0 += 32) {
@@ -507,7 +502,7 @@ __device__ __forceinline__ void fill_flush(const SortedPts &P, const uint32_t *s
         int t = 0;
         if (e < nl) {
             t = list[e];
-            const int p = pos[perm[t]];
+            const int p = (int)sp[t];
             d2 = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0);
             ok = d2 < r2;
         }
@@ -536,9 +531,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int NR = (DIM == 3) ? 9 : 3;
     __shared__ int rs[NR], rp[NR + 1];
-    __shared__ int32_t wc[WARPS][256];
+    static_assert(kListCap <= 256, "lists alias the sort's digit-counter table");
+    __shared__ int32_t wc[WARPS][256];  // radix digit counters during the sort, per-warp lists after
     __shared__ int32_t wsum[WARPS];
-    __shared__ int32_t lists[WARPS][kListCap];
     __shared__ int s_lo, s_hi;
     const int64_t b = blockIdx.x;
     const int q0 = P.cs[b], q1 = P.cs[b + 1];
@@ -559,9 +554,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
             for (int i = lane; i < len; i += 32) {
                 const int p = s + i;
                 const int32_t id = P.id[p];
-                S.pos[off + i] = p;
-                S.ka[off + i] = (uint32_t)id;
-                S.va[off + i] = (uint32_t)(off + i);
+                S.b[0][off + i] = (uint32_t)p;
+                S.b[1][off + i] = (uint32_t)id;
+                S.b[2][off + i] = (uint32_t)(off + i);
                 lo = min(lo, id);
                 hi = max(hi, id);
             }
@@ -576,29 +571,34 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
         __syncthreads();
         lo = s_lo;
         hi = s_hi;
-        for (int t = tid; t < C; t += WARPS * 32) S.ka[t] -= (uint32_t)lo;
+        for (int t = tid; t < C; t += WARPS * 32) S.b[1][t] -= (uint32_t)lo;
         __syncthreads();
         // ---- sort by id (whole block)
         const int bits = (hi > lo) ? 32 - __clz((unsigned)(hi - lo)) : 0;
-        const int which = block_radix_sort_smem<WARPS>(S.ka, S.va, S.kb, S.vb, C, bits, wc, wsum);
-        const uint32_t *skey = which ? S.kb : S.ka;
-        const uint32_t *perm = which ? S.vb : S.va;
+        const int which = block_radix_sort_smem<WARPS>(S.b[1], S.b[2], S.b[3], S.b[4], C, bits, wc, wsum);
+        const uint32_t *skey = which ? S.b[3] : S.b[1];
+        uint32_t *sp = which ? S.b[4] : S.b[2];  // perm, then overwritten in place by positions
+        float *fx = reinterpret_cast<float *>(which ? S.b[1] : S.b[3]);
+        float *fy = reinterpret_cast<float *>(which ? S.b[2] : S.b[4]);
+        float *fz = reinterpret_cast<float *>(S.b[0]);
+        for (int t = tid; t < C; t += WARPS * 32) sp[t] = S.b[0][sp[t]];  // perm -> sorted-SoA position
+        __syncthreads();
         const int CP = (C + 63) & ~63;
         for (int t = tid; t < CP; t += WARPS * 32) {
             if (t < C) {
-                const int p = S.pos[perm[t]];
+                const int p = (int)sp[t];
                 const float4 f = local_f32(P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0, v);
-                S.fx[t] = f.x, S.fy[t] = f.y, S.fz[t] = f.z;
+                fx[t] = f.x, fy[t] = f.y, fz[t] = f.z;
             } else {
-                S.fx[t] = kFar, S.fy[t] = kFar, S.fz[t] = kFar;
+                fx[t] = kFar, fy[t] = kFar, fz[t] = kFar;
             }
         }
         __syncthreads();
         // ---- queries: one warp each
-        int32_t *list = lists[warp];
+        int32_t *list = wc[warp];
         const float t_out = g.use_f32 ? g.t_out : INFINITY;
-        const f2u *X2 = reinterpret_cast<const f2u *>(S.fx), *Y2 = reinterpret_cast<const f2u *>(S.fy),
-                  *Z2 = reinterpret_cast<const f2u *>(S.fz);
+        const f2u *X2 = reinterpret_cast<const f2u *>(fx), *Y2 = reinterpret_cast<const f2u *>(fy),
+                  *Z2 = reinterpret_cast<const f2u *>(fz);
         for (int q = q0 + warp; q < q1; q += WARPS) {
             const double qx = P.x[q], qy = P.y[q], qz = (DIM == 3) ? P.z[q] : 0.0;
             const float4 fq = local_f32(qx, qy, qz, v);
@@ -618,15 +618,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
                 nl += __popc(b0) + __popc(b1);
                 if (nl > kListCap - 64) {
                     __syncwarp();
-                    fill_flush<DIM>(P, skey, perm, S.pos, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum,
-                                    cols, vals);
+                    fill_flush<DIM>(P, skey, sp, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum, cols, vals);
                     __syncwarp();
                     nl = 0;
                 }
             }
             __syncwarp();
-            fill_flush<DIM>(P, skey, perm, S.pos, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum, cols,
-                            vals);
+            fill_flush<DIM>(P, skey, sp, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum, cols, vals);
             __syncwarp();
             for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
             if (lane == 0) hs[qid] = hsum;
