@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtopofilt.so")
+LIB_PATH = os.environ.get("TOPOFILT_LIB") or os.path.join(_HERE, "libtopofilt.so")  # override: tuning variants
 
 TF_OK, TF_ERR_INVALID, TF_ERR_NOMEM, TF_ERR_CUDA, TF_ERR_OVERFLOW = range(5)
 _STATUS = {0: "TF_OK", 1: "TF_ERR_INVALID", 2: "TF_ERR_NOMEM", 3: "TF_ERR_CUDA", 4: "TF_ERR_OVERFLOW"}

@@ -24,6 +24,8 @@
 // + 24N (density); gathers of x/dc hit L2/L1 (neighbour columns are index-local).
 #include <cooperative_groups.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "tf_internal.cuh"
@@ -31,13 +33,31 @@
 namespace tf {
 namespace {
 
-constexpr int kCW = 12;                   // consumer warps per block (+1 producer warp)
+#ifndef TF_APPLY_CW
+#define TF_APPLY_CW 10
+#endif
+#ifndef TF_APPLY_BPS
+#define TF_APPLY_BPS 3
+#endif
+#ifndef TF_APPLY_STAGES
+#define TF_APPLY_STAGES 2
+#endif
+constexpr int kCW = TF_APPLY_CW;          // consumer warps per block (+1 producer warp)
 constexpr int kThreads = kCW * 32;        // consumer threads
-constexpr int kWindow = 1792;             // target nnz per window (row block)
-constexpr int kStage = 2560;              // staged nnz capacity per stage (multiple of 4): 30 KB
-constexpr int kRowCap = 512;              // staged rowptr capacity per stage (int64, multiple of 2): 4 KB
-constexpr int kStages = 3;                // TMA ring depth per block
-constexpr int kBlocksPerSM = 2;           // persistent grid = kBlocksPerSM x SMs
+#ifndef TF_APPLY_WINDOW
+#define TF_APPLY_WINDOW 2048
+#endif
+#ifndef TF_APPLY_STAGE
+#define TF_APPLY_STAGE 2816
+#endif
+#ifndef TF_APPLY_ROWCAP
+#define TF_APPLY_ROWCAP 256
+#endif
+constexpr int kWindow = TF_APPLY_WINDOW;  // target nnz per window (row block)
+constexpr int kStage = TF_APPLY_STAGE;    // staged nnz capacity per stage (multiple of 4): 33 KB
+constexpr int kRowCap = TF_APPLY_ROWCAP;  // staged rowptr capacity per stage (int64, multiple of 2): 2 KB
+constexpr int kStages = TF_APPLY_STAGES;  // TMA ring depth per block
+constexpr int kBlocksPerSM = TF_APPLY_BPS;  // persistent grid = kBlocksPerSM x SMs (tuned on c5: 10 x 3 x 2 x 2048)
 
 __global__ void k_plan(const int64_t *__restrict__ rowptr, int64_t n, int64_t nblocks, int32_t *__restrict__ rb) {
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nblocks;
@@ -351,9 +371,15 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
     // unroll U so that U*G covers ~1.25x the average row in one batch of loads
     const double avg = (double)h->nnz / (double)std::max<int64_t>(1, h->n);
     int g = 1;
-    while (g < 32 && 6.0 * g < avg) g *= 2;
+    while (g < 32 && 12.0 * g < avg) g *= 2;  // measured best at c5 (avg 86): G = 8, U = 4
     h->plan.group = g;
-    h->plan.unroll = (1.25 * avg > 4.0 * g) ? 8 : 4;
+    h->plan.unroll = (g >= 8) ? 4 : 8;
+    // tuning knobs (benchmarks only): TOPOFILT_APPLY_G in {1..32, power of two}, TOPOFILT_APPLY_U in {4, 8}
+    if (const char *e = getenv("TOPOFILT_APPLY_G")) {
+        const int v = atoi(e);
+        if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) h->plan.group = v;
+    }
+    if (const char *e = getenv("TOPOFILT_APPLY_U")) h->plan.unroll = atoi(e) >= 8 ? 8 : 4;
     const unsigned grid = (unsigned)std::min<int64_t>((nblocks + 256) / 256, 65535);
     k_plan<<<grid, 256, 0, s>>>(h->rowptr, h->n, nblocks, h->plan.rb);
     TF_LAUNCH_CHECK();
