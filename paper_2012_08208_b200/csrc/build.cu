@@ -46,8 +46,12 @@ __device__ __forceinline__ double pair_d2(double ax, double ay, double az, doubl
     return d2;
 }
 
+// w = max(0, rmin - sqrt(d2)). d2 == 0 (every row's diagonal) sits outside the fast range of
+// the correctly rounded sqrt sequence and would send the whole warp through its slow-path
+// call once per row; sqrt(0) = 0 exactly, so feed it a safe argument and select rmin.
 __device__ __forceinline__ double weight_of(double rmin, double d2) {
-    double w = __dsub_rn(rmin, __dsqrt_rn(d2));
+    const double r = __dsqrt_rn(d2 > 0.0 ? d2 : 1.0);
+    double w = (d2 > 0.0) ? __dsub_rn(rmin, r) : rmin;
     return w < 0.0 ? 0.0 : w;
 }
 
@@ -350,7 +354,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_count(SortedPts P, Grid g, int c
             const float4 fq = local_f32(qx, qy, qz, v);
             const f2u qx2 = f2_pack(fq.x, fq.x), qy2 = f2_pack(fq.y, fq.y), qz2 = f2_pack(fq.z, fq.z);
             int cnt = 0;
-            for (int k = lane; k < CP / 2; k += 32) {
+            for (int k0 = 0; k0 < CP / 2; k0 += 32) {  // warp-uniform trip count
+                const int k = k0 + lane;
                 const f2u d2 = d2_f32x2<DIM>(X2[k], Y2[k], (DIM == 3) ? Z2[k] : 0ull, qx2, qy2, qz2);
                 const float d0 = f2_lo(d2), d1 = f2_hi(d2);
                 const bool in0 = d0 < t_in, in1 = d1 < t_in;
@@ -607,7 +612,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
             const int64_t base = rowptr[qid];
             int wpos = 0, nl = 0;
             double hsum = 0.0;
-            for (int k = lane; k < CP / 2; k += 32) {
+            for (int k0 = 0; k0 < CP / 2; k0 += 32) {  // warp-uniform trip count
+                const int k = k0 + lane;
                 // candidates 2k and 2k+1 (sorted order): phase A keeps every "maybe" in order
                 const f2u d2 = d2_f32x2<DIM>(X2[k], Y2[k], (DIM == 3) ? Z2[k] : 0ull, qx2, qy2, qz2);
                 const bool m0 = f2_lo(d2) < t_out, m1 = f2_hi(d2) < t_out;

@@ -1,0 +1,90 @@
+#!/usr/bin/env python3
+"""Per-config measurements (BASELINE.json: "report ... on the seeded synthetic centroid
+sets"): build nnz/s and GB/s, sensitivity / density apply GB/s and iterations/s, each as a
+fraction of the 8 TB/s HBM roofline, for configs 1-5 on one B200.
+
+Timing: CUDA events on the launching stream, warm-up first, median of the repetitions.
+"hot" = back-to-back repetitions (small configs stay L2-resident); "cold" = a 512 MB buffer
+is written between repetitions to flush the 126 MB L2. Writes JSON to stdout.
+"""
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import synth  # noqa: E402
+import paper_2012_08208_b200 as tf  # noqa: E402
+
+HBM = 8000.0
+
+
+def timed(fn, reps, flush=None, stream=None):
+    s = stream or torch.cuda.current_stream()
+    out = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.add_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        out.append(a.elapsed_time(b) / 1e3)
+    return statistics.median(out)
+
+
+def main():
+    dev = torch.device("cuda:0")
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float64, device=dev)  # 512 MB
+    res = []
+    for cfg in (1, 2, 3, 4, 5):
+        c, x, dc, rmin, meta = bench.load_workload(cfg)
+        n, dim = c.shape
+        cd, xd, dcd = (torch.from_numpy(a).to(dev) for a in (c, x, dc))
+        out = torch.empty_like(xd)
+        f = tf.tf_build_filter(cd, rmin)
+        nnz = f.nnz
+        f.close()
+        reps_b = 5 if cfg < 5 else 3
+
+        def build():
+            g = tf.tf_build_filter(cd, rmin)
+            g.close()
+
+        t_build = timed(build, reps_b)
+        f = tf.tf_build_filter(cd, rmin)
+        for _ in range(3):
+            f.sensitivity(xd, dcd, out=out)
+            f.density(xd, out=out)
+        torch.cuda.synchronize()
+        reps = 50 if cfg < 5 else 20
+        row = {"config": cfg, "workload": meta["name"], "n": n, "nnz": nnz, "rmin": rmin,
+               "build_ms": t_build * 1e3, "build_nnz_per_s": nnz / t_build,
+               "build_gbs": bench.build_bytes(n, nnz, dim) / t_build / 1e9}
+        row["build_frac_8tbs"] = row["build_gbs"] / HBM
+        for mode, fl in (("hot", None), ("cold", flush)):
+            ts = timed(lambda: f.sensitivity(xd, dcd, out=out), reps, fl)
+            td = timed(lambda: f.density(xd, out=out), reps, fl)
+            row[f"sens_us_{mode}"] = ts * 1e6
+            row[f"sens_gbs_{mode}"] = bench.sens_bytes(n, nnz) / ts / 1e9
+            row[f"dens_us_{mode}"] = td * 1e6
+            row[f"dens_gbs_{mode}"] = bench.dens_bytes(n, nnz) / td / 1e9
+            row[f"sens_frac_8tbs_{mode}"] = row[f"sens_gbs_{mode}"] / HBM
+            row[f"dens_frac_8tbs_{mode}"] = row[f"dens_gbs_{mode}"] / HBM
+            row[f"iters_per_s_{mode}"] = 1.0 / (ts + td)
+        row["stats"] = f.stats()
+        f.close()
+        res.append(row)
+        print(json.dumps(row), flush=True)
+        del cd, xd, dcd, out
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
