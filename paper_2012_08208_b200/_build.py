@@ -51,6 +51,11 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     return target
 
 
+def build_debug() -> str:
+    """Variant with device-side bounds checks (TF_DCHECK -> __trap); load it with TOPOFILT_LIB."""
+    return build(defines=("TF_DEBUG_CHECKS",), out=os.path.join(HERE, "..", "build_variants", "libtopofilt_debug.so"))
+
+
 if __name__ == "__main__":
     import sys
     print(build(force=True, verbose="-v" in sys.argv))

@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                     const int r = r0 + rr;
                     if (sub == 0) hs_r = hs[r], x_r = x[r];  // epilogue operands, issued early
                     const int s = (int)(sr[rr] - a), e = (int)(sr[rr + 1] - a);
+                    TF_DCHECK(s >= 0 && s <= e && e <= (int)n4);
                     int32_t j[U];
                     double v[U], t[U];
 #pragma unroll

@@ -467,6 +467,7 @@ __device__ int block_radix_sort_smem(uint32_t *ka, uint32_t *va, uint32_t *kb, u
             __syncwarp();
             if (valid) {
                 const int dst = before + __popc(peers & lt);
+                TF_DCHECK(dst >= 0 && dst < C);
                 ko[dst] = key;
                 vo[dst] = val;
             }
@@ -515,6 +516,7 @@ __device__ __forceinline__ void fill_flush(const SortedPts &P, const uint32_t *s
         if (ok) {
             const double w = weight_of(rmin, d2);
             const int64_t k = base + wpos + __popc(bal & lt);
+            TF_DCHECK(t >= 0 && (int)sp[t] >= 0);
             cols[k] = (int32_t)skey[t] + lo;
             vals[k] = w;
             hsum += w;
@@ -619,6 +621,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
                 const bool m0 = f2_lo(d2) < t_out, m1 = f2_hi(d2) < t_out;
                 const uint32_t b0 = __ballot_sync(0xffffffffu, m0), b1 = __ballot_sync(0xffffffffu, m1);
                 const int pre = nl + __popc(b0 & lt_mask) + __popc(b1 & lt_mask);
+                TF_DCHECK(pre + 1 < kListCap || !(m0 || m1));
                 if (m0) list[pre] = 2 * k;
                 if (m1) list[pre + (m0 ? 1 : 0)] = 2 * k + 1;
                 nl += __popc(b0) + __popc(b1);
@@ -633,7 +636,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
             fill_flush<DIM>(P, skey, sp, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum, cols, vals);
             __syncwarp();
             for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
-            if (lane == 0) hs[qid] = hsum;
+            if (lane == 0) {
+                hs[qid] = hsum;
+                // the fill must write exactly the row length the count pass produced
+                if (base + wpos != rowptr[qid + 1]) atomicOr(&stats[2], 1);
+            }
         }
     } else {
         // ---- large neighbourhood: exact tests straight from the sorted SoA, written in
@@ -668,6 +675,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
             for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
             if (lane == 0) {
                 hs[qid] = hsum;
+                if (base + wpos != rowptr[qid + 1]) atomicOr(&stats[2], 1);
                 const int slot = atomicAdd(&stats[1], 1);
                 large_rows[slot] = qid;
             }
@@ -801,9 +809,10 @@ tf_status make_grid(const double *bb, int64_t n, int dim, double rmin, Grid *g) 
 template <int DIM, int WARPS>
 tf_status launch_count(const SortedPts &P, const Grid &g, int cap, int32_t *counts, cudaStream_t s) {
     const size_t smem = (size_t)cap * (3 * sizeof(float) + sizeof(int32_t));
+    auto kern = k_count<DIM, WARPS>;
     // always set: dynamic + static shared memory above 48 KB needs the opt-in attribute
-    TF_CUDA_TRY(cudaFuncSetAttribute(k_count<DIM, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_count<DIM, WARPS><<<(unsigned)g.nbins, WARPS * 32, smem, s>>>(P, g, cap, counts);
+    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)g.nbins, WARPS * 32, smem, s>>>(P, g, cap, counts);
     TF_LAUNCH_CHECK();
     return TF_OK;
 }
@@ -935,10 +944,16 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
         k_rowsort<<<(unsigned)di.sms * 2, kSortThreads, smem, s>>>(large_rows.p, stats.p, h->rowptr, h->cols,
                                                                     h->vals, scap);
         TF_LAUNCH_CHECK();
-        int32_t nl = 0;
-        TF_CUDA_TRY(cudaMemcpyAsync(&nl, stats.p + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        TF_CUDA_TRY(cudaStreamSynchronize(s));
-        h->info.large_rows = nl;
+    }
+    // stats[1] = rows that took the large-neighbourhood path; stats[2] = count/fill disagreement
+    // flag (always-on invariant: every row's fill writes exactly its counted length)
+    int32_t tail[2] = {0, 0};
+    TF_CUDA_TRY(cudaMemcpyAsync(tail, stats.p + 1, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    h->info.large_rows = tail[0];
+    if (tail[1] != 0) {
+        set_error("internal: fill pass disagreed with the count pass (row lengths)");
+        return TF_ERR_CUDA;
     }
     return TF_OK;
 }

@@ -49,6 +49,22 @@ struct Status {  // lightweight status carrier for host orchestration
         if (_s != TF_OK) return _s;                                                       \
     } while (0)
 
+// Device-side bounds/invariant checks, compiled in only for the debug variant
+// (`-DTF_DEBUG_CHECKS`, built by _build.py build_debug(); compute-sanitizer is unavailable).
+#ifdef TF_DEBUG_CHECKS
+#define TF_DCHECK(cond)                                                                   \
+    do {                                                                                  \
+        if (!(cond)) {                                                                    \
+            printf("TF_DCHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);          \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+#else
+#define TF_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 // ------------------------------------------------------------------ memory
 // Stream-ordered device allocation with the test-only allocation limit.
 tf_status dev_alloc(void **p, size_t bytes, cudaStream_t s, const char *what);
