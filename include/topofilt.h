@@ -94,6 +94,25 @@ typedef struct {
 TF_API tf_status tf_build_filter(const double *centroids, int64_t n, int dim, double rmin,
                           void *stream, tf_filter *out);
 
+/*
+ * tf_build_stencil -- matrix-free filter for a regular grid (
+ * BASELINE.json north_star "matrix-free stencil variant for structured grids").
+ *   Cells are indexed (k*ny + j)*nx + i with centroid ((i+1/2)h, (j+1/2)h, (k+1/2)h)
+ *   (any common origin); dim = 2 ignores nz. The weight of an integer offset (a,b,c) is
+ *   w = max(0, rmin - sqrt(d2)), d2 = ((a h)^2 + (b h)^2) + (c h)^2 < rmin^2 (the CSR build's
+ *   expression; identical H for dyadic h such as the configs' h = 1). Row sums use the
+ *   in-grid neighbours only (boundary truncation), like the CSR.
+ *   The handle supports tf_sensitivity_filter / tf_density_filter (+ *_host) and
+ *   tf_build_stats; tf_filter_view returns TF_ERR_INVALID (no CSR is stored). tf_filter_nnz gives the
+ *   nnz of the equivalent CSR (for CSR-equivalent bandwidth figures).
+ * Errors: TF_ERR_INVALID (dim, sizes, rmin/h not finite > 0, more than 4096 offsets).
+ */
+TF_API tf_status tf_build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, double rmin,
+                                  void *stream, tf_filter *out);
+
+/* tf_filter_nnz -- stored entries of a CSR filter, or those of the equivalent CSR of a stencil. */
+TF_API int64_t tf_filter_nnz(tf_filter h);
+
 /* tf_filter_view -- borrowed device pointers of the CSR and Hs (no copy). */
 TF_API tf_status tf_filter_view(tf_filter h, tf_view *v);
 

@@ -27,7 +27,7 @@ EXPORTS = [
     "tf_build_filter", "tf_filter_view", "tf_build_stats", "tf_sensitivity_filter", "tf_density_filter",
     "tf_free", "tf_last_error", "tf_build_filter_host", "tf_sensitivity_filter_host",
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
-    "tf_version",
+    "tf_version", "tf_build_stencil", "tf_filter_nnz",
 ]
 
 
@@ -71,6 +71,8 @@ def _load():
         "tf_kernel_launches": ([], ctypes.c_uint64),
         "tf_debug_set_alloc_limit": ([ctypes.c_uint64], None),
         "tf_version": ([], I32),
+        "tf_build_stencil": ([I32, I64, I64, I64, D, D, P, PP], I32),
+        "tf_filter_nnz": ([P], I64),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -124,9 +126,15 @@ class _CudaArray:
 class Filter:
     """A built filter (owns a tf_filter handle). Immutable; applies are stream-ordered."""
 
-    def __init__(self, handle: ctypes.c_void_p, keepalive=None):
+    def __init__(self, handle: ctypes.c_void_p, keepalive=None, stencil=None):
         self._h = handle
         self._keep = keepalive
+        self.is_stencil = stencil is not None
+        if self.is_stencil:  # matrix-free: no CSR view
+            self.dim, self.rmin, self.n = stencil
+            self.nnz = int(_lib.tf_filter_nnz(self._h))
+            self._v = None
+            return
         v = tf_view()
         _check(_lib.tf_filter_view(self._h, ctypes.byref(v)))
         self.n, self.nnz, self.dim, self.rmin = v.n, v.nnz, v.dim, v.rmin
@@ -205,6 +213,15 @@ def tf_build_filter(centroids, rmin: float, stream=None) -> Filter:
     _check(_lib.tf_build_filter(_dptr(centroids, "centroids", torch.float64), n, dim, float(rmin),
                                 _stream_ptr(stream), ctypes.byref(h)))
     return Filter(h)
+
+
+def tf_build_stencil(dim: int, nx: int, ny: int, nz: int, h: float, rmin: float, stream=None) -> Filter:
+    """Matrix-free filter on a regular grid (row a10): cells (k*ny + j)*nx + i, spacing h."""
+    hnd = ctypes.c_void_p()
+    _check(_lib.tf_build_stencil(int(dim), int(nx), int(ny), int(nz), float(h), float(rmin), _stream_ptr(stream),
+                                 ctypes.byref(hnd)))
+    n = int(nx) * int(ny) * (int(nz) if dim == 3 else 1)
+    return Filter(hnd, stencil=(int(dim), float(rmin), n))
 
 
 def tf_build_filter_host(centroids: np.ndarray, rmin: float, stream=None) -> Filter:

@@ -102,6 +102,8 @@ static void destroy(tf_filter_s *h) {
     if (h->hs) cudaFreeAsync(h->hs, 0);
     if (h->plan.rb) cudaFreeAsync(h->plan.rb, 0);
     if (h->plan.wlo) cudaFreeAsync(h->plan.wlo, 0);
+    if (h->stencil_off) cudaFreeAsync(h->stencil_off, 0);
+    if (h->stencil_w) cudaFreeAsync(h->stencil_w, 0);
     cudaFree(h->hx);
     cudaFree(h->hdc);
     cudaFree(h->hout);
@@ -202,9 +204,52 @@ tf_status tf_build_filter_host(const double *centroids_host, int64_t n, int dim,
     }
 }
 
+tf_status tf_build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, double rmin, void *stream,
+                           tf_filter *out) {
+    try {
+        if (!out) {
+            set_error("out is NULL");
+            return TF_ERR_INVALID;
+        }
+        *out = nullptr;
+        if (dim != 2 && dim != 3) {
+            set_error("dim must be 2 or 3 (got %d)", dim);
+            return TF_ERR_INVALID;
+        }
+        const int64_t nzz = (dim == 3) ? nz : 1;
+        if (nx < 1 || ny < 1 || nzz < 1 || nx * ny * nzz >= (int64_t)0x7fffffff) {
+            set_error("grid dimensions must be >= 1 with nx*ny*nz < 2^31-1");
+            return TF_ERR_INVALID;
+        }
+        if (!isfinite(rmin) || !(rmin > 0.0) || !isfinite(h) || !(h > 0.0)) {
+            set_error("rmin and h must be finite and > 0");
+            return TF_ERR_INVALID;
+        }
+        tf_filter_s *f = new (std::nothrow) tf_filter_s();
+        if (!f) return TF_ERR_NOMEM;
+        f->n = nx * ny * nzz;
+        f->dim = dim;
+        f->rmin = rmin;
+        tf_status st = build_stencil(dim, nx, ny, nzz, h, rmin, (cudaStream_t)stream, f);
+        if (st != TF_OK) {
+            destroy(f);
+            return st;
+        }
+        *out = f;
+        return TF_OK;
+    } catch (...) {
+        set_error("tf_build_stencil: unexpected host exception");
+        return TF_ERR_NOMEM;
+    }
+}
+
 tf_status tf_filter_view(tf_filter h, tf_view *v) {
     if (!h || !v) {
         set_error("tf_filter_view: NULL argument");
+        return TF_ERR_INVALID;
+    }
+    if (h->stencil.K > 0) {
+        set_error("tf_filter_view: a stencil filter stores no CSR (build it with tf_build_filter)");
         return TF_ERR_INVALID;
     }
     v->n = h->n;
@@ -352,6 +397,8 @@ tf_status tf_filter_from_csr(const int64_t *rowptr_host, const int32_t *cols_hos
     *out = h;
     return TF_OK;
 }
+
+int64_t tf_filter_nnz(tf_filter h) { return h ? h->nnz : -1; }
 
 void tf_free(tf_filter h) { destroy(h); }
 

@@ -1,0 +1,182 @@
+// stencil.cu -- matrix-free filter apply for regular grids (BASELINE.json
+// north_star: "a matrix-free stencil variant for structured grids, kept only if ncu shows it
+// beats stored CSR").
+//
+// For cells on a regular grid (index (k*ny + j)*nx + i, centroid origin + ((i,j,k)+1/2)*h) the
+// weight of Eq. filter_cond depends only on the integer offset (a,b,c):
+//   d2 = ((a*h)*(a*h) + (b*h)*(b*h)) + (c*h)*(c*h)  (same fp64 expression and order as the CSR
+//   build; exact for the configs' h = 1), stored iff d2 < rmin^2, w = max(0, rmin - sqrt(d2)),
+// so H never needs to be stored: out_i = sum_o w_o t[i + o] over in-grid neighbours, and
+// Hs_i = sum_o w_o over the same neighbours (boundary truncation), recomputed on the fly.
+// HBM traffic per apply: x and dc read once, out written once (24 N bytes for the
+// sensitivity filter, 16 N for density) instead of 12 nnz + ... for the CSR.
+//
+// Kernel: one block per (32 x TY x TZ) tile; the block stages t = x*dc (or x) of the tile
+// plus its halo of radius R in shared memory with coalesced loads, then each thread sums its
+// cell's K offsets from shared memory (offset table: handle-owned device memory, broadcast reads).
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "tf_internal.cuh"
+
+namespace tf {
+namespace {
+
+constexpr int kMaxOffsets = 4096;
+
+constexpr int kTX = 32;
+
+// RC = compile-time halo radius (1..4) or 0 for a runtime radius (general fallback)
+template <bool SENS, int DIM, int RC>
+__global__ void __launch_bounds__(256) k_stencil(StencilGeom sg, const int4 *__restrict__ offs,
+                                                 const double *__restrict__ wts, const double *__restrict__ x,
+                                                 const double *__restrict__ dc, double *__restrict__ out) {
+    extern __shared__ double tile[];
+    constexpr int TY = (DIM == 3) ? 4 : 8, TZ = (DIM == 3) ? 2 : 1;
+    const int R = RC ? RC : sg.R;
+    const int HX = kTX + 2 * R, HY = TY + 2 * R, HZ = (DIM == 3) ? TZ + 2 * R : 1;
+    const int bx0 = blockIdx.x * kTX, by0 = blockIdx.y * TY, bz0 = (DIM == 3) ? blockIdx.z * TZ : 0;
+    const int nx = (int)sg.nx, ny = (int)sg.ny, nz = (int)sg.nz;
+    // stage t over the haloed tile, one x-row per warp iteration (coalesced; no divisions), and
+    // a 0/1 in-grid mask: out-of-grid neighbours then contribute fma(w, 0, .) = exactly nothing,
+    // so every cell runs the same branch-free loop and the truncated Hs is bitwise the checked sum
+    const int rows = HY * HZ;
+    double *mask = tile + rows * HX;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int row = warp; row < rows; row += 8) {
+        const int hy = row % HY, hz = row / HY;
+        const int gy = by0 + hy - R, gz = (DIM == 3) ? bz0 + hz - R : 0;
+        const bool rok = gy >= 0 && gy < ny && gz >= 0 && gz < nz;
+        const int64_t rbase = ((int64_t)gz * ny + gy) * nx;
+        for (int hx = lane; hx < HX; hx += 32) {
+            const int gx = bx0 + hx - R;
+            double t = 0.0, m = 0.0;
+            if (rok && gx >= 0 && gx < nx) {
+                const int64_t g = rbase + gx;
+                t = SENS ? __ldg(x + g) * __ldg(dc + g) : __ldg(x + g);
+                m = 1.0;
+            }
+            tile[row * HX + hx] = t;
+            mask[row * HX + hx] = m;
+        }
+    }
+    // offset table -> shared memory as tile-index deltas
+    int *s_delta = reinterpret_cast<int *>(mask + rows * HX);
+    double *s_w = reinterpret_cast<double *>(s_delta + ((sg.K + 1) & ~1));
+    for (int o = threadIdx.x; o < sg.K; o += 256) {
+        const int4 off = __ldg(offs + o);
+        s_delta[o] = ((DIM == 3) ? off.z * HY * HX : 0) + off.y * HX + off.x;
+        s_w[o] = __ldg(wts + o);
+    }
+    __syncthreads();
+    // one cell per thread: (lx, ly, lz) = (threadIdx.x % 32, ...)
+    const int lx = threadIdx.x & 31, ly = (threadIdx.x >> 5) % TY, lz = (threadIdx.x >> 5) / TY;
+    const int gx = bx0 + lx, gy = by0 + ly, gz = bz0 + lz;
+    if (gx >= nx || gy >= ny || gz >= nz) return;
+    const int center = (((DIM == 3) ? lz + R : 0) * HY + (ly + R)) * HX + (lx + R);
+    double acc = 0.0, hs = 0.0;
+#pragma unroll 9
+    for (int o = 0; o < sg.K; ++o) {
+        const double w = s_w[o];
+        const int si = center + s_delta[o];
+        acc = fma(w, tile[si], acc);
+        hs = fma(w, mask[si], hs);  // w*1 = w and w*0 = 0 exactly: the offset-order in-grid sum
+    }
+    const int64_t g = ((int64_t)gz * ny + gy) * nx + gx;
+    out[g] = SENS ? acc / (hs * fmax(1e-3, __ldg(x + g))) : acc / hs;
+}
+
+}  // namespace
+
+tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, double rmin, cudaStream_t s,
+                        tf_filter_s *f) {
+    // integer offsets with the pair test of the CSR build (d2 < rmin^2, same fp64 expression)
+    const double r2 = rmin * rmin;
+    const int R = (int)floor(rmin / h) + 1;
+    std::vector<int4> off;
+    std::vector<double> w;
+    const int zr = (dim == 3) ? R : 0;
+    for (int c = -zr; c <= zr; ++c)
+        for (int b = -R; b <= R; ++b)
+            for (int a = -R; a <= R; ++a) {
+                const volatile double dx = (double)a * h, dy = (double)b * h, dz = (double)c * h;
+                const volatile double dxx = dx * dx, dyy = dy * dy, dzz = dz * dz;
+                const volatile double s2 = dxx + dyy;
+                const double d2 = (dim == 3) ? (double)(s2 + dzz) : (double)s2;
+                if (!(d2 < r2)) continue;
+                const volatile double sq = sqrt(d2);
+                double ww = rmin - sq;
+                if (ww < 0) ww = 0;
+                off.push_back(make_int4(a, b, c, 0));
+                w.push_back(ww);
+            }
+    if ((int)off.size() > kMaxOffsets) {
+        set_error("stencil radius too large (%zu offsets > %d); use tf_build_filter", off.size(), kMaxOffsets);
+        return TF_ERR_INVALID;
+    }
+    int Rk = 0;
+    for (const int4 &o : off) Rk = std::max(Rk, std::max(abs(o.x), std::max(abs(o.y), abs(o.z))));
+    const size_t halo = 2 * sizeof(double) * (size_t)(32 + 2 * Rk) * ((dim == 3 ? 4 : 8) + 2 * Rk) * (dim == 3 ? 2 + 2 * Rk : 1);
+    if (halo + 12 * off.size() > 200 * 1024) {
+        set_error("stencil halo tile too large for shared memory (rmin/h too big); use tf_build_filter");
+        return TF_ERR_INVALID;
+    }
+    StencilGeom &sg = f->stencil;
+    sg.dim = dim;
+    sg.nx = nx, sg.ny = ny, sg.nz = (dim == 3) ? nz : 1;
+    sg.R = Rk;
+    sg.K = (int)off.size();
+    sg.ty = (dim == 3) ? 4 : 8;  // must match the kernel's TY/TZ
+    sg.tz = (dim == 3) ? 2 : 1;
+    sg.h = h;
+    double hs_full = 0.0;
+    for (double ww : w) hs_full += ww;  // full-stencil row sum (diagnostic)
+    sg.hs_full = hs_full;
+    // handle-owned device copy of the offset table (read-only; concurrent applies are safe)
+    TF_TRY(dalloc(&f->stencil_off, off.size(), s, "stencil offsets"));
+    TF_TRY(dalloc(&f->stencil_w, w.size(), s, "stencil weights"));
+    TF_CUDA_TRY(cudaMemcpyAsync(f->stencil_off, off.data(), sizeof(int4) * off.size(), cudaMemcpyHostToDevice, s));
+    TF_CUDA_TRY(cudaMemcpyAsync(f->stencil_w, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    // nnz of the equivalent CSR: every offset times the cells whose neighbour is in the grid
+    int64_t nnz = 0;
+    for (const int4 &o : off)
+        nnz += std::max<int64_t>(0, nx - abs(o.x)) * std::max<int64_t>(0, ny - abs(o.y)) *
+               std::max<int64_t>(0, sg.nz - abs(o.z));
+    f->nnz = nnz;
+    return TF_OK;
+}
+
+tf_status launch_stencil(const tf_filter_s *f, const double *x, const double *dc, double *out, bool sens,
+                         cudaStream_t s) {
+    const StencilGeom &sg = f->stencil;
+    const int TY = sg.ty, TZ = (sg.dim == 3) ? sg.tz : 1, R = sg.R;
+    const size_t smem = 2 * sizeof(double) * (size_t)(kTX + 2 * R) * (TY + 2 * R) * ((sg.dim == 3) ? TZ + 2 * R : 1) +
+                        sizeof(int) * ((sg.K + 1) & ~1) + sizeof(double) * sg.K;
+    dim3 grid((unsigned)((sg.nx + kTX - 1) / kTX), (unsigned)((sg.ny + TY - 1) / TY),
+              (unsigned)((sg.dim == 3) ? (sg.nz + TZ - 1) / TZ : 1));
+    auto go = [&](auto kern) -> tf_status {
+        TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, 256, smem, s>>>(sg, f->stencil_off, f->stencil_w, x, dc, out);
+        TF_LAUNCH_CHECK();
+        return TF_OK;
+    };
+#define TF_ST_R(D, RR)                                                                          \
+    case RR:                                                                                    \
+        return sens ? go(k_stencil<true, D, RR>) : go(k_stencil<false, D, RR>);
+    if (sg.dim == 3) {
+        switch (R) {
+            TF_ST_R(3, 1) TF_ST_R(3, 2) TF_ST_R(3, 3) TF_ST_R(3, 4)
+            default: return sens ? go(k_stencil<true, 3, 0>) : go(k_stencil<false, 3, 0>);
+        }
+    }
+    switch (R) {
+        TF_ST_R(2, 1) TF_ST_R(2, 2) TF_ST_R(2, 3) TF_ST_R(2, 4)
+        default: return sens ? go(k_stencil<true, 2, 0>) : go(k_stencil<false, 2, 0>);
+    }
+#undef TF_ST_R
+}
+
+}  // namespace tf

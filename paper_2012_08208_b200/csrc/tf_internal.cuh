@@ -135,6 +135,17 @@ struct ApplyPlan {
     int unroll = 4;           // loads in flight per lane in the row loop (4 or 8)
 };
 
+// ------------------------------------------------------------------ matrix-free stencil (a10)
+struct StencilGeom {
+    int dim = 0;
+    int64_t nx = 0, ny = 0, nz = 0;
+    int R = 0;      // largest |offset| component
+    int K = 0;      // number of offsets (0: not a stencil handle)
+    int ty = 4, tz = 2;
+    double h = 0;
+    double hs_full = 0;  // row sum of an interior cell (all offsets in the grid)
+};
+
 }  // namespace tf
 
 // ------------------------------------------------------------------ the handle
@@ -150,6 +161,10 @@ struct tf_filter_s {
     tf_build_info info{};
     // host-API scratch (lazily allocated, owned)
     double *hx = nullptr, *hdc = nullptr, *hout = nullptr;
+    // matrix-free stencil handles (tf_build_stencil): no CSR; offset table on the device
+    tf::StencilGeom stencil;
+    int4 *stencil_off = nullptr;
+    double *stencil_w = nullptr;
 };
 
 namespace tf {
@@ -167,6 +182,12 @@ tf_status radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys_alt, u
 // build.cu
 tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, cudaStream_t s,
                               tf_filter_s *h);
+
+// stencil.cu
+tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, double rmin, cudaStream_t s,
+                        tf_filter_s *f);
+tf_status launch_stencil(const tf_filter_s *f, const double *x, const double *dc, double *out, bool sens,
+                         cudaStream_t s);
 
 // apply.cu
 tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s);

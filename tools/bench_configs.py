@@ -86,5 +86,34 @@ def main():
         torch.cuda.empty_cache()
 
 
+def stencil_rows():
+    """Matrix-free stencil (row a10) on configs 1 and 3: own bytes (x, dc read, out written)
+    and CSR-equivalent GB/s, labelled."""
+    dev = torch.device("cuda:0")
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+    for cfg, dims in ((1, (2, 60, 20, 1)), (3, (3, 160, 80, 80))):
+        c, x, dc, rmin, meta = bench.load_workload(cfg)
+        n = c.shape[0]
+        xd, dcd = torch.from_numpy(x).to(dev), torch.from_numpy(dc).to(dev)
+        out = torch.empty_like(xd)
+        f = tf.tf_build_stencil(*dims, 1.0, rmin)
+        for _ in range(3):
+            f.sensitivity(xd, dcd, out=out)
+        row = {"stencil_config": cfg, "n": n, "nnz_equiv": f.nnz}
+        for mode, fl in (("hot", None), ("cold", flush)):
+            ts = timed(lambda: f.sensitivity(xd, dcd, out=out), 50, fl)
+            td = timed(lambda: f.density(xd, out=out), 50, fl)
+            row[f"sens_us_{mode}"] = ts * 1e6
+            row[f"sens_own_gbs_{mode}"] = 24 * n / ts / 1e9
+            row[f"sens_csr_equiv_gbs_{mode}"] = bench.sens_bytes(n, f.nnz) / ts / 1e9
+            row[f"dens_us_{mode}"] = td * 1e6
+            row[f"dens_own_gbs_{mode}"] = 16 * n / td / 1e9
+            row[f"dens_csr_equiv_gbs_{mode}"] = bench.dens_bytes(n, f.nnz) / td / 1e9
+        print(json.dumps(row), flush=True)
+        f.close()
+
+
 if __name__ == "__main__":
-    main()
+    if not os.environ.get("STENCIL_ONLY"):
+        main()
+    stencil_rows()
