@@ -61,6 +61,9 @@ def lib():
         L.or_apply_sensitivity.restype = None
         L.or_apply_density.argtypes = [I64, P, P, P, P, P, P, P]
         L.or_apply_density.restype = None
+        L.or_oc_update.argtypes = [I64, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                   ctypes.c_double, P, P]
+        L.or_oc_update.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -185,3 +188,16 @@ def apply_density(H: CSR, x: np.ndarray) -> np.ndarray:
     lib().or_apply_density(m, _p(rows), _p(H.rowptr), _p(H.cols), _p(H.vals), _p(H.hs),
                            _p(x), _p(out))
     return out
+
+
+def oc_update(d: np.ndarray, dc: np.ndarray, volfrac: float, move: float = 0.2, l1: float = 0.0,
+              l2: float = 100000.0, tol: float = 1e-4):
+    """NEXT-1: OC update with bisection (Eq. update; listing PAPER.md:380-385),
+    exact-sum branch decisions (R15). Returns (density_new, last l_mid, iterations)."""
+    d = _c64(d)
+    dc = _c64(dc)
+    out = np.empty_like(d)
+    lm = np.zeros(1)
+    it = lib().or_oc_update(d.shape[0], _p(d), _p(dc), float(volfrac), float(move), float(l1), float(l2),
+                            float(tol), _p(out), _p(lm))
+    return out, float(lm[0]), int(it)

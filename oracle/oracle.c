@@ -284,3 +284,59 @@ void or_apply_density(int64_t m, const int64_t *rows, const int64_t *rowptr,
         out[r] = acc / hs[r];
     }
 }
+
+/* ------------------------------------------------------------------ NEXT-1: OC update
+ *
+ * Optimality-criteria update with bisection on the Lagrange multiplier (Eq. update,
+ * PAPER.md:218-228; bisection PAPER.md:229-234; listing PAPER.md:380-385):
+ *
+ *   l1, l2, move = 0, 100000, 0.2
+ *   while l2 - l1 > 1e-4:
+ *       l_mid = 0.5 * (l2 + l1)
+ *       density_new = max(0.001, max(d - move, min(1.0, min(d + move, d * sqrt(-dc / l_mid)))))
+ *       l1, l2 = (l_mid, l2) if sum(density_new) - volfrac * N > 0 else (l1, l_mid)
+ *
+ * Reading R15: the branch compares the EXACT sum with volfrac*N. Every
+ * density_new lies in [0.001, 1], so it is an integer multiple of 2^-62; the sum is
+ * accumulated exactly as 128-bit integers in units of 2^-62 (order-independent), and the
+ * target volfrac*N (one fp64 rounding, as in the listing) is converted exactly.
+ * Preconditions (as for the listing): d in [0, 1], dc <= 0 (filtered compliance sensitivities).
+ * max/min propagate NaN like numpy's maximum/minimum. Returns the number of iterations;
+ * *lmid_out = the last l_mid evaluated; xnew = density_new at that l_mid.
+ */
+static double np_max(double a, double b) { return (a != a || b != b) ? (a != a ? a : b) : (a > b ? a : b); }
+static double np_min(double a, double b) { return (a != a || b != b) ? (a != a ? a : b) : (a < b ? a : b); }
+
+static double oc_value(double d, double dc, double lmid, double move)
+{
+    double s = sqrt(-dc / lmid);
+    return np_max(0.001, np_max(d - move, np_min(1.0, np_min(d + move, d * s))));
+}
+
+/* exact value*2^62 as an integer (value in [0.001, 1], a multiple of 2^-62) */
+static unsigned __int128 oc_units(double v) { return (unsigned __int128)ldexp(v, 62); }
+
+int or_oc_update(int64_t n, const double *d, const double *dc, double volfrac, double move,
+                 double l1, double l2, double tol, double *xnew, double *lmid_out)
+{
+    const double target = volfrac * (double)n;
+    const unsigned __int128 T = oc_units(target);  /* target*2^62 is an integer for target >= 2^-10 */
+    int iters = 0;
+    double lmid = 0.5 * (l2 + l1);
+    while (l2 - l1 > tol) {
+        lmid = 0.5 * (l2 + l1);
+        unsigned __int128 S = 0;
+        int nan = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            double v = oc_value(d[i], dc[i], lmid, move);
+            if (v != v) nan = 1;          /* numpy: NaN sum, NaN > 0 is False */
+            else S += oc_units(v);
+        }
+        if (!nan && S > T) l1 = lmid;
+        else l2 = lmid;
+        ++iters;
+    }
+    for (int64_t i = 0; i < n; ++i) xnew[i] = oc_value(d[i], dc[i], lmid, move);
+    *lmid_out = lmid;
+    return iters;
+}

@@ -1,0 +1,57 @@
+"""Pins for the NEXT-1 oracle (OC update with bisection, listing 380-385)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+
+def paper_listing(density, sensitivity, volfrac, num_cells):
+    """The paper's listing, verbatim numpy; returns the decisions too."""
+    l1, l2, move = 0, 100000, 0.2
+    decisions = []
+    while l2 - l1 > 1e-4:
+        l_mid = 0.5 * (l2 + l1)
+        density_new = np.maximum(0.001, np.maximum(density - move, np.minimum(1.0, np.minimum(density + move, density * np.sqrt(-sensitivity / l_mid)))))
+        up = sum(density_new) - volfrac * num_cells > 0
+        decisions.append(bool(up))
+        l1, l2 = (l_mid, l2) if up else (l1, l_mid)
+    return density_new, l_mid, decisions
+
+
+@pytest.mark.parametrize("n,volfrac,seed", [(50, 0.5, 1), (400, 0.3, 2), (1000, 0.15, 3), (777, 0.4, 4)])
+def test_oc_matches_paper_listing(n, volfrac, seed):
+    """Same l_mid sequence and bitwise-identical density_new as the printed listing (whose
+    rounded-sum decisions agree with the exact ones away from ties)."""
+    d = synth.uniform(100 + seed, 0, n, 0.001, 1.0)
+    dc = -synth.uniform(200 + seed, 0, n, 0.0, 2.0)
+    ref, lref, dec = paper_listing(d, dc, volfrac, n)
+    x, lm, it = oracle.oc_update(d, dc, volfrac)
+    assert it == len(dec) == 30
+    assert lm == lref
+    np.testing.assert_array_equal(x, ref)
+
+
+def test_oc_closed_form_uniform():
+    """Uniform d and dc: d*sqrt(-dc/l) = volfrac at l* = -dc d^2 / volfrac^2 (inside the move
+    limits), so the bisection converges to l* within its tolerance."""
+    n, d0, dc0, vf = 64, 0.5, -0.8, 0.45
+    x, lm, it = oracle.oc_update(np.full(n, d0), np.full(n, dc0), vf)
+    lstar = -dc0 * d0 * d0 / (vf * vf)
+    assert abs(lm - lstar) <= 2e-4
+    assert np.all(x == x[0]) and abs(x[0] - vf) < 1e-4
+
+
+def test_oc_invariants():
+    n = 5000
+    d = synth.uniform(301, 0, n, 0.001, 1.0)
+    dc = -synth.uniform(302, 0, n, 0.0, 3.0)
+    x, lm, it = oracle.oc_update(d, dc, 0.3)
+    assert np.all(x >= 0.001) and np.all(x <= 1.0)
+    assert np.all(x >= d - 0.2)  # move limit m = 0.2 (Eq. update)
+    assert np.all(x <= np.maximum(0.001, np.minimum(1.0, d + 0.2)))
+    # volume constraint met up to the bisection tolerance's effect
+    assert abs(x.sum() - 0.3 * n) < 1e-2 * n
+    # sum of density_new is nonincreasing in the multiplier
+    sums = [oracle.oc_update(d, dc, 0.3, l1=l, l2=l, tol=1.0)[0].sum() for l in (0.01, 0.1, 1.0, 10.0)]
+    assert all(a >= b for a, b in zip(sums, sums[1:]))
