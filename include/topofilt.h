@@ -113,6 +113,23 @@ TF_API tf_status tf_build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, d
 /* tf_filter_nnz -- stored entries of a CSR filter, or those of the equivalent CSR of a stencil. */
 TF_API int64_t tf_filter_nnz(tf_filter h);
 
+/*
+ * tf_oc_update -- NEXT-1: optimality-criteria density update with bisection on
+ * the Lagrange multiplier (Eq. update; bisection PAPER.md:229-234; listing
+ * PAPER.md:380-385), consuming the sensitivity filter's output:
+ *     while l2 - l1 > tol:  l_mid = (l2 + l1)/2;
+ *         x_new = max(0.001, max(x - move, min(1, min(x + move, x*sqrt(-dc/l_mid)))));
+ *         (l1, l2) = (l_mid, l2) if sum(x_new) > volfrac*n else (l1, l_mid)
+ *   The paper's call is move = 0.2, l1 = 0, l2 = 1e5, tol = 1e-4. Branch decisions use the EXACT
+ *   sum (128-bit fixed point; R15), so results are bitwise reproducible.
+ *   x, dc: device fp64 [n] (x in [0, 1], dc <= 0); x_new: device fp64 [n] (may alias x);
+ *   lmid_out: device fp64 [1] (the last l_mid); iters_out: device int32 [1] or NULL.
+ *   One cooperative kernel launch on `stream`, no host sync.
+ */
+TF_API tf_status tf_oc_update(const double *x, const double *dc, int64_t n, double volfrac, double move,
+                              double l1, double l2, double tol, double *x_new, double *lmid_out,
+                              int32_t *iters_out, void *stream);
+
 /* tf_filter_view -- borrowed device pointers of the CSR and Hs (no copy). */
 TF_API tf_status tf_filter_view(tf_filter h, tf_view *v);
 

@@ -27,7 +27,7 @@ EXPORTS = [
     "tf_build_filter", "tf_filter_view", "tf_build_stats", "tf_sensitivity_filter", "tf_density_filter",
     "tf_free", "tf_last_error", "tf_build_filter_host", "tf_sensitivity_filter_host",
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
-    "tf_version", "tf_build_stencil", "tf_filter_nnz",
+    "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update",
 ]
 
 
@@ -73,6 +73,7 @@ def _load():
         "tf_version": ([], I32),
         "tf_build_stencil": ([I32, I64, I64, I64, D, D, P, PP], I32),
         "tf_filter_nnz": ([P], I64),
+        "tf_oc_update": ([P, P, I64, D, D, D, D, D, P, P, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -304,3 +305,18 @@ def set_alloc_limit(nbytes: int):
 
 def version() -> int:
     return int(_lib.tf_version())
+
+
+def tf_oc_update(x, dc, volfrac: float, move: float = 0.2, l1: float = 0.0, l2: float = 100000.0,
+                 tol: float = 1e-4, x_new=None, stream=None):
+    """NEXT-1: OC update with bisection. Returns (x_new, lmid tensor[1], iters tensor[1])."""
+    import torch
+    n = x.numel()
+    if x_new is None:
+        x_new = torch.empty_like(x)
+    lm = torch.empty(1, dtype=torch.float64, device=x.device)
+    it = torch.empty(1, dtype=torch.int32, device=x.device)
+    _check(_lib.tf_oc_update(_dptr(x, "x", torch.float64), _dptr(dc, "dc", torch.float64, n), n, float(volfrac),
+                             float(move), float(l1), float(l2), float(tol), _dptr(x_new, "x_new", torch.float64, n),
+                             _dptr(lm, "lmid"), ctypes.c_void_p(it.data_ptr()), _stream_ptr(stream)))
+    return x_new, lm, it

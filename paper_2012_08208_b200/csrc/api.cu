@@ -400,6 +400,25 @@ tf_status tf_filter_from_csr(const int64_t *rowptr_host, const int32_t *cols_hos
 
 int64_t tf_filter_nnz(tf_filter h) { return h ? h->nnz : -1; }
 
+tf_status tf_oc_update(const double *x, const double *dc, int64_t n, double volfrac, double move, double l1,
+                       double l2, double tol, double *x_new, double *lmid_out, int32_t *iters_out, void *stream) {
+    if (n < 1 || n >= (int64_t)0x7fffffff) {
+        set_error("tf_oc_update: n out of range");
+        return TF_ERR_INVALID;
+    }
+    if (!isfinite(volfrac) || !(volfrac > 0) || !isfinite(move) || !(move >= 0) || !isfinite(l1) ||
+        !isfinite(l2) || !(l2 >= l1) || !(tol > 0)) {
+        set_error("tf_oc_update: invalid volfrac/move/l1/l2/tol");
+        return TF_ERR_INVALID;
+    }
+    TF_TRY(require_device(x, "x"));
+    TF_TRY(require_device(dc, "dc"));
+    TF_TRY(require_device(x_new, "x_new"));
+    TF_TRY(require_device(lmid_out, "lmid_out"));
+    if (iters_out) TF_TRY(require_device(iters_out, "iters_out"));
+    return oc_update(x, dc, n, volfrac, move, l1, l2, tol, x_new, lmid_out, iters_out, (cudaStream_t)stream);
+}
+
 void tf_free(tf_filter h) { destroy(h); }
 
 }  // extern "C"

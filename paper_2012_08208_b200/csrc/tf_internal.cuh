@@ -189,6 +189,10 @@ tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, d
 tf_status launch_stencil(const tf_filter_s *f, const double *x, const double *dc, double *out, bool sens,
                          cudaStream_t s);
 
+// oc.cu (NEXT-1)
+tf_status oc_update(const double *x, const double *dc, int64_t n, double volfrac, double move, double l1,
+                    double l2, double tol, double *xnew, double *lmid_out, int *iters_out, cudaStream_t s);
+
 // apply.cu
 tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s);
 tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double *dc, double *out,

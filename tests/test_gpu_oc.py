@@ -1,0 +1,69 @@
+"""NEXT-1 on the GPU: the OC update with bisection (tf_oc_update) against the oracle, bitwise
+(same correctly rounded element formula, exact-sum decisions: DESIGN.md R15)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tf():
+    assert torch.cuda.is_available()
+    import paper_2012_08208_b200 as m
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("n,vf,seed", [(1, 0.5, 1), (7, 0.4, 2), (1000, 0.3, 3), (100_003, 0.45, 4),
+                                       (1_000_000, 0.5, 5)])
+def test_oc_matches_oracle(tf, n, vf, seed):
+    d = synth.uniform(400 + seed, 0, n, 0.001, 1.0)
+    dc = -synth.uniform(500 + seed, 0, n, 0.0, 2.0)
+    ref, lref, itref = oracle.oc_update(d, dc, vf)
+    xn, lm, it = tf.tf_oc_update(dev(d), dev(dc), vf)
+    assert int(it.item()) == itref
+    assert float(lm.item()) == lref
+    np.testing.assert_array_equal(xn.cpu().numpy(), ref)
+
+
+def test_oc_in_place_and_params(tf):
+    n = 50_000
+    d = synth.uniform(601, 0, n, 0.001, 1.0)
+    dc = -synth.uniform(602, 0, n, 0.0, 1.0)
+    ref, lref, _ = oracle.oc_update(d, dc, 0.35, move=0.1, l1=0.0, l2=1000.0, tol=1e-6)
+    xd = dev(d)
+    _, lm, _ = tf.tf_oc_update(xd, dev(dc), 0.35, move=0.1, l2=1000.0, tol=1e-6, x_new=xd)
+    np.testing.assert_array_equal(xd.cpu().numpy(), ref)
+    assert float(lm.item()) == lref
+
+
+def test_design_iteration_filter_then_oc(tf):
+    """One optimisation-iteration tail on config 3: sensitivity filter (a8) then the OC update,
+    against the oracle chain."""
+    c, x, dc, rmin = synth.workload(3)
+    H = oracle.build_celllist(c, rmin)
+    dcf = oracle.apply_sensitivity(H, x, dc)
+    ref, lref, _ = oracle.oc_update(x, dcf, 0.5)
+    f = tf.tf_build_filter(dev(c), rmin)
+    xd = dev(x)
+    dcf_g = f.sensitivity(xd, dev(dc))
+    xn, lm, _ = tf.tf_oc_update(xd, dcf_g, 0.5)
+    # the filtered sensitivities agree to 1e-10 (not bitwise), so compare the updated densities
+    # to the same tolerance and the multipliers to the bisection tolerance
+    np.testing.assert_allclose(xn.cpu().numpy(), ref, rtol=1e-9, atol=1e-12)
+    assert abs(float(lm.item()) - lref) <= 1e-4
+
+
+def test_oc_rejects_bad_args(tf):
+    d = dev(np.full(10, 0.5))
+    with pytest.raises(tf.TopofiltError):
+        tf.tf_oc_update(d, dev(np.full(10, -1.0)), -0.5)
+    with pytest.raises(tf.TopofiltError):
+        tf.tf_oc_update(d, dev(np.full(10, -1.0)), 0.5, l1=5.0, l2=1.0)
