@@ -94,18 +94,35 @@ __global__ void __launch_bounds__(kOcThreads) k_oc(const double *__restrict__ x,
                 make_ulonglong2((unsigned long long)b, (unsigned long long)(b >> 64) | (bn ? kNanBit : 0ull));
         }
         grid.sync();
-        if (threadIdx.x == 0) {
-            // every block sums the partials in the same order -> the same decision everywhere;
-            // __ldcg: the buffer was last read two iterations ago, so bypass possibly stale L1
+        {
+            // every block sums all partials (integer: any order gives the same total) with all its
+            // threads -> the same decision everywhere; __ldcg: the buffer was last read two
+            // iterations ago, so bypass possibly stale L1 lines
             u128 S = 0;
             int sn = 0;
             const ulonglong2 *pp = parts + (size_t)(it & 1) * gridDim.x;
-            for (unsigned bb = 0; bb < gridDim.x; ++bb) {
+            for (unsigned bb = threadIdx.x; bb < gridDim.x; bb += blockDim.x) {
                 const ulonglong2 p = __ldcg(pp + bb);
                 sn |= (p.y & kNanBit) ? 1 : 0;
                 S += ((u128)(p.y & ~kNanBit) << 64) | p.x;
             }
-            s_up = (!sn && S > T) ? 1 : 0;  // numpy: a NaN sum never compares > 0
+            unsigned long long slo = (unsigned long long)S, shi = (unsigned long long)(S >> 64);
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long olo = __shfl_xor_sync(0xffffffffu, slo, o);
+                const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, shi, o);
+                const u128 t = (((u128)shi << 64) | slo) + (((u128)ohi << 64) | olo);
+                slo = (unsigned long long)t, shi = (unsigned long long)(t >> 64);
+                sn |= __shfl_xor_sync(0xffffffffu, sn, o);
+            }
+            __syncthreads();  // s_lo/s_hi/s_nan of the block reduction above are consumed
+            if (lane == 0) s_lo[warp] = slo, s_hi[warp] = shi, s_nan[warp] = sn;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                u128 tot = 0;
+                int tn = 0;
+                for (int w = 0; w < kOcThreads / 32; ++w) tot += ((u128)s_hi[w] << 64) | s_lo[w], tn |= s_nan[w];
+                s_up = (!tn && tot > T) ? 1 : 0;  // numpy: a NaN sum never compares > 0
+            }
         }
         __syncthreads();
         if (s_up) l1 = lmid;

@@ -113,7 +113,30 @@ def stencil_rows():
         f.close()
 
 
+def oc_rows():
+    """NEXT-1 OC update (30 bisection passes + final write) on configs 3 and 5."""
+    dev = torch.device("cuda:0")
+    for cfg in (3, 5):
+        n = synth.centroids(cfg).shape[0] if cfg != 5 else 12_000_000
+        x = synth.density(cfg, n)
+        dcf = synth.sensitivity(cfg, x)
+        xd, dd = torch.from_numpy(x).to(dev), torch.from_numpy(dcf).to(dev)
+        xn = torch.empty_like(xd)
+        for _ in range(2):
+            tf.tf_oc_update(xd, dd, 0.5, x_new=xn)
+        t = timed(lambda: tf.tf_oc_update(xd, dd, 0.5, x_new=xn), 10)
+        it = 30
+        bytes_ = it * 16 * n + 24 * n
+        print(json.dumps({"oc_config": cfg, "n": n, "us": t * 1e6, "iterations": it,
+                          "bytes_model": "30 x 16N (x, dc per pass) + 24N (final pass)",
+                          "gbs": bytes_ / t / 1e9, "frac_8tbs": bytes_ / t / 1e9 / HBM}), flush=True)
+
+
 if __name__ == "__main__":
+    if os.environ.get("OC_ONLY"):
+        oc_rows()
+        sys.exit(0)
     if not os.environ.get("STENCIL_ONLY"):
         main()
     stencil_rows()
+    oc_rows()
