@@ -145,6 +145,16 @@ TF_API tf_status tf_build_stats(tf_filter h, tf_build_info *info);
 TF_API tf_status tf_sensitivity_filter(tf_filter h, const double *x, const double *dc, double *out,
                                 void *stream);
 
+/*
+ * tf_sensitivity_filter_energy -- NEXT-2: the sensitivity filter with the
+ *   compliance sensitivity evaluated inside the launch from the element energies U:
+ *   dc_j = -penal * x_j^(penal-1) * U_j (listing PAPER.md:376), then
+ *   out_i = (sum_j W_ij x_j dc_j) / (Hs_i * max(1e-3, x_i)). dc is never stored.
+ *   x, U, out: device fp64 [n]; out must not overlap x or U. CSR handles only.
+ */
+TF_API tf_status tf_sensitivity_filter_energy(tf_filter h, const double *x, const double *U, double penal,
+                                              double *out, void *stream);
+
 /* tf_density_filter -- out_i = (sum_j W_ij x_j) / Hs_i. Same conventions. */
 TF_API tf_status tf_density_filter(tf_filter h, const double *x, double *out, void *stream);
 

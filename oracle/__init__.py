@@ -64,6 +64,8 @@ def lib():
         L.or_oc_update.argtypes = [I64, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                    ctypes.c_double, P, P]
         L.or_oc_update.restype = ctypes.c_int
+        L.or_compliance_sensitivity.argtypes = [I64, P, P, ctypes.c_double, P]
+        L.or_compliance_sensitivity.restype = None
         _lib = L
     return _lib
 
@@ -201,3 +203,12 @@ def oc_update(d: np.ndarray, dc: np.ndarray, volfrac: float, move: float = 0.2, 
     it = lib().or_oc_update(d.shape[0], _p(d), _p(dc), float(volfrac), float(move), float(l1), float(l2),
                             float(tol), _p(out), _p(lm))
     return out, float(lm[0]), int(it)
+
+
+def compliance_sensitivity(x: np.ndarray, U: np.ndarray, penal: float) -> np.ndarray:
+    """NEXT-2: dc = -penal * x**(penal-1) * U (listing PAPER.md:376)."""
+    x = _c64(x)
+    U = _c64(U)
+    out = np.empty_like(x)
+    lib().or_compliance_sensitivity(x.shape[0], _p(x), _p(U), float(penal), _p(out))
+    return out

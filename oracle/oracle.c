@@ -340,3 +340,10 @@ int or_oc_update(int64_t n, const double *d, const double *dc, double volfrac, d
     *lmid_out = lmid;
     return iters;
 }
+
+/* NEXT-2: compliance sensitivity (listing PAPER.md:376, numpy order):
+ *   sensitivity = -penal * density ** (penal - 1) * U   ==  ((-penal) * pow(x, penal-1)) * U */
+void or_compliance_sensitivity(int64_t n, const double *x, const double *U, double penal, double *dc)
+{
+    for (int64_t i = 0; i < n; ++i) dc[i] = (-penal * pow(x[i], penal - 1.0)) * U[i];
+}

@@ -27,7 +27,7 @@ EXPORTS = [
     "tf_build_filter", "tf_filter_view", "tf_build_stats", "tf_sensitivity_filter", "tf_density_filter",
     "tf_free", "tf_last_error", "tf_build_filter_host", "tf_sensitivity_filter_host",
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
-    "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update",
+    "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update", "tf_sensitivity_filter_energy",
 ]
 
 
@@ -74,6 +74,7 @@ def _load():
         "tf_build_stencil": ([I32, I64, I64, I64, D, D, P, PP], I32),
         "tf_filter_nnz": ([P], I64),
         "tf_oc_update": ([P, P, I64, D, D, D, D, D, P, P, P, P], I32),
+        "tf_sensitivity_filter_energy": ([P, P, P, D, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -239,6 +240,17 @@ def tf_sensitivity_filter(f: Filter, x, dc, out, stream=None):
     _check(_lib.tf_sensitivity_filter(f.handle, _dptr(x, "x", torch.float64, f.n),
                                       _dptr(dc, "dc", torch.float64, f.n),
                                       _dptr(out, "out", torch.float64, f.n), _stream_ptr(stream)))
+    return out
+
+
+def tf_sensitivity_filter_energy(f: Filter, x, U, penal: float, out=None, stream=None):
+    """NEXT-2: sensitivity filter of dc = -penal x^(penal-1) U, dc evaluated in-kernel."""
+    import torch
+    if out is None:
+        out = torch.empty_like(x)
+    _check(_lib.tf_sensitivity_filter_energy(f.handle, _dptr(x, "x", torch.float64, f.n),
+                                             _dptr(U, "U", torch.float64, f.n), float(penal),
+                                             _dptr(out, "out", torch.float64, f.n), _stream_ptr(stream)))
     return out
 
 

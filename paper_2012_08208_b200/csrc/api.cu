@@ -293,6 +293,20 @@ tf_status tf_sensitivity_filter(tf_filter h, const double *x, const double *dc, 
     return launch_sensitivity(h, x, dc, out, (cudaStream_t)stream);
 }
 
+tf_status tf_sensitivity_filter_energy(tf_filter h, const double *x, const double *U, double penal, double *out,
+                                       void *stream) {
+    TF_TRY(check_apply(h, x, U, out, true));
+    if (!isfinite(penal)) {
+        set_error("penal must be finite");
+        return TF_ERR_INVALID;
+    }
+    if (h->stencil.K > 0) {
+        set_error("tf_sensitivity_filter_energy: stencil handles are not supported (use a CSR filter)");
+        return TF_ERR_INVALID;
+    }
+    return launch_sensitivity_energy(h, x, U, penal, out, (cudaStream_t)stream);
+}
+
 tf_status tf_density_filter(tf_filter h, const double *x, double *out, void *stream) {
     TF_TRY(check_apply(h, x, nullptr, out, false));
     return launch_density(h, x, out, (cudaStream_t)stream);

@@ -144,7 +144,8 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                                                                       double *__restrict__ out,
                                                                       const int32_t *__restrict__ rb,
                                                                       const int64_t *__restrict__ wlo,
-                                                                      int64_t nwin, double *tbuf, int64_t n) {
+                                                                      int64_t nwin, double *tbuf, int64_t n,
+                                                                      double penal, int energy) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *svals = reinterpret_cast<double *>(smem_raw);                           // [kStages][kStage]
     int64_t *srow = reinterpret_cast<int64_t *>(svals + kStages * kStage);          // [kStages][kRowCap]
@@ -201,8 +202,17 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
     if (SENS) {
         // fused Hadamard pass t = x o dc (PAPER.md:447 np.multiply(density, sensitivity)),
         // then a grid-wide barrier: the SpMV gathers one array instead of two
-        for (int64_t i = (int64_t)blockIdx.x * kThreads + tid; i < n; i += (int64_t)gridDim.x * kThreads)
-            tbuf[i] = __ldg(x + i) * __ldg(dc + i);
+        // NEXT-2 (energy != 0): dc is evaluated here from the element energies U passed in `dc`,
+        // dc = -p x^(p-1) U (listing PAPER.md:376), never stored
+        if (energy) {
+            for (int64_t i = (int64_t)blockIdx.x * kThreads + tid; i < n; i += (int64_t)gridDim.x * kThreads) {
+                const double xi = __ldg(x + i);
+                tbuf[i] = xi * ((-penal * pow(xi, penal - 1.0)) * __ldg(dc + i));
+            }
+        } else {
+            for (int64_t i = (int64_t)blockIdx.x * kThreads + tid; i < n; i += (int64_t)gridDim.x * kThreads)
+                tbuf[i] = __ldg(x + i) * __ldg(dc + i);
+        }
         cooperative_groups::this_grid().sync();
     }
     // t was written in this launch: read it with plain cached loads, never the read-only path
@@ -281,7 +291,8 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
 }
 
 template <bool SENS, int G, int U>
-tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s) {
+tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s,
+                         double penal, int energy) {
     const size_t smem = (size_t)kStages * (kStage * (sizeof(double) + sizeof(int32_t)) + kRowCap * sizeof(int64_t));
     auto kern = k_spmv<SENS, G, U>;
     // per-instantiation attribute (dynamic shared memory above 48 KB needs the opt-in)
@@ -306,8 +317,9 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
     if (SENS) {
         // per-call scratch (stream-ordered): concurrent applies on different streams stay safe
         TF_TRY(dalloc(&tbuf, (size_t)n, s, "sensitivity scratch t = x*dc"));
-        void *args[] = {(void *)&rowptr, (void *)&cols, (void *)&vals, (void *)&hs, (void *)&x, (void *)&dc,
-                        (void *)&out, (void *)&rb, (void *)&wlo, (void *)&nwin, (void *)&tbuf, (void *)&n};
+        void *args[] = {(void *)&rowptr, (void *)&cols, (void *)&vals, (void *)&hs,   (void *)&x,
+                        (void *)&dc,     (void *)&out,  (void *)&rb,   (void *)&wlo,  (void *)&nwin,
+                        (void *)&tbuf,   (void *)&n,    (void *)&penal, (void *)&energy};
         cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads + 32), args, smem, s);
         count_launch();
         dev_free(tbuf, s);
@@ -317,26 +329,28 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
         }
         return TF_OK;
     }
-    kern<<<grid, kThreads + 32, smem, s>>>(rowptr, cols, vals, hs, x, dc, out, rb, wlo, nwin, tbuf, n);
+    kern<<<grid, kThreads + 32, smem, s>>>(rowptr, cols, vals, hs, x, dc, out, rb, wlo, nwin, tbuf, n, penal, energy);
     TF_LAUNCH_CHECK();
     return TF_OK;
 }
 
 template <bool SENS, int G>
-tf_status launch_spmv_g(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s) {
-    if (h->plan.unroll >= 8) return launch_spmv_gu<SENS, G, 8>(h, x, dc, out, s);
-    return launch_spmv_gu<SENS, G, 4>(h, x, dc, out, s);
+tf_status launch_spmv_g(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s,
+                        double penal, int energy) {
+    if (h->plan.unroll >= 8) return launch_spmv_gu<SENS, G, 8>(h, x, dc, out, s, penal, energy);
+    return launch_spmv_gu<SENS, G, 4>(h, x, dc, out, s, penal, energy);
 }
 
 template <bool SENS>
-tf_status launch_spmv(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s) {
+tf_status launch_spmv(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s,
+                      double penal = 0.0, int energy = 0) {
     switch (h->plan.group) {
-        case 1: return launch_spmv_g<SENS, 1>(h, x, dc, out, s);
-        case 2: return launch_spmv_g<SENS, 2>(h, x, dc, out, s);
-        case 4: return launch_spmv_g<SENS, 4>(h, x, dc, out, s);
-        case 8: return launch_spmv_g<SENS, 8>(h, x, dc, out, s);
-        case 16: return launch_spmv_g<SENS, 16>(h, x, dc, out, s);
-        default: return launch_spmv_g<SENS, 32>(h, x, dc, out, s);
+        case 1: return launch_spmv_g<SENS, 1>(h, x, dc, out, s, penal, energy);
+        case 2: return launch_spmv_g<SENS, 2>(h, x, dc, out, s, penal, energy);
+        case 4: return launch_spmv_g<SENS, 4>(h, x, dc, out, s, penal, energy);
+        case 8: return launch_spmv_g<SENS, 8>(h, x, dc, out, s, penal, energy);
+        case 16: return launch_spmv_g<SENS, 16>(h, x, dc, out, s, penal, energy);
+        default: return launch_spmv_g<SENS, 32>(h, x, dc, out, s, penal, energy);
     }
 }
 
@@ -393,6 +407,11 @@ tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double
                              cudaStream_t s) {
     if (h->stencil.K > 0) return launch_stencil(h, x, dc, out, true, s);
     return launch_spmv<true>(h, x, dc, out, s);
+}
+
+tf_status launch_sensitivity_energy(const tf_filter_s *h, const double *x, const double *U, double penal,
+                                    double *out, cudaStream_t s) {
+    return launch_spmv<true>(h, x, U, out, s, penal, 1);
 }
 
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s) {

@@ -198,5 +198,7 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s);
 tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double *dc, double *out,
                              cudaStream_t s);
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s);
+tf_status launch_sensitivity_energy(const tf_filter_s *h, const double *x, const double *U, double penal,
+                                    double *out, cudaStream_t s);
 
 }  // namespace tf

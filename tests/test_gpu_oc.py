@@ -67,3 +67,16 @@ def test_oc_rejects_bad_args(tf):
         tf.tf_oc_update(d, dev(np.full(10, -1.0)), -0.5)
     with pytest.raises(tf.TopofiltError):
         tf.tf_oc_update(d, dev(np.full(10, -1.0)), 0.5, l1=5.0, l2=1.0)
+
+
+@pytest.mark.parametrize("cfg,penal", [(2, 3.0), (3, 3.0), (4, 2.5)])
+def test_sensitivity_from_energy(tf, cfg, penal):
+    """NEXT-2: dc evaluated inside the sensitivity filter's fused pass from element energies."""
+    c, x, dc, rmin = synth.workload(cfg)
+    U = synth.uniform(800 + cfg, 0, x.shape[0], 0.0, 2.0)
+    H = oracle.build_celllist(c, rmin)
+    ref = oracle.apply_sensitivity(H, x, oracle.compliance_sensitivity(x, U, penal))
+    f = tf.tf_build_filter(dev(c), rmin)
+    got = tf.tf_sensitivity_filter_energy(f, dev(x), dev(U), penal).cpu().numpy()
+    scale = np.where(ref != 0, np.abs(ref), np.abs(ref).max())
+    assert np.all(np.abs(got - ref) <= 1e-10 * scale)

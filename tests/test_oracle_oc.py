@@ -56,3 +56,14 @@ def test_oc_invariants():
     # sum of density_new is nonincreasing in the multiplier
     sums = [oracle.oc_update(d, dc, 0.3, l1=l, l2=l, tol=1.0)[0].sum() for l in (0.01, 0.1, 1.0, 10.0)]
     assert all(a >= b for a, b in zip(sums, sums[1:]))
+
+
+def test_compliance_sensitivity_matches_listing():
+    """NEXT-2 oracle: the paper's listing evaluated verbatim by numpy."""
+    x = synth.uniform(701, 0, 1000, 0.001, 1.0)
+    U = synth.uniform(702, 0, 1000, 0.0, 5.0)
+    for penal in (3.0, 1.0, 2.5):
+        ref = -penal * (x) ** (penal - 1) * U
+        np.testing.assert_allclose(oracle.compliance_sensitivity(x, U, penal), ref, rtol=4e-16, atol=0)
+    # p = 1: dc = -U exactly
+    np.testing.assert_array_equal(oracle.compliance_sensitivity(x, U, 1.0), -U)
