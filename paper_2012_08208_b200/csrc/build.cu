@@ -25,6 +25,7 @@
 // structure and weights are bit-identical to it.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -494,7 +495,10 @@ struct FillSmem {
 
 constexpr int kListCap = 128;  // per-warp compacted candidate list (phase A -> phase B)
 
-template <int DIM>
+// Phase B over list[0, nl): exact fp64 test on the original centroid bytes, weight, CSR write
+// at rowptr[row] + rank (ballot compaction keeps the sorted order), Hs partial per lane.
+// FULL: nl is a multiple of 32 (every lane has an entry: no bounds checks, no divergence).
+template <int DIM, bool FULL>
 __device__ __forceinline__ void fill_flush(const SortedPts &P, const uint32_t *skey, const uint32_t *sp,
                                            const int32_t *list, int nl, int lo, double qx, double qy, double qz,
                                            double r2, double rmin, int64_t base, int &wpos, double &hsum,
@@ -503,20 +507,16 @@ __device__ __forceinline__ void fill_flush(const SortedPts &P, const uint32_t *s
     const uint32_t lt = (1u << lane) - 1u;
     for (int e0 = 0; e0 < nl; e0 += 32) {
         const int e = e0 + lane;
-        bool ok = false;
-        double d2 = 0.0;
-        int t = 0;
-        if (e < nl) {
-            t = list[e];
-            const int p = (int)sp[t];
-            d2 = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0);
-            ok = d2 < r2;
-        }
+        const bool have = FULL || e < nl;
+        const int t = have ? list[e] : list[e0];  // idle lanes redo a valid entry, then drop it
+        const int p = (int)sp[t];
+        const double d2 = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0);
+        const bool ok = have && d2 < r2;
         const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+        const double w = weight_of(rmin, d2);
         if (ok) {
-            const double w = weight_of(rmin, d2);
             const int64_t k = base + wpos + __popc(bal & lt);
-            TF_DCHECK(t >= 0 && (int)sp[t] >= 0);
+            TF_DCHECK(t >= 0 && p >= 0);
             cols[k] = (int32_t)skey[t] + lo;
             vals[k] = w;
             hsum += w;
@@ -621,19 +621,26 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
                 const bool m0 = f2_lo(d2) < t_out, m1 = f2_hi(d2) < t_out;
                 const uint32_t b0 = __ballot_sync(0xffffffffu, m0), b1 = __ballot_sync(0xffffffffu, m1);
                 const int pre = nl + __popc(b0 & lt_mask) + __popc(b1 & lt_mask);
-                TF_DCHECK(pre + 1 < kListCap || !(m0 || m1));
+                TF_DCHECK(pre + 1 < kListCap || !(m0 || m1));  // nl < 64 before a 64-wide chunk
                 if (m0) list[pre] = 2 * k;
                 if (m1) list[pre + (m0 ? 1 : 0)] = 2 * k + 1;
                 nl += __popc(b0) + __popc(b1);
-                if (nl > kListCap - 64) {
+                if (nl >= kListCap - 64) {
+                    // flush whole 32-entry chunks only; the < 32 tail moves to the front
+                    const int full = nl & ~31;
                     __syncwarp();
-                    fill_flush<DIM>(P, skey, sp, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum, cols, vals);
+                    fill_flush<DIM, true>(P, skey, sp, list, full, lo, qx, qy, qz, r2, rmin, base, wpos, hsum, cols,
+                                          vals);
+                    const int tail = nl - full;
+                    const int moved = (lane < tail) ? list[full + lane] : 0;
                     __syncwarp();
-                    nl = 0;
+                    if (lane < tail) list[lane] = moved;
+                    __syncwarp();
+                    nl = tail;
                 }
             }
             __syncwarp();
-            fill_flush<DIM>(P, skey, sp, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum, cols, vals);
+            fill_flush<DIM, false>(P, skey, sp, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum, cols, vals);
             __syncwarp();
             for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
             if (lane == 0) {
@@ -930,11 +937,15 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     TF_TRY(dalloc(&h->hs, n, s, "Hs"));
     DevBuf<int32_t> large_rows;
     if (maxC > cap) TF_TRY(large_rows.alloc(n, s, "large-neighbourhood rows"));
+    int fw = wide ? 4 : 2;  // warps per fill block (queries of one bin in parallel)
+    if (const char *e = getenv("TOPOFILT_FILL_WARPS")) fw = atoi(e);  // tuning knob (benchmarks only)
     if (dim == 3) {
-        if (wide) TF_TRY((launch_fill<3, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
+        if (fw >= 8) TF_TRY((launch_fill<3, 8>(P, g, h, cap, large_rows.p, stats.p, s)));
+        else if (fw >= 4) TF_TRY((launch_fill<3, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
         else TF_TRY((launch_fill<3, 2>(P, g, h, cap, large_rows.p, stats.p, s)));
     } else {
-        if (wide) TF_TRY((launch_fill<2, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
+        if (fw >= 8) TF_TRY((launch_fill<2, 8>(P, g, h, cap, large_rows.p, stats.p, s)));
+        else if (fw >= 4) TF_TRY((launch_fill<2, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
         else TF_TRY((launch_fill<2, 2>(P, g, h, cap, large_rows.p, stats.p, s)));
     }
     if (maxC > cap) {
