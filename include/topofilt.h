@@ -174,7 +174,12 @@ TF_API tf_status tf_build_filter_host(const double *centroids_host, int64_t n, i
 TF_API tf_status tf_sensitivity_filter_host(tf_filter h, const double *x_host, const double *dc_host,
                                      double *out_host, void *stream);
 TF_API tf_status tf_density_filter_host(tf_filter h, const double *x_host, double *out_host,
-                                 void *stream);
+                                        void *stream);
+/* One optimisation iteration's filtering on host buffers: uploads x and dc once, runs the
+ * sensitivity and the density filter, and overlaps the download of the sensitivity result
+ * (on a handle-owned side stream) with the density kernel. Synchronises before returning. */
+TF_API tf_status tf_filter_iteration_host(tf_filter h, const double *x_host, const double *dc_host,
+                                          double *sens_host, double *dens_host, void *stream);
 
 /* ------------------------------------------------------------------ test / diagnostics */
 

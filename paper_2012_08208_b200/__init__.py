@@ -28,6 +28,7 @@ EXPORTS = [
     "tf_free", "tf_last_error", "tf_build_filter_host", "tf_sensitivity_filter_host",
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
     "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update", "tf_sensitivity_filter_energy",
+    "tf_filter_iteration_host",
 ]
 
 
@@ -75,6 +76,7 @@ def _load():
         "tf_filter_nnz": ([P], I64),
         "tf_oc_update": ([P, P, I64, D, D, D, D, D, P, P, P, P], I32),
         "tf_sensitivity_filter_energy": ([P, P, P, D, P, P], I32),
+        "tf_filter_iteration_host": ([P, P, P, P, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -275,6 +277,18 @@ def tf_sensitivity_filter_host(f: Filter, x, dc, out=None, stream=None):
     _check(_lib.tf_sensitivity_filter_host(f.handle, _host(x, f.n, "x"), _host(dc, f.n, "dc"),
                                            _host(out, f.n, "out", True), _stream_ptr(stream)))
     return out
+
+
+def tf_filter_iteration_host(f: Filter, x, dc, sens_out=None, dens_out=None, stream=None):
+    """Both filters of one iteration on host arrays (x, dc uploaded once; D2H overlapped)."""
+    if sens_out is None:
+        sens_out = np.empty(f.n, dtype=np.float64)
+    if dens_out is None:
+        dens_out = np.empty(f.n, dtype=np.float64)
+    _check(_lib.tf_filter_iteration_host(f.handle, _host(x, f.n, "x"), _host(dc, f.n, "dc"),
+                                         _host(sens_out, f.n, "sens_out", True),
+                                         _host(dens_out, f.n, "dens_out", True), _stream_ptr(stream)))
+    return sens_out, dens_out
 
 
 def tf_density_filter_host(f: Filter, x, out=None, stream=None):

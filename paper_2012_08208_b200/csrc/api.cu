@@ -107,6 +107,9 @@ static void destroy(tf_filter_s *h) {
     cudaFree(h->hx);
     cudaFree(h->hdc);
     cudaFree(h->hout);
+    cudaFree(h->hout2);
+    if (h->side) cudaStreamDestroy(h->side);
+    if (h->ev) cudaEventDestroy(h->ev);
     delete h;
 }
 
@@ -334,6 +337,33 @@ tf_status tf_sensitivity_filter_host(tf_filter h, const double *x_host, const do
     TF_CUDA_TRY(cudaMemcpyAsync(h->hdc, dc_host, bytes, cudaMemcpyHostToDevice, s));
     TF_TRY(launch_sensitivity(h, h->hx, h->hdc, h->hout, s));
     TF_CUDA_TRY(cudaMemcpyAsync(out_host, h->hout, bytes, cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    return TF_OK;
+}
+
+tf_status tf_filter_iteration_host(tf_filter h, const double *x_host, const double *dc_host, double *sens_host,
+                                   double *dens_host, void *stream) {
+    if (!h || !x_host || !dc_host || !sens_host || !dens_host) {
+        set_error("tf_filter_iteration_host: NULL argument");
+        return TF_ERR_INVALID;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    TF_TRY(ensure_host_scratch(h));
+    if (!h->hout2) TF_CUDA_TRY(cudaMalloc(&h->hout2, (size_t)h->n * sizeof(double)));
+    if (!h->side) TF_CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    if (!h->ev) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev, cudaEventDisableTiming));
+    const size_t bytes = (size_t)h->n * sizeof(double);
+    // x and dc go up once for both filters
+    TF_CUDA_TRY(cudaMemcpyAsync(h->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
+    TF_CUDA_TRY(cudaMemcpyAsync(h->hdc, dc_host, bytes, cudaMemcpyHostToDevice, s));
+    TF_TRY(launch_sensitivity(h, h->hx, h->hdc, h->hout, s));
+    // the sensitivity result drains on the side stream while the density filter runs
+    TF_CUDA_TRY(cudaEventRecord(h->ev, s));
+    TF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev, 0));
+    TF_CUDA_TRY(cudaMemcpyAsync(sens_host, h->hout, bytes, cudaMemcpyDeviceToHost, h->side));
+    TF_TRY(launch_density(h, h->hx, h->hout2, s));
+    TF_CUDA_TRY(cudaMemcpyAsync(dens_host, h->hout2, bytes, cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(h->side));
     TF_CUDA_TRY(cudaStreamSynchronize(s));
     return TF_OK;
 }

@@ -244,6 +244,9 @@ def test_host_variants_match_device(tf):
     xp = torch.from_numpy(x).pin_memory().numpy()
     np.testing.assert_array_equal(fh.sensitivity_host(xp, dc), fd.sensitivity(dev(x), dev(dc)).cpu().numpy())
     np.testing.assert_array_equal(fh.density_host(x), fd.density(dev(x)).cpu().numpy())
+    s2, d2 = tf.tf_filter_iteration_host(fh, x, dc)
+    np.testing.assert_array_equal(s2, fd.sensitivity(dev(x), dev(dc)).cpu().numpy())
+    np.testing.assert_array_equal(d2, fd.density(dev(x)).cpu().numpy())
 
 
 def test_streams_concurrent_applies(tf):

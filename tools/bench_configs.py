@@ -113,6 +113,38 @@ def stencil_rows():
         f.close()
 
 
+def graph_rows():
+    """Configs 1-3 with the applies captured in a CUDA graph (20 iterations of sensitivity +
+    density per graph): removes the per-call host overhead that dominates the small configs."""
+    dev = torch.device("cuda:0")
+    for cfg in (1, 2, 3):
+        c, x, dc, rmin, meta = bench.load_workload(cfg)
+        n = c.shape[0]
+        xd, dcd = torch.from_numpy(x).to(dev), torch.from_numpy(dc).to(dev)
+        os_, od = torch.empty_like(xd), torch.empty_like(xd)
+        f = tf.tf_build_filter(torch.from_numpy(c).to(dev), rmin)
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            f.sensitivity(xd, dcd, out=os_)
+            f.density(xd, out=od)
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        iters = 20
+        with torch.cuda.graph(g):
+            for _ in range(iters):
+                f.sensitivity(xd, dcd, out=os_)
+                f.density(xd, out=od)
+        g.replay()
+        torch.cuda.synchronize()
+        t = timed(g.replay, 10) / iters
+        print(json.dumps({"graph_config": cfg, "n": n, "nnz": f.nnz, "iteration_us": t * 1e6,
+                          "iters_per_s": 1.0 / t,
+                          "gbs": (bench.sens_bytes(n, f.nnz) + bench.dens_bytes(n, f.nnz)) / t / 1e9}), flush=True)
+        f.close()
+
+
 def oc_rows():
     """NEXT-1 OC update (30 bisection passes + final write) on configs 3 and 5."""
     dev = torch.device("cuda:0")
@@ -136,7 +168,11 @@ if __name__ == "__main__":
     if os.environ.get("OC_ONLY"):
         oc_rows()
         sys.exit(0)
+    if os.environ.get("GRAPH_ONLY"):
+        graph_rows()
+        sys.exit(0)
     if not os.environ.get("STENCIL_ONLY"):
         main()
     stencil_rows()
+    graph_rows()
     oc_rows()
