@@ -167,6 +167,14 @@ def load_workload(cfg):
 
 # ------------------------------------------------------------------ CPU oracle baseline
 
+def host_cpu():
+    try:
+        model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+    except Exception:
+        model = "unknown CPU"
+    return f"{model} ({os.cpu_count()} logical cores on the host)"
+
+
 def oracle_sample(c, x, dc, rmin, applies, rows_per_step, steps, seed_cfg):
     """Time the oracle (as it stands, single thread) on a bounded sample of the workload:
     the cell list over all N points (setup, charged pro rata), then for `rows_per_step`
@@ -196,7 +204,8 @@ def oracle_sample(c, x, dc, rmin, applies, rows_per_step, steps, seed_cfg):
     cl.close()
     desc = (f"{rows_per_step} seeded rows per step (stream S(c,5,0)) of the same workload: row build "
             f"+ {applies}x(sensitivity+density) on those rows; cell-list setup over all {n} points "
-            f"({t_setup:.2f} s) charged pro rata; single-threaded C oracle (-O2 -ffp-contract=off)")
+            f"({t_setup:.2f} s) charged pro rata; single-threaded C oracle (-O2 -ffp-contract=off) "
+            f"on {host_cpu()}")
     return statistics.median(vals), times, desc
 
 

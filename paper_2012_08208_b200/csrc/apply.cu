@@ -405,6 +405,7 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
 
 tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double *dc, double *out,
                              cudaStream_t s) {
+    NvtxRange r("tf_apply/sensitivity");
     if (h->stencil.K > 0) return launch_stencil(h, x, dc, out, true, s);
     return launch_spmv<true>(h, x, dc, out, s);
 }
@@ -415,6 +416,7 @@ tf_status launch_sensitivity_energy(const tf_filter_s *h, const double *x, const
 }
 
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s) {
+    NvtxRange r("tf_apply/density");
     if (h->stencil.K > 0) return launch_stencil(h, x, nullptr, out, false, s);
     return launch_spmv<false>(h, x, nullptr, out, s);
 }

@@ -844,7 +844,9 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     const int threads = 256;
     const unsigned grid_n = (unsigned)std::min<int64_t>((n + threads - 1) / threads, (int64_t)di.sms * 16);
 
+    NvtxRange r_all("tf_build");
     // a2 bounding box
+    NvtxRange r_bbox("tf_build/a2 bbox");
     DevBuf<double> part, bbd;
     TF_TRY(part.alloc((size_t)grid_n * 7, s, "bbox partials"));
     TF_TRY(bbd.alloc(8, s, "bbox"));
@@ -866,6 +868,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     h->info.nbins = g.nbins;
 
     // a3 keys
+    NvtxRange r_keys("tf_build/a3-a4 keys, radix sort, cell start");
     DevBuf<uint32_t> k0, v0, k1, v1;
     TF_TRY(k0.alloc(n, s, "keys"));
     TF_TRY(v0.alloc(n, s, "ids"));
@@ -916,6 +919,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     const bool wide = (double)n / (double)g.nbins >= 12.0;
 
     // a5 count
+    NvtxRange r_count("tf_build/a5 count + a6 scan");
     if (dim == 3) TF_TRY(wide ? (launch_count<3, 4>(P, g, cap, counts.p, s)) : (launch_count<3, 2>(P, g, cap, counts.p, s)));
     else TF_TRY(wide ? (launch_count<2, 4>(P, g, cap, counts.p, s)) : (launch_count<2, 2>(P, g, cap, counts.p, s)));
 
@@ -932,6 +936,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     h->nnz = nnz;
 
     // a7 fill
+    NvtxRange r_fill("tf_build/a7 fill");
     TF_TRY(dalloc(&h->cols, nnz + 4, s, "cols (nnz int32, +4 padding for 16-byte bulk copies)"));
     TF_TRY(dalloc(&h->vals, nnz + 4, s, "vals (nnz fp64, +4 padding)"));
     TF_TRY(dalloc(&h->hs, n, s, "Hs"));

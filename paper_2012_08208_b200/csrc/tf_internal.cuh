@@ -8,6 +8,8 @@
 #include <atomic>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/topofilt.h"
 
 namespace tf {
@@ -64,6 +66,14 @@ struct Status {  // lightweight status carrier for host orchestration
     do {                \
     } while (0)
 #endif
+
+// NVTX range per build/apply phase (SURVEY.md sec. 5 tracing); near-free without a tool attached.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // ------------------------------------------------------------------ memory
 // Stream-ordered device allocation with the test-only allocation limit.
