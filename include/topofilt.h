@@ -175,9 +175,10 @@ TF_API tf_status tf_sensitivity_filter_host(tf_filter h, const double *x_host, c
                                      double *out_host, void *stream);
 TF_API tf_status tf_density_filter_host(tf_filter h, const double *x_host, double *out_host,
                                         void *stream);
-/* One optimisation iteration's filtering on host buffers: uploads x and dc once, runs the
- * sensitivity and the density filter, and overlaps the download of the sensitivity result
- * (on a handle-owned side stream) with the density kernel. Synchronises before returning. */
+/* One optimisation iteration's filtering on host buffers: uploads x once for both filters,
+ * runs the density filter while dc uploads (handle-owned side stream), the sensitivity filter
+ * while the density result downloads, then downloads the sensitivity result. Synchronises
+ * before returning. Not safe to call concurrently on the same handle. */
 TF_API tf_status tf_filter_iteration_host(tf_filter h, const double *x_host, const double *dc_host,
                                           double *sens_host, double *dens_host, void *stream);
 

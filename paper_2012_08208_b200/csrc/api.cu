@@ -104,12 +104,13 @@ static void destroy(tf_filter_s *h) {
     if (h->plan.wlo) cudaFreeAsync(h->plan.wlo, 0);
     if (h->stencil_off) cudaFreeAsync(h->stencil_off, 0);
     if (h->stencil_w) cudaFreeAsync(h->stencil_w, 0);
-    cudaFree(h->hx);
-    cudaFree(h->hdc);
-    cudaFree(h->hout);
-    cudaFree(h->hout2);
+    if (h->hx) cudaFreeAsync(h->hx, 0);
+    if (h->hdc) cudaFreeAsync(h->hdc, 0);
+    if (h->hout) cudaFreeAsync(h->hout, 0);
+    if (h->hout2) cudaFreeAsync(h->hout2, 0);
     if (h->side) cudaStreamDestroy(h->side);
     if (h->ev) cudaEventDestroy(h->ev);
+    if (h->ev2) cudaEventDestroy(h->ev2);
     delete h;
 }
 
@@ -315,12 +316,16 @@ tf_status tf_density_filter(tf_filter h, const double *x, double *out, void *str
     return launch_density(h, x, out, (cudaStream_t)stream);
 }
 
-static tf_status ensure_host_scratch(tf_filter h) {
-    if (h->hx) return TF_OK;
+// Device staging for the *_host calls: stream-ordered pool allocations on the caller's stream
+// (every later use is on that stream or on the side stream after an event recorded on it).
+static tf_status ensure_host_scratch(tf_filter h, cudaStream_t s, bool second_out) {
     const size_t bytes = (size_t)h->n * sizeof(double);
-    TF_CUDA_TRY(cudaMalloc(&h->hx, bytes));
-    TF_CUDA_TRY(cudaMalloc(&h->hdc, bytes));
-    TF_CUDA_TRY(cudaMalloc(&h->hout, bytes));
+    if (!h->hx) {
+        TF_TRY(dev_alloc((void **)&h->hx, bytes, s, "host-path staging x"));
+        TF_TRY(dev_alloc((void **)&h->hdc, bytes, s, "host-path staging dc"));
+        TF_TRY(dev_alloc((void **)&h->hout, bytes, s, "host-path staging out"));
+    }
+    if (second_out && !h->hout2) TF_TRY(dev_alloc((void **)&h->hout2, bytes, s, "host-path staging out2"));
     return TF_OK;
 }
 
@@ -331,7 +336,7 @@ tf_status tf_sensitivity_filter_host(tf_filter h, const double *x_host, const do
         return TF_ERR_INVALID;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    TF_TRY(ensure_host_scratch(h));
+    TF_TRY(ensure_host_scratch(h, s, false));
     const size_t bytes = (size_t)h->n * sizeof(double);
     TF_CUDA_TRY(cudaMemcpyAsync(h->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
     TF_CUDA_TRY(cudaMemcpyAsync(h->hdc, dc_host, bytes, cudaMemcpyHostToDevice, s));
@@ -348,21 +353,25 @@ tf_status tf_filter_iteration_host(tf_filter h, const double *x_host, const doub
         return TF_ERR_INVALID;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    TF_TRY(ensure_host_scratch(h));
-    if (!h->hout2) TF_CUDA_TRY(cudaMalloc(&h->hout2, (size_t)h->n * sizeof(double)));
+    TF_TRY(ensure_host_scratch(h, s, true));
     if (!h->side) TF_CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     if (!h->ev) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev, cudaEventDisableTiming));
+    if (!h->ev2) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev2, cudaEventDisableTiming));
     const size_t bytes = (size_t)h->n * sizeof(double);
-    // x and dc go up once for both filters
+    // x goes up once for both filters; the density filter (needs only x) runs while dc uploads
+    // on the side stream; the density result drains while the sensitivity filter runs
     TF_CUDA_TRY(cudaMemcpyAsync(h->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
-    TF_CUDA_TRY(cudaMemcpyAsync(h->hdc, dc_host, bytes, cudaMemcpyHostToDevice, s));
-    TF_TRY(launch_sensitivity(h, h->hx, h->hdc, h->hout, s));
-    // the sensitivity result drains on the side stream while the density filter runs
-    TF_CUDA_TRY(cudaEventRecord(h->ev, s));
+    TF_CUDA_TRY(cudaEventRecord(h->ev, s));  // (orders the side stream after earlier work on s)
     TF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev, 0));
-    TF_CUDA_TRY(cudaMemcpyAsync(sens_host, h->hout, bytes, cudaMemcpyDeviceToHost, h->side));
+    TF_CUDA_TRY(cudaMemcpyAsync(h->hdc, dc_host, bytes, cudaMemcpyHostToDevice, h->side));
+    TF_CUDA_TRY(cudaEventRecord(h->ev2, h->side));  // dc is on the device
     TF_TRY(launch_density(h, h->hx, h->hout2, s));
-    TF_CUDA_TRY(cudaMemcpyAsync(dens_host, h->hout2, bytes, cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaEventRecord(h->ev, s));  // (a wait binds the record made before it)
+    TF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev, 0));
+    TF_CUDA_TRY(cudaMemcpyAsync(dens_host, h->hout2, bytes, cudaMemcpyDeviceToHost, h->side));
+    TF_CUDA_TRY(cudaStreamWaitEvent(s, h->ev2, 0));
+    TF_TRY(launch_sensitivity(h, h->hx, h->hdc, h->hout, s));
+    TF_CUDA_TRY(cudaMemcpyAsync(sens_host, h->hout, bytes, cudaMemcpyDeviceToHost, s));
     TF_CUDA_TRY(cudaStreamSynchronize(h->side));
     TF_CUDA_TRY(cudaStreamSynchronize(s));
     return TF_OK;
@@ -374,7 +383,7 @@ tf_status tf_density_filter_host(tf_filter h, const double *x_host, double *out_
         return TF_ERR_INVALID;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    TF_TRY(ensure_host_scratch(h));
+    TF_TRY(ensure_host_scratch(h, s, false));
     const size_t bytes = (size_t)h->n * sizeof(double);
     TF_CUDA_TRY(cudaMemcpyAsync(h->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
     TF_TRY(launch_density(h, h->hx, h->hout, s));

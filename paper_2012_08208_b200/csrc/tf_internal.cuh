@@ -172,7 +172,7 @@ struct tf_filter_s {
     // host-API scratch (lazily allocated, owned) + a side stream / event for copy overlap
     double *hx = nullptr, *hdc = nullptr, *hout = nullptr, *hout2 = nullptr;
     cudaStream_t side = nullptr;
-    cudaEvent_t ev = nullptr;
+    cudaEvent_t ev = nullptr, ev2 = nullptr;
     // matrix-free stencil handles (tf_build_stencil): no CSR; offset table on the device
     tf::StencilGeom stencil;
     int4 *stencil_off = nullptr;
