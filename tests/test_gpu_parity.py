@@ -163,6 +163,42 @@ def test_config5_sampled_rows(tf):
     del rid, first, asc, diag
 
 
+def test_nnz_beyond_int32(tf):
+    """Maximum-size case: 28.8M Kuhn tets (300x160x100 cubes) give nnz = 2,479,728,752 > 2^31
+    (exact lattice count), so every element offset past 2^31 goes through the int64 paths of
+    the fill, the apply plan and the TMA window addresses. Checked: nnz against the closed
+    form; 3,000 seeded rows plus the rows straddling element 2^31 and the last rows bit-exact
+    against the oracle; both filters at those rows; ascending columns over the whole CSR."""
+    c = synth.kuhn_tets(300, 160, 100)
+    n, rmin = c.shape[0], 1.5
+    f = tf.tf_build_filter(dev(c), rmin)
+    assert f.nnz == 2_479_728_752 > 2**31
+    rowptr, colsd, _, _ = f.csr()
+    r31 = int(torch.searchsorted(rowptr, torch.tensor([2**31], device="cuda"), right=True).item()) - 1
+    assert rowptr[r31] <= 2**31 < rowptr[r31 + 1]
+    extra = np.concatenate([np.arange(r31 - 2, r31 + 3), np.arange(n - 50, n)])
+    rows = np.unique(np.concatenate([synth.sample_rows(6, n, 3000), extra]))
+    cl = oracle.CellList(c, rmin)
+    ref = cl.rows(rows)
+    cl.close()
+    rp, cols, vals, hs = _sampled(f, rows)
+    np.testing.assert_array_equal(rp, ref.rowptr)
+    np.testing.assert_array_equal(cols, ref.cols)
+    np.testing.assert_array_equal(vals, ref.vals)
+    assert_rel(hs, ref.hs, RTOL_HS, "Hs")
+    x, dc = inputs_for(n, 611)
+    rt = torch.from_numpy(rows).cuda()
+    s = f.sensitivity(dev(x), dev(dc))[rt].cpu().numpy()
+    d = f.density(dev(x))[rt].cpu().numpy()
+    assert_rel(s, oracle.apply_sensitivity(ref, x, dc), RTOL_OUT, "sensitivity")
+    assert_rel(d, oracle.apply_density(ref, x), RTOL_OUT, "density")
+    first = torch.zeros(f.nnz, dtype=torch.bool, device="cuda")
+    first[rowptr[:-1]] = True
+    assert bool(((colsd[1:] > colsd[:-1]) | first[1:]).all())
+    del first, rowptr, colsd
+    f.close()
+
+
 # ------------------------------------------------------------------ fp-decided and paper workloads
 
 @pytest.mark.parametrize("name,c,rmin", [
