@@ -136,6 +136,69 @@ def kuhn_tets(nx: int, ny: int, nz: int) -> np.ndarray:
     return out.reshape(ncube * 6, 3)
 
 
+def tri_mesh(nx: int, ny: int, pattern: str = "right", jitter: float = 0.0, stream: int = 0):
+    """Nodes and cells of the tri_grid triangulation (same cell order and vertex order, so the
+    vertex means are tri_grid's centroids when jitter = 0). Node index j*(nx+1) + i at (i, j);
+    `jitter` > 0 moves every interior node by U(-jitter, jitter) per component (stream)."""
+    J, I = np.meshgrid(np.arange(ny + 1), np.arange(nx + 1), indexing="ij")
+    nodes = np.stack([I.ravel(), J.ravel()], axis=1).astype(np.float64)
+    j, i = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+    i = i.ravel()
+    j = j.ravel()
+    v = lambda a, b: b * (nx + 1) + a  # noqa: E731
+    r0 = (v(i, j), v(i + 1, j), v(i + 1, j + 1))
+    r1 = (v(i, j), v(i + 1, j + 1), v(i, j + 1))
+    l0 = (v(i, j), v(i + 1, j), v(i, j + 1))
+    l1 = (v(i + 1, j), v(i + 1, j + 1), v(i, j + 1))
+    if pattern == "right":
+        t0, t1 = r0, r1
+    elif pattern == "left":
+        t0, t1 = l0, l1
+    elif pattern in ("right/left", "alternate"):
+        even = ((i + j) % 2) == 0
+        t0 = tuple(np.where(even, a, b) for a, b in zip(r0, l0))
+        t1 = tuple(np.where(even, a, b) for a, b in zip(r1, l1))
+    else:
+        raise ValueError(pattern)
+    cells = np.empty((i.size * 2, 3), dtype=np.int32)
+    cells[0::2] = np.stack(t0, axis=1)
+    cells[1::2] = np.stack(t1, axis=1)
+    if jitter > 0:
+        _jitter_interior(nodes, [nx, ny], jitter, stream)
+    return nodes, cells
+
+
+def kuhn_mesh(nx: int, ny: int, nz: int, jitter: float = 0.0, stream: int = 0):
+    """Nodes and cells of kuhn_tets (same cell and vertex order: v0, v1 = v0+e_s1,
+    v2 = v1+e_s2, v3 = v0+(1,1,1)). Node index (k*(ny+1) + j)*(nx+1) + i at (i, j, k)."""
+    K, J, I = np.meshgrid(np.arange(nz + 1), np.arange(ny + 1), np.arange(nx + 1), indexing="ij")
+    nodes = np.stack([I.ravel(), J.ravel(), K.ravel()], axis=1).astype(np.float64)
+    k, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    base = np.stack([i.ravel(), j.ravel(), k.ravel()], axis=1)
+    node = lambda p: (p[:, 2] * (ny + 1) + p[:, 1]) * (nx + 1) + p[:, 0]  # noqa: E731
+    cells = np.empty((base.shape[0], 6, 4), dtype=np.int32)
+    for t, s in enumerate(_PERMS):
+        e1 = np.zeros(3, dtype=np.int64)
+        e1[s[0]] = 1
+        e2 = np.zeros(3, dtype=np.int64)
+        e2[s[1]] = 1
+        cells[:, t, 0] = node(base)
+        cells[:, t, 1] = node(base + e1)
+        cells[:, t, 2] = node(base + e1 + e2)
+        cells[:, t, 3] = node(base + 1)
+    if jitter > 0:
+        _jitter_interior(nodes, [nx, ny, nz], jitter, stream)
+    return nodes, cells.reshape(-1, 4)
+
+
+def _jitter_interior(nodes, n, jitter, stream):
+    inner = np.ones(nodes.shape[0], dtype=bool)
+    for d, nd in enumerate(n):
+        inner &= (nodes[:, d] > 0) & (nodes[:, d] < nd)
+    m = int(inner.sum())
+    nodes[inner] += uniform(stream, 0, m * len(n), -jitter, jitter).reshape(m, len(n))
+
+
 def ground_structure(config: int = 4, nx: int = 2000, ny: int = 1000):
     """Config 4: jittered 2D grid with 5 seeded circular holes and an L-bracket cut-out.
 
