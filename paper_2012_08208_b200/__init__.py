@@ -29,6 +29,9 @@ EXPORTS = [
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
     "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update", "tf_sensitivity_filter_energy",
     "tf_filter_iteration_host",
+    # include/topofilt_helmholtz.h (NEXT-3)
+    "tf_helmholtz_build", "tf_helmholtz_filter", "tf_helmholtz_sensitivity", "tf_helmholtz_view",
+    "tf_helmholtz_free",
 ]
 
 
@@ -48,6 +51,17 @@ class tf_build_info(ctypes.Structure):
     _fields_ = [("bin_side", ctypes.c_double), ("bins", ctypes.c_int64 * 3), ("nbins", ctypes.c_int64),
                 ("max_candidates", ctypes.c_int64), ("large_rows", ctypes.c_int64),
                 ("radix_passes", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class tf_helmholtz_info(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("converged", ctypes.c_int32), ("rel_residual", ctypes.c_double)]
+
+
+class tf_helmholtz_system(ctypes.Structure):
+    _fields_ = [("n_nodes", ctypes.c_int64), ("n_cells", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("dim", ctypes.c_int32), ("R", ctypes.c_double), ("rowptr", ctypes.c_void_p),
+                ("cols", ctypes.c_void_p), ("vals_A", ctypes.c_void_p), ("vals_M", ctypes.c_void_p),
+                ("node_weight", ctypes.c_void_p), ("cell_volume", ctypes.c_void_p)]
 
 
 def _load():
@@ -77,6 +91,11 @@ def _load():
         "tf_oc_update": ([P, P, I64, D, D, D, D, D, P, P, P, P], I32),
         "tf_sensitivity_filter_energy": ([P, P, P, D, P, P], I32),
         "tf_filter_iteration_host": ([P, P, P, P, P, P], I32),
+        "tf_helmholtz_build": ([P, I64, P, I64, I32, D, P, PP], I32),
+        "tf_helmholtz_filter": ([P, P, P, D, I32, P, P], I32),
+        "tf_helmholtz_sensitivity": ([P, P, P, P, D, I32, P, P], I32),
+        "tf_helmholtz_view": ([P, ctypes.POINTER(tf_helmholtz_system)], I32),
+        "tf_helmholtz_free": ([P], None),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -346,3 +365,96 @@ def tf_oc_update(x, dc, volfrac: float, move: float = 0.2, l1: float = 0.0, l2: 
                              float(move), float(l1), float(l2), float(tol), _dptr(x_new, "x_new", torch.float64, n),
                              _dptr(lm, "lmid"), ctypes.c_void_p(it.data_ptr()), _stream_ptr(stream)))
     return x_new, lm, it
+
+
+# ------------------------------------------------------------------ NEXT-3: Helmholtz PDE filter
+
+def helmholtz_radius(rmin: float) -> float:
+    """R = rmin / (2 sqrt 3) (R17)."""
+    return float(rmin) / (2.0 * 3.0 ** 0.5)
+
+
+class Helmholtz:
+    """A built Helmholtz filter (owns a tf_helmholtz handle; include/topofilt_helmholtz.h).
+    Calls on one handle share its CG scratch: keep them on one stream."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self._h = handle
+        v = tf_helmholtz_system()
+        _check(_lib.tf_helmholtz_view(self._h, ctypes.byref(v)))
+        self._v = v
+        self.n_nodes, self.n_cells, self.nnz, self.dim, self.R = v.n_nodes, v.n_cells, v.nnz, v.dim, v.R
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("Helmholtz filter is closed")
+        return self._h
+
+    def _info(self, device):
+        import torch
+        return torch.zeros(2, dtype=torch.float64, device=device)  # 16 bytes = tf_helmholtz_info
+
+    @staticmethod
+    def decode_info(t) -> dict:
+        """(iterations, converged, rel_residual) from the 16-byte info tensor (synchronises)."""
+        raw = t.cpu().numpy().tobytes()
+        info = tf_helmholtz_info.from_buffer_copy(raw)
+        return {"iterations": info.iterations, "converged": bool(info.converged), "rel_residual": info.rel_residual}
+
+    def filter(self, sigma, out=None, rtol: float = 1e-12, maxit: int = 1000, info=None, stream=None):
+        """s~ = Helmholtz(sigma) over cells. Returns (out, info tensor)."""
+        import torch
+        if out is None:
+            out = torch.empty_like(sigma)
+        if info is None:
+            info = self._info(sigma.device)
+        _check(_lib.tf_helmholtz_filter(self.handle, _dptr(sigma, "sigma", torch.float64, self.n_cells),
+                                        _dptr(out, "out", torch.float64, self.n_cells), float(rtol), int(maxit),
+                                        ctypes.c_void_p(info.data_ptr()), _stream_ptr(stream)))
+        return out, info
+
+    def sensitivity(self, x, dc, out=None, rtol: float = 1e-12, maxit: int = 1000, info=None, stream=None):
+        """dc~ = Helmholtz(x∘dc) / max(1e-3, x). Returns (out, info tensor)."""
+        import torch
+        if out is None:
+            out = torch.empty_like(x)
+        if info is None:
+            info = self._info(x.device)
+        _check(_lib.tf_helmholtz_sensitivity(self.handle, _dptr(x, "x", torch.float64, self.n_cells),
+                                             _dptr(dc, "dc", torch.float64, self.n_cells),
+                                             _dptr(out, "out", torch.float64, self.n_cells), float(rtol), int(maxit),
+                                             ctypes.c_void_p(info.data_ptr()), _stream_ptr(stream)))
+        return out, info
+
+    def system(self):
+        """Zero-copy views (rowptr, cols, vals_A, vals_M, node_weight, cell_volume)."""
+        import torch
+        v = self._v
+        mk = lambda p, n, t: torch.as_tensor(_CudaArray(p, (n,), t), device="cuda")  # noqa: E731
+        return (mk(v.rowptr, self.n_nodes + 1, "<i8"), mk(v.cols, self.nnz, "<i4"), mk(v.vals_A, self.nnz, "<f8"),
+                mk(v.vals_M, self.nnz, "<f8"), mk(v.node_weight, self.n_nodes, "<f8"),
+                mk(v.cell_volume, self.n_cells, "<f8"))
+
+    def close(self):
+        if self._h is not None:
+            _lib.tf_helmholtz_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def tf_helmholtz_build(nodes, cells, R: float, stream=None) -> Helmholtz:
+    """Assemble the Helmholtz filter: nodes [Nn, dim] float64, cells [Nc, dim+1] int32 (device)."""
+    import torch
+    if nodes.dim() != 2 or cells.dim() != 2 or cells.shape[1] != nodes.shape[1] + 1:
+        raise ValueError("nodes must be [Nn, dim] and cells [Nc, dim+1]")
+    h = ctypes.c_void_p()
+    _check(_lib.tf_helmholtz_build(_dptr(nodes, "nodes", torch.float64), nodes.shape[0],
+                                   _dptr(cells, "cells", torch.int32), cells.shape[0], nodes.shape[1], float(R),
+                                   _stream_ptr(stream), ctypes.byref(h)))
+    return Helmholtz(h)

@@ -68,7 +68,7 @@ tf_status device_info(DeviceInfo *di) {
 }
 
 // Device (or managed) memory check: host pointers are rejected with TF_ERR_INVALID.
-static tf_status require_device(const void *p, const char *name) {
+tf_status require_device(const void *p, const char *name) {
     if (!p) {
         set_error("%s is NULL", name);
         return TF_ERR_INVALID;

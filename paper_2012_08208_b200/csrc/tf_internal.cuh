@@ -118,6 +118,8 @@ struct DeviceInfo {
     size_t smem_optin = 227 * 1024;
 };
 tf_status device_info(DeviceInfo *di);
+// TF_ERR_INVALID unless p is a non-NULL device (or managed) pointer
+tf_status require_device(const void *p, const char *name);
 
 // ------------------------------------------------------------------ grid of the cell list
 struct Grid {

@@ -11,11 +11,12 @@ import pytest
 import paper_2012_08208_b200 as tf
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "topofilt.h")
+HEADERS = sorted(os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))
+                 if f.endswith(".h"))
 
 
 def declared():
-    src = open(HEADER).read()
+    src = "".join(open(h).read() for h in HEADERS)
     return sorted(set(re.findall(r"TF_API\s+[\w\s\*]*?\b(tf_\w+)\s*\(", src)))
 
 
@@ -101,3 +102,17 @@ def test_no_oracle_in_product():
                 assert "import oracle" not in src and "from oracle" not in src and "oracle.h" not in src
     ldd = subprocess.run(["ldd", tf.LIB_PATH], capture_output=True, text=True).stdout
     assert "oracle" not in ldd
+
+
+@pytest.mark.parametrize("nn,nc,dim,R,frag", [
+    (10, 5, 4, 1.0, "dim"), (0, 5, 2, 1.0, "n_nodes"), (2 ** 31, 5, 3, 1.0, "n_nodes"), (10, 0, 2, 1.0, "n_nodes"),
+    (10, 5, 2, -1.0, "R must"), (10, 5, 3, float("nan"), "R must"), (10, 5, 2, float("inf"), "R must"),
+    (10, 2 ** 27, 3, 1.0, "2^31"),
+])
+def test_helmholtz_build_rejects_bad_args(nn, nc, dim, R, frag):
+    """NEXT-3 argument validation happens before any CUDA call."""
+    h = ctypes.c_void_p()
+    st = tf.lib().tf_helmholtz_build(None, nn, None, nc, dim, R, None, ctypes.byref(h))
+    assert st in (tf.TF_ERR_INVALID, tf.TF_ERR_OVERFLOW)
+    assert frag in tf.lib().tf_last_error().decode()
+    assert not h.value

@@ -12,7 +12,7 @@ import pytest
 from oracle import helmholtz as hz
 import synth
 
-GOLD = os.path.join(os.path.dirname(__file__), "golden")
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "helmholtz")
 
 
 def load(name):
