@@ -17,10 +17,13 @@
 //   P1  b = M s_n, r = b - A u, z = D^-1 r, p_old = 0;   dots (b.b, r.z, r.r)
 //   loop:  PA  p = z + beta p_old (row owner), q = A p computed from z and p_old directly
 //              (q_a = sum_b A_ab (z_b + beta p_old_b): no separate p pass, so two grid
-//              syncs per iteration instead of three);   dot p.q
-//          PB  u += alpha p, r -= alpha q, z = D^-1 r;   dots (r.z, r.r)
+//              syncs per iteration instead of three; z and p_old are stored interleaved so
+//              each entry costs one 16-byte gather);   dot p.q
+//          PB  u += alpha p, r -= alpha q, z = D^-1 r, store (z, p);   dots (r.z, r.r)
 //   P2  s~_c = mean of u over the cell's nodes (/ max(1e-3, x_c) for the sensitivity use)
-// CSR rows use 4 lanes each (3D rows hold ~15 entries, 2D ~7).
+// CSR rows and incidence lists use 2 lanes x 4 loads in flight; 5 blocks/SM (48 registers).
+// Swept on config 5 (tools/helm_probe.py): per CG iteration 120 us at (2, 4, 5) vs 164 at
+// (4, 4, -), 151 at (1, 8, -), 205 at (2, 2, -); more registers cost more than they hide.
 #include <cooperative_groups.h>
 #include <math.h>
 
@@ -42,7 +45,7 @@ struct tf_helmholtz_s {
     int32_t *cols = nullptr;      // [nnz]
     double *valA = nullptr, *valM = nullptr;  // [nnz]
     double *dinv = nullptr;       // [nn] 1/A_aa (0 on empty rows)
-    double *vec = nullptr;        // [7*nn] CG scratch: sn, u, r, z, q, p0, p1
+    double *vec = nullptr;        // [7*nn] CG scratch: (z,p) pairs, sn, u, r, q, p_new
     double *parts = nullptr;      // [2 * grid * 4] block partials
     int grid = 0;
 };
@@ -51,7 +54,19 @@ namespace tf {
 namespace {
 
 constexpr int kHzThreads = 256;
-constexpr int kRowLanes = 4;
+// lanes per CSR row / incidence list, and loads each lane issues before its gathers
+// (tuning macros for tools/variant_sweep.py)
+#ifndef TF_HZ_LANES
+#define TF_HZ_LANES 2
+#endif
+#ifndef TF_HZ_UNROLL
+#define TF_HZ_UNROLL 4
+#endif
+#ifndef TF_HZ_MINB
+#define TF_HZ_MINB 5
+#endif
+constexpr int kRowLanes = TF_HZ_LANES;
+constexpr int kUnroll = TF_HZ_UNROLL;
 
 int ceil_log2_i64(int64_t v) {
     int b = 0;
@@ -288,7 +303,8 @@ struct HzArgs {
     const int64_t *rowptr;
     const int32_t *cols;
     const double *valA, *valM, *dinv;
-    double *sn, *u, *r, *z, *q, *p0, *p1;
+    double2 *zp;  // (z, p) interleaved: one 16-byte gather per entry in the SpMV
+    double *sn, *u, *r, *q, *pn;
     double *parts;
     int64_t nn, nc;
     const double *sigma;  // filter input (SENS: unused)
@@ -300,7 +316,7 @@ struct HzArgs {
 };
 
 template <int D, bool SENS>
-__global__ void __launch_bounds__(kHzThreads) k_hz_apply(HzArgs A) {
+__global__ void __launch_bounds__(kHzThreads, TF_HZ_MINB) k_hz_apply(HzArgs A) {
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     __shared__ double sm3[kHzThreads / 32][3];
     __shared__ double sm2[kHzThreads / 32][2];
@@ -312,31 +328,61 @@ __global__ void __launch_bounds__(kHzThreads) k_hz_apply(HzArgs A) {
     const int64_t rgid = gid / kRowLanes, RT = T / kRowLanes;
     const int64_t rounds = (nn + RT - 1) / RT;  // warp-uniform row loop (shuffles inside)
 
-    // P0: projection
-    for (int64_t a = gid; a < nn; a += T) {
+    // P0: projection (kRowLanes lanes per node over its incident cells, ascending per lane)
+    for (int64_t it = 0; it < rounds; ++it) {
+        const int64_t a = it * RT + rgid;
         double s = 0.0;
-        for (int64_t j = A.inc_ptr[a]; j < A.inc_ptr[a + 1]; ++j) {
-            const int32_t c = A.inc_cell[j];
-            const double sc = SENS ? A.x[c] * A.dc[c] : A.sigma[c];
-            s += A.vol[c] * sc;
+        if (a < nn) {
+            const int64_t j0 = A.inc_ptr[a], j1 = A.inc_ptr[a + 1];
+            for (int64_t jb = j0 + g; jb < j1; jb += kRowLanes * kUnroll) {
+                int32_t c[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int64_t j = jb + (int64_t)u * kRowLanes;
+                    c[u] = (j < j1) ? A.inc_cell[j] : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    if (c[u] >= 0) {
+                        const double sc = SENS ? A.x[c[u]] * A.dc[c[u]] : A.sigma[c[u]];
+                        s += A.vol[c[u]] * sc;
+                    }
+                }
+            }
         }
-        const double w = A.W[a];
-        const double v = (w > 0.0) ? s / w : 0.0;
-        A.sn[a] = v;
-        A.u[a] = v;
+        for (int o = 1; o < kRowLanes; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (a < nn && g == 0) {
+            const double w = A.W[a];
+            const double v = (w > 0.0) ? s / w : 0.0;
+            A.sn[a] = v;
+            A.u[a] = v;
+        }
     }
     grid.sync();
-    // P1: b = M sn, r = b - A u, z = D^-1 r, p0 = 0
+    // P1: b = M sn, r = b - A u, z = D^-1 r, p_old = 0
     double d3[3] = {0.0, 0.0, 0.0};  // b.b, r.z, r.r
     for (int64_t it = 0; it < rounds; ++it) {
         const int64_t a = it * RT + rgid;
         double bm = 0.0, au = 0.0;
         if (a < nn) {
-            for (int64_t k = A.rowptr[a] + g; k < A.rowptr[a + 1]; k += kRowLanes) {
-                const int32_t col = A.cols[k];
-                const double s = __ldcg(A.sn + col);
-                bm += A.valM[k] * s;
-                au += A.valA[k] * s;  // u = sn here
+            const int64_t k0 = A.rowptr[a], k1 = A.rowptr[a + 1];
+            for (int64_t kb = k0 + g; kb < k1; kb += kRowLanes * kUnroll) {
+                int32_t c[kUnroll];
+                double vm[kUnroll], va[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int64_t k = kb + (int64_t)u * kRowLanes;
+                    const bool ok = k < k1;
+                    c[u] = ok ? A.cols[k] : (int32_t)a;
+                    vm[u] = ok ? A.valM[k] : 0.0;
+                    va[u] = ok ? A.valA[k] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const double sv = __ldcg(A.sn + c[u]);
+                    bm += vm[u] * sv;
+                    au += va[u] * sv;  // u = sn here
+                }
             }
         }
         for (int o = 1; o < kRowLanes; o <<= 1) {
@@ -347,8 +393,7 @@ __global__ void __launch_bounds__(kHzThreads) k_hz_apply(HzArgs A) {
             const double rr = bm - au;
             const double zz = A.dinv[a] * rr;
             A.r[a] = rr;
-            A.z[a] = zz;
-            A.p0[a] = 0.0;
+            A.zp[a] = make_double2(zz, 0.0);  // p_old = 0
             d3[0] += bm * bm;
             d3[1] += rr * zz;
             d3[2] += rr * rr;
@@ -362,23 +407,37 @@ __global__ void __launch_bounds__(kHzThreads) k_hz_apply(HzArgs A) {
     bool conv = rr <= A.rtol2 * bb;
     double beta = 0.0;
     int iters = 0;
-    double *pold = A.p0, *pnew = A.p1;
     while (!conv && iters < A.maxit) {
-        // PA: p = z + beta p_old (owner), q = A (z + beta p_old)
+        // PA: p = z + beta p_old (owner), q = A (z + beta p_old); each lane loads up to
+        // kUnroll (col, val) pairs before the gathers (memory-level parallelism)
         double d1[1] = {0.0};
         for (int64_t it = 0; it < rounds; ++it) {
             const int64_t a = it * RT + rgid;
             double qa = 0.0;
             if (a < nn) {
-                for (int64_t k = A.rowptr[a] + g; k < A.rowptr[a + 1]; k += kRowLanes) {
-                    const int32_t col = A.cols[k];
-                    qa += A.valA[k] * (__ldcg(A.z + col) + beta * __ldcg(pold + col));
+                const int64_t k0 = A.rowptr[a], k1 = A.rowptr[a + 1];
+                for (int64_t kb = k0 + g; kb < k1; kb += kRowLanes * kUnroll) {
+                    int32_t c[kUnroll];
+                    double v[kUnroll];
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u) {
+                        const int64_t k = kb + (int64_t)u * kRowLanes;
+                        const bool ok = k < k1;
+                        c[u] = ok ? A.cols[k] : (int32_t)a;
+                        v[u] = ok ? A.valA[k] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u) {
+                        const double2 t = __ldcg(A.zp + c[u]);
+                        qa += v[u] * (t.x + beta * t.y);
+                    }
                 }
             }
             for (int o = 1; o < kRowLanes; o <<= 1) qa += __shfl_xor_sync(0xffffffffu, qa, o);
             if (a < nn && g == 0) {
-                const double pa = __ldcg(A.z + a) + beta * __ldcg(pold + a);
-                pnew[a] = pa;
+                const double2 t = __ldcg(A.zp + a);
+                const double pa = t.x + beta * t.y;
+                A.pn[a] = pa;
                 A.q[a] = qa;
                 d1[0] += pa * qa;
             }
@@ -386,15 +445,15 @@ __global__ void __launch_bounds__(kHzThreads) k_hz_apply(HzArgs A) {
         grid_sum<1>(d1, sm1, A.parts, slot, grid);
         slot ^= 1;
         const double alpha = rz / d1[0];
-        // PB: u += alpha p, r -= alpha q, z = D^-1 r
+        // PB: u += alpha p, r -= alpha q, z = D^-1 r; (z, p) stored as the next PA's pair
         double d2[2] = {0.0, 0.0};
         for (int64_t a = gid; a < nn; a += T) {
-            const double pa = __ldcg(pnew + a);
+            const double pa = __ldcg(A.pn + a);
             A.u[a] = __ldcg(A.u + a) + alpha * pa;
             const double ra = __ldcg(A.r + a) - alpha * __ldcg(A.q + a);
             const double za = A.dinv[a] * ra;
             A.r[a] = ra;
-            A.z[a] = za;
+            A.zp[a] = make_double2(za, pa);
             d2[0] += ra * za;
             d2[1] += ra * ra;
         }
@@ -405,9 +464,6 @@ __global__ void __launch_bounds__(kHzThreads) k_hz_apply(HzArgs A) {
         rz = d2[0];
         rr = d2[1];
         conv = rr <= A.rtol2 * bb;
-        double *t = pold;
-        pold = pnew;
-        pnew = t;
     }
     // P2: nodal mean per cell (u was last written before the final grid_sum's sync)
     for (int64_t c = gid; c < A.nc; c += T) {
@@ -432,8 +488,9 @@ tf_status hz_launch(tf_helmholtz_s *h, const double *sigma, const double *x, con
     A.cells = h->cells, A.vol = h->vol, A.inc_ptr = h->inc_ptr, A.inc_cell = h->inc_cell, A.W = h->W;
     A.rowptr = h->rowptr, A.cols = h->cols, A.valA = h->valA, A.valM = h->valM, A.dinv = h->dinv;
     const int64_t nn = h->nn;
-    A.sn = h->vec, A.u = h->vec + nn, A.r = h->vec + 2 * nn, A.z = h->vec + 3 * nn, A.q = h->vec + 4 * nn;
-    A.p0 = h->vec + 5 * nn, A.p1 = h->vec + 6 * nn;
+    A.zp = reinterpret_cast<double2 *>(h->vec);  // first: 16-byte aligned
+    A.sn = h->vec + 2 * nn, A.u = h->vec + 3 * nn, A.r = h->vec + 4 * nn, A.q = h->vec + 5 * nn;
+    A.pn = h->vec + 6 * nn;
     A.parts = h->parts, A.nn = nn, A.nc = h->nc;
     A.sigma = sigma, A.x = x, A.dc = dc, A.out = out;
     A.rtol2 = rtol * rtol, A.maxit = maxit, A.info = info;
@@ -448,12 +505,16 @@ tf_status hz_launch(tf_helmholtz_s *h, const double *sigma, const double *x, con
     return TF_OK;
 }
 
+// Co-resident maximum, but no more blocks than the node rows need (small meshes are bound by
+// the grid syncs, whose cost grows with the block count); at least one block per SM.
 template <int D>
-int hz_grid(const DeviceInfo &di) {
+int hz_grid(const DeviceInfo &di, int64_t nn) {
     int o1 = 0, o2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_hz_apply<D, false>, kHzThreads, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_hz_apply<D, true>, kHzThreads, 0);
-    return di.sms * std::max(1, std::min(std::min(o1, o2), 4));
+    const int64_t full = (int64_t)di.sms * std::max(1, std::min(std::min(o1, o2), 8));
+    const int64_t need = (nn * kRowLanes + kHzThreads - 1) / kHzThreads;
+    return (int)std::max<int64_t>(std::min<int64_t>(full, need), std::min<int64_t>(full, di.sms));
 }
 
 void hz_destroy(tf_helmholtz_s *h) {
@@ -571,7 +632,7 @@ tf_status hz_build(const double *nodes, int64_t nn, const int32_t *cells, int64_
     TF_TRY(dalloc(&h->dinv, (size_t)nn, s, "helmholtz diag"));
     k_hz_diag<<<blocks(nn), threads, 0, s>>>(h->rowptr, h->cols, h->valA, nn, h->dinv);
     TF_LAUNCH_CHECK();
-    h->grid = hz_grid<D>(di);
+    h->grid = hz_grid<D>(di, nn);
     TF_TRY(dalloc(&h->vec, (size_t)7 * nn, s, "helmholtz CG vectors"));
     TF_TRY(dalloc(&h->parts, (size_t)2 * h->grid * 4, s, "helmholtz partials"));
     TF_CUDA_TRY(cudaStreamSynchronize(s));  // h2d of nnz above reads a host stack value

@@ -164,7 +164,47 @@ def oc_rows():
                           "gbs": bytes_ / t / 1e9, "frac_8tbs": bytes_ / t / 1e9 / HBM}), flush=True)
 
 
+def helmholtz_rows():
+    """NEXT-3 Helmholtz filter (sensitivity use, rtol 1e-12) on the config-2 and config-5 meshes:
+    build ms, solve us, CG iterations, and bytes per CG iteration (CSR 12 B/nnz + 8 B/row,
+    vectors 104 B/node: z and p_old gathered once per node, p and q written; u, r, q, p, dinv
+    read and u, r, z written in the update) against the 8 TB/s roofline."""
+    dev = torch.device("cuda:0")
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+    for cfg, (nodes, cells), rmin in ((2, synth.tri_mesh(300, 100, "right"), 2.5),
+                                      (5, synth.kuhn_mesh(200, 100, 100), 1.5)):
+        n = cells.shape[0]
+        R = tf.helmholtz_radius(rmin)
+        nd, cd = torch.from_numpy(nodes).to(dev), torch.from_numpy(cells).to(dev)
+        x = torch.from_numpy(synth.density(cfg, n)).to(dev)
+        dc = torch.from_numpy(synth.sensitivity(cfg, synth.density(cfg, n))).to(dev)
+        tf.tf_helmholtz_build(nd, cd, R).close()
+        holder = {}
+
+        def build():
+            holder["h"] = tf.tf_helmholtz_build(nd, cd, R)
+        tb = timed(build, 3)
+        h = holder["h"]
+        out = torch.empty_like(x)
+        info = h._info(dev)
+        h.sensitivity(x, dc, out=out, info=info)
+        t = timed(lambda: h.sensitivity(x, dc, out=out, info=info), 10, flush=flush)
+        inf = h.decode_info(info)
+        it = inf["iterations"]
+        per_it = 12 * h.nnz + 8 * h.n_nodes + 104 * h.n_nodes
+        print(json.dumps({"helmholtz_config": cfg, "cells": n, "nodes": h.n_nodes, "nnz": h.nnz, "R": R,
+                          "build_ms": tb * 1e3, "solve_us_cold": t * 1e6, "iterations": it,
+                          "rel_residual": inf["rel_residual"], "us_per_iteration": t * 1e6 / max(1, it),
+                          "bytes_per_iteration": per_it,
+                          "iteration_gbs": per_it * it / t / 1e9 if it else None,
+                          "iteration_frac_8tbs": per_it * it / t / 1e9 / HBM if it else None}), flush=True)
+        h.close()
+
+
 if __name__ == "__main__":
+    if os.environ.get("HELM_ONLY"):
+        helmholtz_rows()
+        sys.exit(0)
     if os.environ.get("OC_ONLY"):
         oc_rows()
         sys.exit(0)
@@ -176,3 +216,4 @@ if __name__ == "__main__":
     stencil_rows()
     graph_rows()
     oc_rows()
+    helmholtz_rows()
