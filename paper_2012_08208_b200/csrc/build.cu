@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(256) k_binstats(const int32_t *__restrict__ cs
 }
 
 // ------------------------------------------------------------------ a5: count pass
+
 // Block per query bin, WARPS warps, one warp per query. The bin's candidates (the 3^(dim-1)
 // contiguous x-triples) are staged once as bin-local fp32 SoA (padded with far sentinels to
 // a multiple of 64) plus their sorted position for the rare exact re-test; each query sweeps
@@ -350,32 +351,48 @@ __global__ void __launch_bounds__(WARPS * 32) k_count(SortedPts P, Grid g, int c
         const float t_in = g.t_in, t_out = g.t_out;
         const f2u *X2 = reinterpret_cast<const f2u *>(FX), *Y2 = reinterpret_cast<const f2u *>(FY),
                   *Z2 = reinterpret_cast<const f2u *>(FZ);
-        for (int q = q0 + warp; q < q1; q += WARPS) {
-            const double qx = P.x[q], qy = P.y[q], qz = (DIM == 3) ? P.z[q] : 0.0;
-            const float4 fq = local_f32(qx, qy, qz, v);
-            const f2u qx2 = f2_pack(fq.x, fq.x), qy2 = f2_pack(fq.y, fq.y), qz2 = f2_pack(fq.z, fq.z);
-            int cnt = 0;
-            for (int k0 = 0; k0 < CP / 2; k0 += 32) {  // warp-uniform trip count
+        // two queries per warp pass (the second may be absent: far sentinel, never in or band):
+        // the staged candidate pairs are loaded once for both; per-lane counts packed as
+        // lo16 + hi16 (<= 2*32*... < 65536 per lane) into one warp reduction.
+        for (int q = q0 + warp; q < q1; q += 2 * WARPS) {
+            const int qb = q + WARPS;
+            const bool hasb = qb < q1;
+            const double ax = P.x[q], ay = P.y[q], az = (DIM == 3) ? P.z[q] : 0.0;
+            const double bx = hasb ? P.x[qb] : 0.0, by = hasb ? P.y[qb] : 0.0,
+                         bz = (DIM == 3 && hasb) ? P.z[qb] : 0.0;
+            const float4 fa = local_f32(ax, ay, az, v);
+            const float4 fb = hasb ? local_f32(bx, by, bz, v) : make_float4(kFar, kFar, kFar, 0.f);
+            const f2u ax2 = f2_pack(fa.x, fa.x), ay2 = f2_pack(fa.y, fa.y), az2 = f2_pack(fa.z, fa.z);
+            const f2u bx2 = f2_pack(fb.x, fb.x), by2 = f2_pack(fb.y, fb.y), bz2 = f2_pack(fb.z, fb.z);
+            int cnt = 0;  // query a in the low 16 bits, query b in the high 16 bits
+            auto exact = [&](int t, double x, double y, double z) -> bool {
+                const int p = POS[t];
+                return pair_d2<DIM>(x, y, z, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0) < r2;
+            };
+            for (int k0 = 0; k0 < CP / 2; k0 += 32) {
                 const int k = k0 + lane;
-                const f2u d2 = d2_f32x2<DIM>(X2[k], Y2[k], (DIM == 3) ? Z2[k] : 0ull, qx2, qy2, qz2);
-                const float d0 = f2_lo(d2), d1 = f2_hi(d2);
-                const bool in0 = d0 < t_in, in1 = d1 < t_in;
-                cnt += __popc(__ballot_sync(0xffffffffu, in0)) + __popc(__ballot_sync(0xffffffffu, in1));
-                const bool b0 = !in0 && d0 < t_out, b1 = !in1 && d1 < t_out;
-                if (__any_sync(0xffffffffu, b0 || b1)) {
-                    bool ok0 = false, ok1 = false;
-                    if (b0) {
-                        const int p = POS[2 * k];
-                        ok0 = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0) < r2;
-                    }
-                    if (b1) {
-                        const int p = POS[2 * k + 1];
-                        ok1 = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0) < r2;
-                    }
-                    cnt += __popc(__ballot_sync(0xffffffffu, ok0)) + __popc(__ballot_sync(0xffffffffu, ok1));
+                const f2u X = X2[k], Y = Y2[k], Z = (DIM == 3) ? Z2[k] : 0ull;
+                const f2u da = d2_f32x2<DIM>(X, Y, Z, ax2, ay2, az2);
+                const f2u db = d2_f32x2<DIM>(X, Y, Z, bx2, by2, bz2);
+                const float a0 = f2_lo(da), a1 = f2_hi(da), b0 = f2_lo(db), b1 = f2_hi(db);
+                if (a0 < t_in) cnt += 1;
+                if (a1 < t_in) cnt += 1;
+                if (b0 < t_in) cnt += 0x10000;
+                if (b1 < t_in) cnt += 0x10000;
+                const bool ba0 = !(a0 < t_in) && a0 < t_out, ba1 = !(a1 < t_in) && a1 < t_out;
+                const bool bb0 = !(b0 < t_in) && b0 < t_out, bb1 = !(b1 < t_in) && b1 < t_out;
+                if (ba0 || ba1 || bb0 || bb1) {
+                    if (ba0 && exact(2 * k, ax, ay, az)) cnt += 1;
+                    if (ba1 && exact(2 * k + 1, ax, ay, az)) cnt += 1;
+                    if (bb0 && exact(2 * k, bx, by, bz)) cnt += 0x10000;
+                    if (bb1 && exact(2 * k + 1, bx, by, bz)) cnt += 0x10000;
                 }
             }
-            if (lane == 0) counts[P.id[q]] = cnt;
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            if (lane == 0) {
+                counts[P.id[q]] = cnt & 0xffff;
+                if (hasb) counts[P.id[qb]] = cnt >> 16;
+            }
         }
     } else {
         for (int q = q0 + warp; q < q1; q += WARPS) {
