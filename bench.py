@@ -175,36 +175,50 @@ def host_cpu():
     return f"{model} ({os.cpu_count()} logical cores on the host)"
 
 
-def oracle_sample(c, x, dc, rmin, applies, rows_per_step, steps, seed_cfg):
-    """Time the oracle (as it stands, single thread) on a bounded sample of the workload:
-    the cell list over all N points (setup, charged pro rata), then for `rows_per_step`
-    seeded rows: the row build (count + fill) and `applies` sensitivity + density applies.
-    Returns (GB/s of the sample's algorithmic bytes, per-step seconds list, description)."""
+def oracle_sample(c, x, dc, rmin, applies, rows_per_step, steps, seed_cfg, threads=1):
+    """Time the oracle (as it stands) on a bounded sample of the workload: the cell list over
+    all N points (setup, charged pro rata), then for `rows_per_step` seeded rows: the row build
+    (count + fill) and `applies` sensitivity + density applies. threads > 1 runs the same
+    oracle calls on contiguous row chunks in host threads (ctypes releases the GIL; the oracle's
+    row functions only read the cell list): SURVEY 8(d)'s multicore CPU baseline, no oracle
+    change. Returns (GB/s of the sample's algorithmic bytes, per-step seconds list, description)."""
     import oracle
+    from concurrent.futures import ThreadPoolExecutor
     n, dim = c.shape
     t0 = time.perf_counter()
     cl = oracle.CellList(c, rmin)
     t_setup = time.perf_counter() - t0
     all_rows = synth.sample_rows(seed_cfg, n, rows_per_step * steps)
-    vals, times = [], []
-    for s in range(steps):
-        rows = np.sort(all_rows[s * rows_per_step:(s + 1) * rows_per_step])
-        t0 = time.perf_counter()
+
+    def work(rows):
         H = cl.rows(rows)
         for _ in range(applies):
             oracle.apply_sensitivity(H, x, dc)
             oracle.apply_density(H, x)
-        dt = time.perf_counter() - t0 + t_setup * len(rows) / n
-        m = len(rows)
-        nnz = H.nnz
-        b = (8 * dim * m + 12 * nnz + 8 * m + 8 * m) + applies * (
-            (12 * nnz + 8 * m + 32 * m) + (12 * nnz + 8 * m + 24 * m))
-        vals.append(b / dt / 1e9)
-        times.append(dt)
+        return H.nnz
+
+    vals, times = [], []
+    with ThreadPoolExecutor(threads) as ex:
+        # one untimed pass first (first-touch page faults of a fresh cell list / buffers)
+        warm = np.sort(all_rows[:max(1, min(len(all_rows), rows_per_step // 4))])
+        list(ex.map(work, [ch for ch in np.array_split(warm, threads) if ch.size]))
+        for s in range(steps):
+            rows = np.sort(all_rows[s * rows_per_step:(s + 1) * rows_per_step])
+            chunks = [ch for ch in np.array_split(rows, threads) if ch.size]
+            t0 = time.perf_counter()
+            nnz = sum(ex.map(work, chunks))
+            dt = time.perf_counter() - t0 + t_setup * len(rows) / n
+            m = len(rows)
+            b = (8 * dim * m + 12 * nnz + 8 * m + 8 * m) + applies * (
+                (12 * nnz + 8 * m + 32 * m) + (12 * nnz + 8 * m + 24 * m))
+            vals.append(b / dt / 1e9)
+            times.append(dt)
     cl.close()
+    how = "single-threaded" if threads == 1 else f"{threads} host threads over row chunks"
     desc = (f"{rows_per_step} seeded rows per step (stream S(c,5,0)) of the same workload: row build "
             f"+ {applies}x(sensitivity+density) on those rows; cell-list setup over all {n} points "
-            f"({t_setup:.2f} s) charged pro rata; single-threaded C oracle (-O2 -ffp-contract=off) "
+            f"({t_setup:.2f} s, single thread) charged pro rata; one untimed warm-up pass; C oracle "
+            f"(-O2 -ffp-contract=off), {how}, "
             f"on {host_cpu()}")
     return statistics.median(vals), times, desc
 
@@ -304,6 +318,11 @@ def run_ours(args):
         v, times, desc = oracle_sample(c, x, dc, rmin, applies, args.cpu_rows, 1, args.config)
         cpu = {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc,
                "seconds": times}
+        th = max(1, min(os.cpu_count() or 1, 64))
+        if th > 1:  # the same oracle loops over row chunks on all host cores
+            vp, tp, dp = oracle_sample(c, x, dc, rmin, applies, args.cpu_rows, 1, args.config, th)
+            cpu["parallel"] = {"value": vp, "unit": "GB/s", "cores": th, "kind": "oracle, row chunks in host threads",
+                               "sample": dp, "seconds": tp}
 
     if rank == 0:
         line = {
@@ -406,7 +425,7 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-rows", type=int, default=20000)
+    ap.add_argument("--cpu-rows", type=int, default=200000)
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: timing rules need --warmup >= 3", file=sys.stderr)
