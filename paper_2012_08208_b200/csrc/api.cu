@@ -108,7 +108,11 @@ static void destroy(tf_filter_s *h) {
     if (h->hdc) cudaFreeAsync(h->hdc, 0);
     if (h->hout) cudaFreeAsync(h->hout, 0);
     if (h->hout2) cudaFreeAsync(h->hout2, 0);
+    if (h->ht) cudaFreeAsync(h->ht, 0);
     if (h->side) cudaStreamDestroy(h->side);
+    if (h->side2) cudaStreamDestroy(h->side2);
+    for (cudaEvent_t e : h->evc)
+        if (e) cudaEventDestroy(e);
     if (h->ev) cudaEventDestroy(h->ev);
     if (h->ev2) cudaEventDestroy(h->ev2);
     delete h;
@@ -326,6 +330,7 @@ static tf_status ensure_host_scratch(tf_filter h, cudaStream_t s, bool second_ou
         TF_TRY(dev_alloc((void **)&h->hout, bytes, s, "host-path staging out"));
     }
     if (second_out && !h->hout2) TF_TRY(dev_alloc((void **)&h->hout2, bytes, s, "host-path staging out2"));
+    if (second_out && !h->ht) TF_TRY(dev_alloc((void **)&h->ht, bytes, s, "host-path t = x*dc"));
     return TF_OK;
 }
 
@@ -355,23 +360,52 @@ tf_status tf_filter_iteration_host(tf_filter h, const double *x_host, const doub
     cudaStream_t s = (cudaStream_t)stream;
     TF_TRY(ensure_host_scratch(h, s, true));
     if (!h->side) TF_CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    if (!h->side2) TF_CUDA_TRY(cudaStreamCreateWithFlags(&h->side2, cudaStreamNonBlocking));
     if (!h->ev) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev, cudaEventDisableTiming));
     if (!h->ev2) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev2, cudaEventDisableTiming));
     const size_t bytes = (size_t)h->n * sizeof(double);
-    // x goes up once for both filters; the density filter (needs only x) runs while dc uploads
-    // on the side stream; the density result drains while the sensitivity filter runs
+    const int K = (h->stencil.K > 0) ? 0 : h->plan.nchunks;
+    // x goes up once for both filters; dc uploads (side stream) while the density filter runs
     TF_CUDA_TRY(cudaMemcpyAsync(h->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
-    TF_CUDA_TRY(cudaEventRecord(h->ev, s));  // (orders the side stream after earlier work on s)
+    TF_CUDA_TRY(cudaEventRecord(h->ev, s));  // also orders the side streams after earlier work on s
     TF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev, 0));
+    TF_CUDA_TRY(cudaStreamWaitEvent(h->side2, h->ev, 0));
     TF_CUDA_TRY(cudaMemcpyAsync(h->hdc, dc_host, bytes, cudaMemcpyHostToDevice, h->side));
     TF_CUDA_TRY(cudaEventRecord(h->ev2, h->side));  // dc is on the device
-    TF_TRY(launch_density(h, h->hx, h->hout2, s));
-    TF_CUDA_TRY(cudaEventRecord(h->ev, s));  // (a wait binds the record made before it)
-    TF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev, 0));
-    TF_CUDA_TRY(cudaMemcpyAsync(dens_host, h->hout2, bytes, cudaMemcpyDeviceToHost, h->side));
-    TF_CUDA_TRY(cudaStreamWaitEvent(s, h->ev2, 0));
-    TF_TRY(launch_sensitivity(h, h->hx, h->hdc, h->hout, s));
-    TF_CUDA_TRY(cudaMemcpyAsync(sens_host, h->hout, bytes, cudaMemcpyDeviceToHost, s));
+    if (K < 2) {
+        // stencil handles / tiny plans: whole-array launches; the density result drains (side2)
+        // while the sensitivity filter runs
+        TF_TRY(launch_density(h, h->hx, h->hout2, s));
+        TF_CUDA_TRY(cudaEventRecord(h->ev, s));  // (a wait binds the record made before it)
+        TF_CUDA_TRY(cudaStreamWaitEvent(h->side2, h->ev, 0));
+        TF_CUDA_TRY(cudaMemcpyAsync(dens_host, h->hout2, bytes, cudaMemcpyDeviceToHost, h->side2));
+        TF_CUDA_TRY(cudaStreamWaitEvent(s, h->ev2, 0));
+        TF_TRY(launch_sensitivity(h, h->hx, h->hdc, h->hout, s));
+        TF_CUDA_TRY(cudaMemcpyAsync(sens_host, h->hout, bytes, cudaMemcpyDeviceToHost, s));
+    } else {
+        // row-range chunks: every chunk's result starts its download (side2, while the next
+        // chunk computes), so both downloads overlap compute and the dc upload (PCIe is duplex)
+        for (int i = 0; i < 2 * K; ++i)
+            if (!h->evc[i]) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->evc[i], cudaEventDisableTiming));
+        auto drain = [&](double *dst_host, const double *src, int i, cudaEvent_t e) -> tf_status {
+            TF_CUDA_TRY(cudaEventRecord(e, s));
+            TF_CUDA_TRY(cudaStreamWaitEvent(h->side2, e, 0));
+            const int64_t r0 = h->plan.chunk_r[i], r1 = h->plan.chunk_r[i + 1];
+            TF_CUDA_TRY(cudaMemcpyAsync(dst_host + r0, src + r0, (size_t)(r1 - r0) * sizeof(double),
+                                        cudaMemcpyDeviceToHost, h->side2));
+            return TF_OK;
+        };
+        for (int i = 0; i < K; ++i) {
+            TF_TRY(launch_density_range(h, h->hx, h->hout2, i, s));
+            TF_TRY(drain(dens_host, h->hout2, i, h->evc[i]));
+        }
+        TF_CUDA_TRY(cudaStreamWaitEvent(s, h->ev2, 0));
+        for (int i = 0; i < K; ++i) {
+            TF_TRY(launch_sensitivity_range(h, h->hx, h->hdc, h->hout, h->ht, i, s));
+            TF_TRY(drain(sens_host, h->hout, i, h->evc[K + i]));
+        }
+    }
+    TF_CUDA_TRY(cudaStreamSynchronize(h->side2));
     TF_CUDA_TRY(cudaStreamSynchronize(h->side));
     TF_CUDA_TRY(cudaStreamSynchronize(s));
     return TF_OK;

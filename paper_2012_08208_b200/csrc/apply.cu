@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                                                                       const int32_t *__restrict__ rb,
                                                                       const int64_t *__restrict__ wlo,
                                                                       int64_t nwin, double *tbuf, int64_t n,
-                                                                      double penal, int energy) {
+                                                                      double penal, int energy, int64_t wbeg,
+                                                                      int64_t wend, int tpass) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *svals = reinterpret_cast<double *>(smem_raw);                           // [kStages][kStage]
     int64_t *srow = reinterpret_cast<int64_t *>(svals + kStages * kStage);          // [kStages][kRowCap]
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
         uint64_t pol = 0;
         if (lane == 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         int it = 0;
-        int64_t w = blockIdx.x;
+        int64_t w = wbeg + blockIdx.x;
         auto issue = [&](int st) {
             const int64_t a = wlo[w], n4 = wlo[w + 1 + nwin] - a;  // wlo[nwin+1+w] = aligned end
             next_row[st] = 0;  // published to the consumers by the full-barrier completion
@@ -184,13 +185,13 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
         };
         // prologue: the first kStages windows need no empty-wait (overlaps the t pass)
         if (lane == 0)
-            for (; w < nwin && it < kStages; w += gridDim.x, ++it) issue(it);
-        if (SENS) {
+            for (; w < wend && it < kStages; w += gridDim.x, ++it) issue(it);
+        if (SENS && tpass) {
             __syncwarp();
             cooperative_groups::this_grid().sync();
         }
         if (lane == 0)
-            for (; w < nwin; w += gridDim.x, ++it) {
+            for (; w < wend; w += gridDim.x, ++it) {
                 const int st = it % kStages;
                 mbar_wait_sleep(&empty[st], ((it / kStages) - 1) & 1);
                 issue(st);
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
     }
 
     // ---------------- consumers
-    if (SENS) {
+    if (SENS && tpass) {
         // fused Hadamard pass t = x o dc (PAPER.md:447 np.multiply(density, sensitivity)),
         // then a grid-wide barrier: the SpMV gathers one array instead of two
         // NEXT-2 (energy != 0): dc is evaluated here from the element energies U passed in `dc`,
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
     constexpr int RPW = 32 / G;  // rows per warp claim
     const int sub = lane & (G - 1);
     int it = 0;
-    for (int64_t w = blockIdx.x; w < nwin; w += gridDim.x, ++it) {
+    for (int64_t w = wbeg + blockIdx.x; w < wend; w += gridDim.x, ++it) {
         const int st = it % kStages;
         const int r0 = rb[w], R = rb[w + 1] - r0;
         const int64_t a = wlo[w], n4 = wlo[w + 1 + nwin] - a;
@@ -290,9 +291,12 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
     }
 }
 
+// Windows [wbeg, wend) of the plan. SENS: tbuf == nullptr -> per-call scratch, t pass and a
+// cooperative launch (the normal API); tbuf given -> tpass selects whether this launch computes
+// t (cooperative) or reuses it (ordinary launch; the row-range chunks of the host pipeline).
 template <bool SENS, int G, int U>
 tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s,
-                         double penal, int energy) {
+                         double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf_ext, int tpass) {
     const size_t smem = (size_t)kStages * (kStage * (sizeof(double) + sizeof(int32_t)) + kRowCap * sizeof(int64_t));
     auto kern = k_spmv<SENS, G, U>;
     // per-instantiation attribute (dynamic shared memory above 48 KB needs the opt-in)
@@ -305,52 +309,59 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
             return TF_ERR_CUDA;
         }
     }
+    if (wend <= wbeg) return TF_OK;
     const unsigned grid = (unsigned)std::min<int64_t>(
-        std::min<int64_t>(h->plan.nblocks, (int64_t)h->plan.grid), (int64_t)occ * (h->plan.grid / kBlocksPerSM));
+        std::min<int64_t>(wend - wbeg, (int64_t)h->plan.grid), (int64_t)occ * (h->plan.grid / kBlocksPerSM));
     const int64_t *rowptr = h->rowptr;
     const int32_t *cols = h->cols;
     const double *vals = h->vals, *hs = h->hs;
     const int32_t *rb = h->plan.rb;
     const int64_t *wlo = h->plan.wlo;
     int64_t nwin = h->plan.nblocks, n = h->n;
-    double *tbuf = nullptr;
-    if (SENS) {
-        // per-call scratch (stream-ordered): concurrent applies on different streams stay safe
-        TF_TRY(dalloc(&tbuf, (size_t)n, s, "sensitivity scratch t = x*dc"));
-        void *args[] = {(void *)&rowptr, (void *)&cols, (void *)&vals, (void *)&hs,   (void *)&x,
-                        (void *)&dc,     (void *)&out,  (void *)&rb,   (void *)&wlo,  (void *)&nwin,
-                        (void *)&tbuf,   (void *)&n,    (void *)&penal, (void *)&energy};
+    double *tbuf = tbuf_ext;
+    if (SENS && (tbuf_ext == nullptr || tpass)) {
+        // per-call scratch (stream-ordered) unless the caller owns it: concurrent applies on
+        // different streams stay safe
+        if (!tbuf_ext) TF_TRY(dalloc(&tbuf, (size_t)n, s, "sensitivity scratch t = x*dc"));
+        tpass = 1;
+        void *args[] = {(void *)&rowptr, (void *)&cols, (void *)&vals,  (void *)&hs,     (void *)&x,
+                        (void *)&dc,     (void *)&out,  (void *)&rb,    (void *)&wlo,    (void *)&nwin,
+                        (void *)&tbuf,   (void *)&n,    (void *)&penal, (void *)&energy, (void *)&wbeg,
+                        (void *)&wend,   (void *)&tpass};
         cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads + 32), args, smem, s);
         count_launch();
-        dev_free(tbuf, s);
+        if (!tbuf_ext) dev_free(tbuf, s);
         if (e != cudaSuccess) {
             set_error("cooperative launch failed: %s", cudaGetErrorString(e));
             return TF_ERR_CUDA;
         }
         return TF_OK;
     }
-    kern<<<grid, kThreads + 32, smem, s>>>(rowptr, cols, vals, hs, x, dc, out, rb, wlo, nwin, tbuf, n, penal, energy);
+    kern<<<grid, kThreads + 32, smem, s>>>(rowptr, cols, vals, hs, x, dc, out, rb, wlo, nwin, tbuf, n, penal, energy,
+                                           wbeg, wend, 0);
     TF_LAUNCH_CHECK();
     return TF_OK;
 }
 
 template <bool SENS, int G>
 tf_status launch_spmv_g(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s,
-                        double penal, int energy) {
-    if (h->plan.unroll >= 8) return launch_spmv_gu<SENS, G, 8>(h, x, dc, out, s, penal, energy);
-    return launch_spmv_gu<SENS, G, 4>(h, x, dc, out, s, penal, energy);
+                        double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf, int tpass) {
+    if (h->plan.unroll >= 8) return launch_spmv_gu<SENS, G, 8>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
+    return launch_spmv_gu<SENS, G, 4>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
 }
 
 template <bool SENS>
 tf_status launch_spmv(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s,
-                      double penal = 0.0, int energy = 0) {
+                      double penal = 0.0, int energy = 0, int64_t wbeg = 0, int64_t wend = -1,
+                      double *tbuf = nullptr, int tpass = 1) {
+    if (wend < 0) wend = h->plan.nblocks;
     switch (h->plan.group) {
-        case 1: return launch_spmv_g<SENS, 1>(h, x, dc, out, s, penal, energy);
-        case 2: return launch_spmv_g<SENS, 2>(h, x, dc, out, s, penal, energy);
-        case 4: return launch_spmv_g<SENS, 4>(h, x, dc, out, s, penal, energy);
-        case 8: return launch_spmv_g<SENS, 8>(h, x, dc, out, s, penal, energy);
-        case 16: return launch_spmv_g<SENS, 16>(h, x, dc, out, s, penal, energy);
-        default: return launch_spmv_g<SENS, 32>(h, x, dc, out, s, penal, energy);
+        case 1: return launch_spmv_g<SENS, 1>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
+        case 2: return launch_spmv_g<SENS, 2>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
+        case 4: return launch_spmv_g<SENS, 4>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
+        case 8: return launch_spmv_g<SENS, 8>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
+        case 16: return launch_spmv_g<SENS, 16>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
+        default: return launch_spmv_g<SENS, 32>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
     }
 }
 
@@ -400,7 +411,27 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
     TF_LAUNCH_CHECK();
     k_plan_windows<<<grid, 256, 0, s>>>(h->rowptr, h->plan.rb, nblocks, h->plan.wlo);
     TF_LAUNCH_CHECK();
+    // row-range chunks for the host pipeline (tf_filter_iteration_host): window and first-row
+    // boundaries, read back once here
+    const int K = (int)std::min<int64_t>(kMaxChunks, nblocks);
+    h->plan.nchunks = K;
+    for (int i = 0; i <= K; ++i) {
+        h->plan.chunk_w[i] = nblocks * i / K;
+        TF_CUDA_TRY(cudaMemcpyAsync(&h->plan.chunk_r[i], h->plan.rb + h->plan.chunk_w[i], sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, s));
+    }
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
     return TF_OK;
+}
+
+tf_status launch_density_range(const tf_filter_s *h, const double *x, double *out, int chunk, cudaStream_t s) {
+    return launch_spmv<false>(h, x, nullptr, out, s, 0.0, 0, h->plan.chunk_w[chunk], h->plan.chunk_w[chunk + 1]);
+}
+
+tf_status launch_sensitivity_range(const tf_filter_s *h, const double *x, const double *dc, double *out, double *tbuf,
+                                   int chunk, cudaStream_t s) {
+    return launch_spmv<true>(h, x, dc, out, s, 0.0, 0, h->plan.chunk_w[chunk], h->plan.chunk_w[chunk + 1], tbuf,
+                             chunk == 0 ? 1 : 0);
 }
 
 tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double *dc, double *out,

@@ -145,7 +145,13 @@ struct ApplyPlan {
     int64_t *wlo = nullptr;   // [2*nblocks+1] aligned staging window start / end per row block
     int grid = 0;             // persistent grid size
     int unroll = 4;           // loads in flight per lane in the row loop (4 or 8)
+    // row-range chunks of the host pipeline: windows [chunk_w[i], chunk_w[i+1]) cover rows
+    // [chunk_r[i], chunk_r[i+1])
+    int nchunks = 0;
+    int64_t chunk_w[9] = {};
+    int32_t chunk_r[9] = {};
 };
+constexpr int kMaxChunks = 8;
 
 // ------------------------------------------------------------------ matrix-free stencil (a10)
 struct StencilGeom {
@@ -172,9 +178,10 @@ struct tf_filter_s {
     tf::ApplyPlan plan;
     tf_build_info info{};
     // host-API scratch (lazily allocated, owned) + a side stream / event for copy overlap
-    double *hx = nullptr, *hdc = nullptr, *hout = nullptr, *hout2 = nullptr;
-    cudaStream_t side = nullptr;
+    double *hx = nullptr, *hdc = nullptr, *hout = nullptr, *hout2 = nullptr, *ht = nullptr;
+    cudaStream_t side = nullptr, side2 = nullptr;  // upload / download streams of the host pipeline
     cudaEvent_t ev = nullptr, ev2 = nullptr;
+    cudaEvent_t evc[2 * tf::kMaxChunks] = {};  // per-chunk completion of the host pipeline
     // matrix-free stencil handles (tf_build_stencil): no CSR; offset table on the device
     tf::StencilGeom stencil;
     int4 *stencil_off = nullptr;
@@ -212,6 +219,11 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s);
 tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double *dc, double *out,
                              cudaStream_t s);
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s);
+// row-range chunk i of the plan (host pipeline); the sensitivity chunk 0 computes t = x*dc into
+// tbuf (cooperative), later chunks reuse it
+tf_status launch_density_range(const tf_filter_s *h, const double *x, double *out, int chunk, cudaStream_t s);
+tf_status launch_sensitivity_range(const tf_filter_s *h, const double *x, const double *dc, double *out, double *tbuf,
+                                   int chunk, cudaStream_t s);
 tf_status launch_sensitivity_energy(const tf_filter_s *h, const double *x, const double *U, double penal,
                                     double *out, cudaStream_t s);
 

@@ -285,6 +285,30 @@ def test_host_variants_match_device(tf):
     np.testing.assert_array_equal(d2, fd.density(dev(x)).cpu().numpy())
 
 
+@pytest.mark.parametrize("case", ["one_window", "c1", "c3", "stencil_c3"])
+def test_iteration_host_pipeline(tf, case):
+    """tf_filter_iteration_host: the row-range chunk pipeline (plans with >= 2 windows: up to 8
+    chunks, each downloaded while the next computes) and the whole-array path (one window,
+    stencil handles) give the device calls' results bitwise; repeated calls stay correct."""
+    if case == "one_window":
+        c, rmin = synth.random_points(611, 40, 2, 0.0, 3.0), 1.0
+        n = c.shape[0]
+        x, dc = inputs_for(n, 612)
+        f = tf.tf_build_filter(dev(c), rmin)
+    elif case == "stencil_c3":
+        c, x, dc, rmin = synth.workload(3)
+        f = tf.tf_build_stencil(3, 160, 80, 80, 1.0, rmin)
+    else:
+        c, x, dc, rmin = synth.workload(int(case[1]))
+        f = tf.tf_build_filter(dev(c), rmin)
+    want_s = f.sensitivity(dev(x), dev(dc)).cpu().numpy()
+    want_d = f.density(dev(x)).cpu().numpy()
+    for _ in range(2):
+        s2, d2 = tf.tf_filter_iteration_host(f, x, dc)
+        np.testing.assert_array_equal(s2, want_s)
+        np.testing.assert_array_equal(d2, want_d)
+
+
 def test_streams_concurrent_applies(tf):
     c, x, dc, rmin = synth.workload(3)
     f = tf.tf_build_filter(dev(c), rmin)
