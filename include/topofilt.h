@@ -175,12 +175,13 @@ TF_API tf_status tf_sensitivity_filter_host(tf_filter h, const double *x_host, c
                                      double *out_host, void *stream);
 TF_API tf_status tf_density_filter_host(tf_filter h, const double *x_host, double *out_host,
                                         void *stream);
-/* One optimisation iteration's filtering on host buffers: uploads x once for both filters and dc
- * on a handle-owned upload stream while the density filter runs; both filters run as up to 8
- * row-range launches, and each range's result downloads on a handle-owned download stream while
- * the next range computes (PCIe is duplex: uploads and downloads overlap). Stencil handles and
- * one-window plans use whole-array launches. Results are bitwise those of the device calls.
- * Synchronises before returning. Not safe to call concurrently on the same handle. */
+/* One optimisation iteration's filtering on host buffers. Pipelined over the apply plan's (up to
+ * 8) row-range chunks: x then dc upload in row pieces on a handle-owned upload stream; a chunk of
+ * either filter starts once the pieces up to the one holding its largest column have landed;
+ * each chunk's result downloads on a handle-owned download stream while the next chunk computes.
+ * Stencil handles and one-window plans use whole-array launches. Results are bitwise those of
+ * the device calls. Synchronises before returning. Not safe to call concurrently on the same
+ * handle. */
 TF_API tf_status tf_filter_iteration_host(tf_filter h, const double *x_host, const double *dc_host,
                                           double *sens_host, double *dens_host, void *stream);
 

@@ -113,6 +113,10 @@ static void destroy(tf_filter_s *h) {
     if (h->side2) cudaStreamDestroy(h->side2);
     for (cudaEvent_t e : h->evc)
         if (e) cudaEventDestroy(e);
+    for (int i = 0; i < tf::kMaxChunks; ++i) {
+        if (h->evx[i]) cudaEventDestroy(h->evx[i]);
+        if (h->evd[i]) cudaEventDestroy(h->evd[i]);
+    }
     if (h->ev) cudaEventDestroy(h->ev);
     if (h->ev2) cudaEventDestroy(h->ev2);
     delete h;
@@ -150,6 +154,7 @@ static tf_status build_common(const double *c, int64_t n, int dim, double rmin, 
     h->dim = dim;
     h->rmin = rmin;
     tf_status st = build_filter_device(c, n, dim, rmin, s, h);
+    h->cols_ascending = true;  // the fill writes every row's columns ascending
     if (st == TF_OK) st = make_apply_plan(h, s);
     if (st == TF_OK) {
         cudaError_t e = cudaStreamSynchronize(s);
@@ -365,14 +370,16 @@ tf_status tf_filter_iteration_host(tf_filter h, const double *x_host, const doub
     if (!h->ev2) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev2, cudaEventDisableTiming));
     const size_t bytes = (size_t)h->n * sizeof(double);
     const int K = (h->stencil.K > 0) ? 0 : h->plan.nchunks;
-    // x goes up once for both filters; dc uploads (side stream) while the density filter runs
-    TF_CUDA_TRY(cudaMemcpyAsync(h->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
-    TF_CUDA_TRY(cudaEventRecord(h->ev, s));  // also orders the side streams after earlier work on s
+    TF_CUDA_TRY(cudaEventRecord(h->ev, s));  // orders the side streams after earlier work on s
     TF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev, 0));
     TF_CUDA_TRY(cudaStreamWaitEvent(h->side2, h->ev, 0));
-    TF_CUDA_TRY(cudaMemcpyAsync(h->hdc, dc_host, bytes, cudaMemcpyHostToDevice, h->side));
-    TF_CUDA_TRY(cudaEventRecord(h->ev2, h->side));  // dc is on the device
     if (K < 2) {
+        // x goes up once for both filters; dc uploads (side stream) while the density filter runs
+        TF_CUDA_TRY(cudaMemcpyAsync(h->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
+        TF_CUDA_TRY(cudaEventRecord(h->ev2, s));  // x first at full PCIe bandwidth, then dc
+        TF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev2, 0));
+        TF_CUDA_TRY(cudaMemcpyAsync(h->hdc, dc_host, bytes, cudaMemcpyHostToDevice, h->side));
+        TF_CUDA_TRY(cudaEventRecord(h->ev2, h->side));  // dc is on the device
         // stencil handles / tiny plans: whole-array launches; the density result drains (side2)
         // while the sensitivity filter runs
         TF_TRY(launch_density(h, h->hx, h->hout2, s));
@@ -383,25 +390,58 @@ tf_status tf_filter_iteration_host(tf_filter h, const double *x_host, const doub
         TF_TRY(launch_sensitivity(h, h->hx, h->hdc, h->hout, s));
         TF_CUDA_TRY(cudaMemcpyAsync(sens_host, h->hout, bytes, cudaMemcpyDeviceToHost, s));
     } else {
-        // row-range chunks: every chunk's result starts its download (side2, while the next
-        // chunk computes), so both downloads overlap compute and the dc upload (PCIe is duplex)
+        // Row-range pipeline. Uploads (side stream) in K pieces = the chunks' row ranges, x first
+        // then dc; chunk i of a filter starts once the pieces up to the one holding its largest
+        // column (and its own rows) have landed; t = x o dc is formed piece by piece as dc
+        // arrives; every chunk's result downloads on side2 while the next chunk computes
+        // (PCIe is duplex). Pieces land in order on one stream, so waiting for piece P covers
+        // pieces 0..P.
         for (int i = 0; i < 2 * K; ++i)
             if (!h->evc[i]) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->evc[i], cudaEventDisableTiming));
+        for (int i = 0; i < K; ++i) {
+            if (!h->evx[i]) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->evx[i], cudaEventDisableTiming));
+            if (!h->evd[i]) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->evd[i], cudaEventDisableTiming));
+        }
+        const int32_t *cr = h->plan.chunk_r;
+        auto piece_bytes = [&](int p) { return (size_t)(cr[p + 1] - cr[p]) * sizeof(double); };
+        auto gate = [&](int i) {  // last piece chunk i reads
+            int g = i;
+            const int32_t mc = h->plan.chunk_maxcol[i];
+            for (int p = 0; p < K; ++p)
+                if (mc >= cr[p] && mc < cr[p + 1]) g = std::max(g, p);
+            return g;
+        };
+        // the x upload issued on s above is replaced by pieces on the side stream
+        for (int p = 0; p < K; ++p) {
+            TF_CUDA_TRY(cudaMemcpyAsync(h->hx + cr[p], x_host + cr[p], piece_bytes(p), cudaMemcpyHostToDevice, h->side));
+            TF_CUDA_TRY(cudaEventRecord(h->evx[p], h->side));
+        }
+        for (int p = 0; p < K; ++p) {
+            TF_CUDA_TRY(cudaMemcpyAsync(h->hdc + cr[p], dc_host + cr[p], piece_bytes(p), cudaMemcpyHostToDevice,
+                                        h->side));
+            TF_CUDA_TRY(cudaEventRecord(h->evd[p], h->side));
+        }
         auto drain = [&](double *dst_host, const double *src, int i, cudaEvent_t e) -> tf_status {
             TF_CUDA_TRY(cudaEventRecord(e, s));
             TF_CUDA_TRY(cudaStreamWaitEvent(h->side2, e, 0));
-            const int64_t r0 = h->plan.chunk_r[i], r1 = h->plan.chunk_r[i + 1];
-            TF_CUDA_TRY(cudaMemcpyAsync(dst_host + r0, src + r0, (size_t)(r1 - r0) * sizeof(double),
-                                        cudaMemcpyDeviceToHost, h->side2));
+            TF_CUDA_TRY(cudaMemcpyAsync(dst_host + cr[i], src + cr[i], piece_bytes(i), cudaMemcpyDeviceToHost,
+                                        h->side2));
             return TF_OK;
         };
         for (int i = 0; i < K; ++i) {
+            TF_CUDA_TRY(cudaStreamWaitEvent(s, h->evx[gate(i)], 0));
             TF_TRY(launch_density_range(h, h->hx, h->hout2, i, s));
             TF_TRY(drain(dens_host, h->hout2, i, h->evc[i]));
         }
-        TF_CUDA_TRY(cudaStreamWaitEvent(s, h->ev2, 0));
+        int tdone = -1;  // pieces of t formed so far
         for (int i = 0; i < K; ++i) {
-            TF_TRY(launch_sensitivity_range(h, h->hx, h->hdc, h->hout, h->ht, i, s));
+            const int gi = gate(i);
+            for (; tdone < gi; ) {
+                ++tdone;
+                TF_CUDA_TRY(cudaStreamWaitEvent(s, h->evd[tdone], 0));
+                TF_TRY(launch_hadamard_piece(h, h->hx, h->hdc, h->ht, tdone, s));
+            }
+            TF_TRY(launch_sensitivity_range(h, h->hx, h->hdc, h->hout, h->ht, i, 0, s));
             TF_TRY(drain(sens_host, h->hout, i, h->evc[K + i]));
         }
     }

@@ -365,6 +365,23 @@ tf_status launch_spmv(const tf_filter_s *h, const double *x, const double *dc, d
     }
 }
 
+// max over rows r in [r0, r1) of the row's largest column (rows are ascending: the last entry;
+// an empty row contributes nothing)
+__global__ void k_chunk_maxcol(const int64_t *__restrict__ rowptr, const int32_t *__restrict__ cols, int64_t r0,
+                               int64_t r1, int ascending, int32_t *__restrict__ out) {
+    int m = -1;
+    for (int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = rowptr[r], e = rowptr[r + 1];
+        if (ascending) {
+            if (e > s) m = max(m, cols[e - 1]);
+        } else {
+            for (int64_t k = s; k < e; ++k) m = max(m, cols[k]);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m >= 0) atomicMax(out, m);
+}
+
 // Aligned staging window of each row block: wlo[w] = rowptr[rb[w]] & ~3 and
 // wlo[nwin + 1 + w] = (rowptr[rb[w+1]] + 3) & ~3 (16-byte aligned bulk copies).
 __global__ void k_plan_windows(const int64_t *__restrict__ rowptr, const int32_t *__restrict__ rb, int64_t nwin,
@@ -421,6 +438,40 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
                                     cudaMemcpyDeviceToHost, s));
     }
     TF_CUDA_TRY(cudaStreamSynchronize(s));
+    // largest column each chunk reads (exact, from the stored columns): the host pipeline starts
+    // chunk i once the input pieces up to the one holding that column have landed
+    DevBuf<int32_t> mx;
+    TF_TRY(mx.alloc(kMaxChunks, s, "chunk max columns"));
+    TF_CUDA_TRY(cudaMemsetAsync(mx.p, 0xff, kMaxChunks * sizeof(int32_t), s));  // -1
+    for (int i = 0; i < K; ++i) {
+        const int64_t r0 = h->plan.chunk_r[i], r1 = h->plan.chunk_r[i + 1];
+        if (r1 > r0) {
+            k_chunk_maxcol<<<(unsigned)std::min<int64_t>((r1 - r0 + 255) / 256, 1184), 256, 0, s>>>(h->rowptr, h->cols,
+                                                                                                 r0, r1, h->cols_ascending ? 1 : 0,
+                                                                                                 mx.p + i);
+            TF_LAUNCH_CHECK();
+        }
+    }
+    TF_CUDA_TRY(cudaMemcpyAsync(h->plan.chunk_maxcol, mx.p, kMaxChunks * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    return TF_OK;
+}
+
+__global__ void k_hadamard(const double *__restrict__ x, const double *__restrict__ dc, double *__restrict__ t,
+                           int64_t r0, int64_t r1) {
+    for (int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x)
+        t[i] = x[i] * dc[i];
+}
+
+// t = x o dc on rows [chunk_r[piece], chunk_r[piece+1]) (the host pipeline's per-piece pass;
+// same product as the fused pass of k_spmv)
+tf_status launch_hadamard_piece(const tf_filter_s *h, const double *x, const double *dc, double *t, int piece,
+                                cudaStream_t s) {
+    const int64_t r0 = h->plan.chunk_r[piece], r1 = h->plan.chunk_r[piece + 1];
+    if (r1 <= r0) return TF_OK;
+    const unsigned grid = (unsigned)std::min<int64_t>((r1 - r0 + 255) / 256, 148 * 8);
+    k_hadamard<<<grid, 256, 0, s>>>(x, dc, t, r0, r1);
+    TF_LAUNCH_CHECK();
     return TF_OK;
 }
 
@@ -429,9 +480,9 @@ tf_status launch_density_range(const tf_filter_s *h, const double *x, double *ou
 }
 
 tf_status launch_sensitivity_range(const tf_filter_s *h, const double *x, const double *dc, double *out, double *tbuf,
-                                   int chunk, cudaStream_t s) {
+                                   int chunk, int tpass, cudaStream_t s) {
     return launch_spmv<true>(h, x, dc, out, s, 0.0, 0, h->plan.chunk_w[chunk], h->plan.chunk_w[chunk + 1], tbuf,
-                             chunk == 0 ? 1 : 0);
+                             tpass);
 }
 
 tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double *dc, double *out,

@@ -150,6 +150,7 @@ struct ApplyPlan {
     int nchunks = 0;
     int64_t chunk_w[9] = {};
     int32_t chunk_r[9] = {};
+    int32_t chunk_maxcol[8] = {};  // largest column read by chunk i (-1: none)
 };
 constexpr int kMaxChunks = 8;
 
@@ -176,12 +177,14 @@ struct tf_filter_s {
     double *vals = nullptr;
     double *hs = nullptr;
     tf::ApplyPlan plan;
+    bool cols_ascending = false;  // set by the library's own build (tf_filter_from_csr: unknown)
     tf_build_info info{};
     // host-API scratch (lazily allocated, owned) + a side stream / event for copy overlap
     double *hx = nullptr, *hdc = nullptr, *hout = nullptr, *hout2 = nullptr, *ht = nullptr;
     cudaStream_t side = nullptr, side2 = nullptr;  // upload / download streams of the host pipeline
     cudaEvent_t ev = nullptr, ev2 = nullptr;
     cudaEvent_t evc[2 * tf::kMaxChunks] = {};  // per-chunk completion of the host pipeline
+    cudaEvent_t evx[tf::kMaxChunks] = {}, evd[tf::kMaxChunks] = {};  // x / dc piece uploaded
     // matrix-free stencil handles (tf_build_stencil): no CSR; offset table on the device
     tf::StencilGeom stencil;
     int4 *stencil_off = nullptr;
@@ -222,8 +225,10 @@ tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cud
 // row-range chunk i of the plan (host pipeline); the sensitivity chunk 0 computes t = x*dc into
 // tbuf (cooperative), later chunks reuse it
 tf_status launch_density_range(const tf_filter_s *h, const double *x, double *out, int chunk, cudaStream_t s);
+tf_status launch_hadamard_piece(const tf_filter_s *h, const double *x, const double *dc, double *t, int piece,
+                                cudaStream_t s);
 tf_status launch_sensitivity_range(const tf_filter_s *h, const double *x, const double *dc, double *out, double *tbuf,
-                                   int chunk, cudaStream_t s);
+                                   int chunk, int tpass, cudaStream_t s);
 tf_status launch_sensitivity_energy(const tf_filter_s *h, const double *x, const double *U, double penal,
                                     double *out, cudaStream_t s);
 

@@ -285,12 +285,19 @@ def test_host_variants_match_device(tf):
     np.testing.assert_array_equal(d2, fd.density(dev(x)).cpu().numpy())
 
 
-@pytest.mark.parametrize("case", ["one_window", "c1", "c3", "stencil_c3"])
+@pytest.mark.parametrize("case", ["one_window", "c1", "c3", "stencil_c3", "random_ids"])
 def test_iteration_host_pipeline(tf, case):
     """tf_filter_iteration_host: the row-range chunk pipeline (plans with >= 2 windows: up to 8
-    chunks, each downloaded while the next computes) and the whole-array path (one window,
-    stencil handles) give the device calls' results bitwise; repeated calls stay correct."""
-    if case == "one_window":
+    chunks; chunk i starts once the input pieces up to its largest column have landed, and
+    downloads while the next computes) and the whole-array path (one window, stencil handles)
+    give the device calls' results bitwise; repeated calls stay correct. random_ids: ids carry no
+    spatial order, so every chunk reads columns up to ~N and waits for every piece."""
+    if case == "random_ids":
+        c, rmin = synth.random_points(613, 200_000, 3, 0.0, 40.0), 1.2
+        n = c.shape[0]
+        x, dc = inputs_for(n, 614)
+        f = tf.tf_build_filter(dev(c), rmin)
+    elif case == "one_window":
         c, rmin = synth.random_points(611, 40, 2, 0.0, 3.0), 1.0
         n = c.shape[0]
         x, dc = inputs_for(n, 612)
