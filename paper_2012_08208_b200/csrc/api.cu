@@ -4,6 +4,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <new>
@@ -44,6 +45,40 @@ tf_status dev_alloc(void **p, size_t bytes, cudaStream_t s, const char *what) {
 
 void dev_free(void *p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
+}
+
+bool PhaseTrace::enabled() {
+    const char *e = getenv("TOPOFILT_TRACE");
+    return e && *e && *e != '0';
+}
+void PhaseTrace::begin(cudaStream_t s) {
+    on = enabled();
+    k = 0;
+    if (on) mark("start", s);
+}
+void PhaseTrace::mark(const char *nm, cudaStream_t s) {
+    if (!on || k >= 24) return;
+    if (!ev[k]) cudaEventCreate(&ev[k]);
+    cudaEventRecord(ev[k], s);
+    name[k++] = nm;
+}
+void PhaseTrace::report(const char *what) {
+    if (!on || k < 2) return;
+    cudaEventSynchronize(ev[k - 1]);
+    float total = 0.f;
+    cudaEventElapsedTime(&total, ev[0], ev[k - 1]);
+    fprintf(stderr, "[topofilt trace] %s %.3f ms:", what, total);
+    for (int i = 1; i < k; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+        fprintf(stderr, " %s %.3f", name[i], ms);
+    }
+    fprintf(stderr, "\n");
+    on = false;
+}
+PhaseTrace &build_trace() {
+    static thread_local PhaseTrace t;
+    return t;
 }
 
 tf_status device_info(DeviceInfo *di) {
@@ -153,9 +188,11 @@ static tf_status build_common(const double *c, int64_t n, int dim, double rmin, 
     h->n = n;
     h->dim = dim;
     h->rmin = rmin;
+    build_trace().begin(s);
     tf_status st = build_filter_device(c, n, dim, rmin, s, h);
     h->cols_ascending = true;  // the fill writes every row's columns ascending
     if (st == TF_OK) st = make_apply_plan(h, s);
+    build_trace().mark("apply_plan", s);
     if (st == TF_OK) {
         cudaError_t e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) {
@@ -163,6 +200,7 @@ static tf_status build_common(const double *c, int64_t n, int dim, double rmin, 
             st = TF_ERR_CUDA;
         }
     }
+    build_trace().report(st == TF_OK ? "tf_build_filter" : "tf_build_filter (failed)");
     if (st != TF_OK) {
         destroy(h);
         return st;
@@ -369,6 +407,7 @@ tf_status tf_filter_iteration_host(tf_filter h, const double *x_host, const doub
     if (!h->ev) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev, cudaEventDisableTiming));
     if (!h->ev2) TF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev2, cudaEventDisableTiming));
     const size_t bytes = (size_t)h->n * sizeof(double);
+    if (h->stencil.K == 0) TF_TRY(ensure_chunk_plan(h, s));
     const int K = (h->stencil.K > 0) ? 0 : h->plan.nchunks;
     TF_CUDA_TRY(cudaEventRecord(h->ev, s));  // orders the side streams after earlier work on s
     TF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev, 0));

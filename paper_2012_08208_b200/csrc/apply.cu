@@ -428,10 +428,35 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
     TF_LAUNCH_CHECK();
     k_plan_windows<<<grid, 256, 0, s>>>(h->rowptr, h->plan.rb, nblocks, h->plan.wlo);
     TF_LAUNCH_CHECK();
-    // row-range chunks for the host pipeline (tf_filter_iteration_host): window and first-row
-    // boundaries, read back once here
+    h->plan.nchunks = -1;  // host-pipeline chunks: computed on first use (ensure_chunk_plan)
+    return TF_OK;
+}
+
+__global__ void k_hadamard(const double *__restrict__ x, const double *__restrict__ dc, double *__restrict__ t,
+                           int64_t r0, int64_t r1) {
+    for (int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x)
+        t[i] = x[i] * dc[i];
+}
+
+// t = x o dc on rows [chunk_r[piece], chunk_r[piece+1]) (the host pipeline's per-piece pass;
+// same product as the fused pass of k_spmv)
+tf_status launch_hadamard_piece(const tf_filter_s *h, const double *x, const double *dc, double *t, int piece,
+                                cudaStream_t s) {
+    const int64_t r0 = h->plan.chunk_r[piece], r1 = h->plan.chunk_r[piece + 1];
+    if (r1 <= r0) return TF_OK;
+    const unsigned grid = (unsigned)std::min<int64_t>((r1 - r0 + 255) / 256, 148 * 8);
+    k_hadamard<<<grid, 256, 0, s>>>(x, dc, t, r0, r1);
+    TF_LAUNCH_CHECK();
+    return TF_OK;
+}
+
+// Row-range chunks of the host pipeline (tf_filter_iteration_host), computed once on first use
+// so device-only users never pay for them: window and first-row boundaries and the largest
+// column each chunk reads (exact, from the stored columns). Synchronises `s`.
+tf_status ensure_chunk_plan(tf_filter_s *h, cudaStream_t s) {
+    if (h->plan.nchunks >= 0) return TF_OK;
+    const int64_t nblocks = h->plan.nblocks;
     const int K = (int)std::min<int64_t>(kMaxChunks, nblocks);
-    h->plan.nchunks = K;
     for (int i = 0; i <= K; ++i) {
         h->plan.chunk_w[i] = nblocks * i / K;
         TF_CUDA_TRY(cudaMemcpyAsync(&h->plan.chunk_r[i], h->plan.rb + h->plan.chunk_w[i], sizeof(int32_t),
@@ -454,24 +479,7 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
     }
     TF_CUDA_TRY(cudaMemcpyAsync(h->plan.chunk_maxcol, mx.p, kMaxChunks * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     TF_CUDA_TRY(cudaStreamSynchronize(s));
-    return TF_OK;
-}
-
-__global__ void k_hadamard(const double *__restrict__ x, const double *__restrict__ dc, double *__restrict__ t,
-                           int64_t r0, int64_t r1) {
-    for (int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x)
-        t[i] = x[i] * dc[i];
-}
-
-// t = x o dc on rows [chunk_r[piece], chunk_r[piece+1]) (the host pipeline's per-piece pass;
-// same product as the fused pass of k_spmv)
-tf_status launch_hadamard_piece(const tf_filter_s *h, const double *x, const double *dc, double *t, int piece,
-                                cudaStream_t s) {
-    const int64_t r0 = h->plan.chunk_r[piece], r1 = h->plan.chunk_r[piece + 1];
-    if (r1 <= r0) return TF_OK;
-    const unsigned grid = (unsigned)std::min<int64_t>((r1 - r0 + 255) / 256, 148 * 8);
-    k_hadamard<<<grid, 256, 0, s>>>(x, dc, t, r0, r1);
-    TF_LAUNCH_CHECK();
+    h->plan.nchunks = K;  // published only once complete
     return TF_OK;
 }
 

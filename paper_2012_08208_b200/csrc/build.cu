@@ -874,6 +874,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     double bb[7];
     TF_CUDA_TRY(cudaMemcpyAsync(bb, bbd.p, 7 * sizeof(double), cudaMemcpyDeviceToHost, s));
     TF_CUDA_TRY(cudaStreamSynchronize(s));
+    build_trace().mark("bbox+sync", s);
     if (bb[6] != 0.0) {
         set_error("tf_build_filter: non-finite centroid coordinate (NaN or Inf)");
         return TF_ERR_INVALID;
@@ -897,7 +898,9 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     // a4 radix sort + cell start + sorted SoA
     uint32_t *ks = nullptr, *vs = nullptr;
     int passes = 0;
+    build_trace().mark("keys", s);
     TF_TRY(radix_sort_pairs(k0.p, v0.p, k1.p, v1.p, n, ceil_log2(g.nbins), s, &ks, &vs, &passes));
+    build_trace().mark("radix", s);
     h->info.radix_passes = passes;
     DevBuf<int32_t> cs;
     TF_TRY(cs.alloc(g.nbins + 1, s, "cell start"));
@@ -917,6 +920,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
 
     // largest neighbourhood -> shared-memory capacity of the count / fill passes
     DevBuf<int32_t> counts, stats;
+    build_trace().mark("cellstart+gather", s);
     TF_TRY(counts.alloc(n, s, "row counts"));
     TF_TRY(stats.alloc(4, s, "build stats"));
     TF_CUDA_TRY(cudaMemsetAsync(stats.p, 0, 4 * sizeof(int32_t), s));
@@ -936,11 +940,13 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     const bool wide = (double)n / (double)g.nbins >= 12.0;
 
     // a5 count
+    build_trace().mark("binstats+sync", s);
     NvtxRange r_count("tf_build/a5 count + a6 scan");
     if (dim == 3) TF_TRY(wide ? (launch_count<3, 4>(P, g, cap, counts.p, s)) : (launch_count<3, 2>(P, g, cap, counts.p, s)));
     else TF_TRY(wide ? (launch_count<2, 4>(P, g, cap, counts.p, s)) : (launch_count<2, 2>(P, g, cap, counts.p, s)));
 
     // a6 row pointers + nnz readback
+    build_trace().mark("count", s);
     TF_TRY(dalloc(&h->rowptr, n + 3, s, "rowptr (+2 padding for 16-byte bulk copies)"));
     TF_TRY(exclusive_scan_i32_i64(counts.p, h->rowptr, n, s));
     int64_t nnz = 0;
@@ -953,11 +959,13 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     h->nnz = nnz;
 
     // a7 fill
+    build_trace().mark("scan+sync", s);
     NvtxRange r_fill("tf_build/a7 fill");
     TF_TRY(dalloc(&h->cols, nnz + 4, s, "cols (nnz int32, +4 padding for 16-byte bulk copies)"));
     TF_TRY(dalloc(&h->vals, nnz + 4, s, "vals (nnz fp64, +4 padding)"));
     TF_TRY(dalloc(&h->hs, n, s, "Hs"));
     DevBuf<int32_t> large_rows;
+    build_trace().mark("alloc_csr", s);
     if (maxC > cap) TF_TRY(large_rows.alloc(n, s, "large-neighbourhood rows"));
     int fw = wide ? 4 : 2;  // warps per fill block (queries of one bin in parallel)
     if (const char *e = getenv("TOPOFILT_FILL_WARPS")) fw = atoi(e);  // tuning knob (benchmarks only)
@@ -970,6 +978,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
         else if (fw >= 4) TF_TRY((launch_fill<2, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
         else TF_TRY((launch_fill<2, 2>(P, g, h, cap, large_rows.p, stats.p, s)));
     }
+    build_trace().mark("fill", s);
     if (maxC > cap) {
         const int scap = 8192;
         const size_t smem = (size_t)scap * (sizeof(double) + sizeof(int32_t));
@@ -983,6 +992,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     int32_t tail[2] = {0, 0};
     TF_CUDA_TRY(cudaMemcpyAsync(tail, stats.p + 1, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     TF_CUDA_TRY(cudaStreamSynchronize(s));
+    build_trace().mark("rowsort+stats+sync", s);
     h->info.large_rows = tail[0];
     if (tail[1] != 0) {
         set_error("internal: fill pass disagreed with the count pass (row lengths)");

@@ -75,6 +75,20 @@ struct NvtxRange {
     NvtxRange &operator=(const NvtxRange &) = delete;
 };
 
+// Opt-in phase timer of the build (TOPOFILT_TRACE=1): CUDA events at phase boundaries on the
+// build stream, printed to stderr (ms per phase) when the build finishes. Off: no events.
+struct PhaseTrace {
+    static bool enabled();
+    void begin(cudaStream_t s);
+    void mark(const char *name, cudaStream_t s);
+    void report(const char *what);
+    bool on = false;
+    int k = 0;
+    cudaEvent_t ev[24] = {};
+    const char *name[24] = {};
+};
+PhaseTrace &build_trace();
+
 // ------------------------------------------------------------------ memory
 // Stream-ordered device allocation with the test-only allocation limit.
 tf_status dev_alloc(void **p, size_t bytes, cudaStream_t s, const char *what);
@@ -147,7 +161,7 @@ struct ApplyPlan {
     int unroll = 4;           // loads in flight per lane in the row loop (4 or 8)
     // row-range chunks of the host pipeline: windows [chunk_w[i], chunk_w[i+1]) cover rows
     // [chunk_r[i], chunk_r[i+1])
-    int nchunks = 0;
+    int nchunks = -1;  // -1: not computed yet
     int64_t chunk_w[9] = {};
     int32_t chunk_r[9] = {};
     int32_t chunk_maxcol[8] = {};  // largest column read by chunk i (-1: none)
@@ -224,6 +238,7 @@ tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s);
 // row-range chunk i of the plan (host pipeline); the sensitivity chunk 0 computes t = x*dc into
 // tbuf (cooperative), later chunks reuse it
+tf_status ensure_chunk_plan(tf_filter_s *h, cudaStream_t s);
 tf_status launch_density_range(const tf_filter_s *h, const double *x, double *out, int chunk, cudaStream_t s);
 tf_status launch_hadamard_piece(const tf_filter_s *h, const double *x, const double *dc, double *t, int piece,
                                 cudaStream_t s);
