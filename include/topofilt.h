@@ -21,6 +21,8 @@
  *     Device arrays are contiguous, 8-byte aligned, and owned by the caller.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *     Work is stream-ordered; apply calls are asynchronous (no host sync).
+ *   - A handle is bound to the CUDA device that was current when it was built; calls on it
+ *     must be made with that device current (TF_ERR_INVALID otherwise).
  *   - Every call returns tf_status; nothing throws or aborts across the ABI.
  *     On a non-OK status tf_last_error() returns a thread-local message.
  *   - Sizes: 1 <= n < 2^31 - 1 (int32 column indices); nnz < 2^63.

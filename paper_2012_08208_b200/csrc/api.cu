@@ -81,6 +81,16 @@ PhaseTrace &build_trace() {
     return t;
 }
 
+tf_status require_current_device(int device, const char *who) {
+    int cur = -1;
+    TF_CUDA_TRY(cudaGetDevice(&cur));
+    if (cur != device) {
+        set_error("%s: the handle was built on device %d but device %d is current", who, device, cur);
+        return TF_ERR_INVALID;
+    }
+    return TF_OK;
+}
+
 tf_status device_info(DeviceInfo *di) {
     TF_CUDA_TRY(cudaGetDevice(&di->device));
     // Keep freed stream-ordered allocations cached in the device's default pool (like a
@@ -185,6 +195,11 @@ static tf_status build_common(const double *c, int64_t n, int dim, double rmin, 
         set_error("host allocation failed");
         return TF_ERR_NOMEM;
     }
+    if (cudaGetDevice(&h->device) != cudaSuccess) {
+        delete h;
+        set_error("cudaGetDevice failed");
+        return TF_ERR_CUDA;
+    }
     h->n = n;
     h->dim = dim;
     h->rmin = rmin;
@@ -278,6 +293,7 @@ tf_status tf_build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h
         }
         tf_filter_s *f = new (std::nothrow) tf_filter_s();
         if (!f) return TF_ERR_NOMEM;
+        cudaGetDevice(&f->device);
         f->n = nx * ny * nzz;
         f->dim = dim;
         f->rmin = rmin;
@@ -328,6 +344,7 @@ static tf_status check_apply(tf_filter h, const double *x, const double *dc, dou
         set_error("filter handle is NULL");
         return TF_ERR_INVALID;
     }
+    TF_TRY(require_current_device(h->device, "apply"));
     TF_TRY(require_device(x, "x"));
     if (sens) TF_TRY(require_device(dc, "dc"));
     TF_TRY(require_device(out, "out"));
@@ -383,6 +400,7 @@ tf_status tf_sensitivity_filter_host(tf_filter h, const double *x_host, const do
         set_error("tf_sensitivity_filter_host: NULL argument");
         return TF_ERR_INVALID;
     }
+    TF_TRY(require_current_device(h->device, "tf_sensitivity_filter_host"));
     cudaStream_t s = (cudaStream_t)stream;
     TF_TRY(ensure_host_scratch(h, s, false));
     const size_t bytes = (size_t)h->n * sizeof(double);
@@ -400,6 +418,7 @@ tf_status tf_filter_iteration_host(tf_filter h, const double *x_host, const doub
         set_error("tf_filter_iteration_host: NULL argument");
         return TF_ERR_INVALID;
     }
+    TF_TRY(require_current_device(h->device, "tf_filter_iteration_host"));
     cudaStream_t s = (cudaStream_t)stream;
     TF_TRY(ensure_host_scratch(h, s, true));
     if (!h->side) TF_CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
@@ -495,6 +514,7 @@ tf_status tf_density_filter_host(tf_filter h, const double *x_host, double *out_
         set_error("tf_density_filter_host: NULL argument");
         return TF_ERR_INVALID;
     }
+    TF_TRY(require_current_device(h->device, "tf_density_filter_host"));
     cudaStream_t s = (cudaStream_t)stream;
     TF_TRY(ensure_host_scratch(h, s, false));
     const size_t bytes = (size_t)h->n * sizeof(double);
@@ -534,6 +554,7 @@ tf_status tf_filter_from_csr(const int64_t *rowptr_host, const int32_t *cols_hos
     cudaStream_t s = (cudaStream_t)stream;
     tf_filter_s *h = new (std::nothrow) tf_filter_s();
     if (!h) return TF_ERR_NOMEM;
+    cudaGetDevice(&h->device);
     h->n = n;
     h->nnz = nnz;
     tf_status st = TF_OK;

@@ -28,10 +28,14 @@
 
 #include <algorithm>
 
+#include <atomic>
+
 #include "tf_internal.cuh"
 
 namespace tf {
 namespace {
+
+constexpr int kMaxDevices = 64;
 
 #ifndef TF_APPLY_CW
 #define TF_APPLY_CW 10
@@ -299,8 +303,17 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
                          double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf_ext, int tpass) {
     const size_t smem = (size_t)kStages * (kStage * (sizeof(double) + sizeof(int32_t)) + kRowCap * sizeof(int64_t));
     auto kern = k_spmv<SENS, G, U>;
-    // per-instantiation attribute (dynamic shared memory above 48 KB needs the opt-in)
-    static int occ = 0;  // co-resident blocks per SM (a cooperative grid must not exceed it)
+    // per-instantiation, per-device attribute (dynamic shared memory above 48 KB needs the
+    // opt-in on every device the process launches on) and co-resident blocks per SM (a
+    // cooperative grid must not exceed it); cached after the first launch on each device
+    static std::atomic<int> occ_of[kMaxDevices];
+    int dev = 0;
+    TF_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kMaxDevices) {
+        set_error("device ordinal %d out of range", dev);
+        return TF_ERR_CUDA;
+    }
+    int occ = occ_of[dev].load(std::memory_order_acquire);
     if (!occ) {
         TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads + 32, smem));
@@ -308,6 +321,7 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
             set_error("apply kernel does not fit on an SM");
             return TF_ERR_CUDA;
         }
+        occ_of[dev].store(occ, std::memory_order_release);
     }
     if (wend <= wbeg) return TF_OK;
     const unsigned grid = (unsigned)std::min<int64_t>(

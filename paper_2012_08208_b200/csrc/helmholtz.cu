@@ -33,6 +33,7 @@
 #include "tf_internal.cuh"
 
 struct tf_helmholtz_s {
+    int device = -1;  // the CUDA device current at build time; every call must use it
     int64_t nn = 0, nc = 0, nnz = 0;
     int dim = 0;
     double R = 0;
@@ -674,6 +675,7 @@ TF_API tf_status tf_helmholtz_build(const double *nodes, int64_t n_nodes, const 
     TF_TRY(require_device(nodes, "tf_helmholtz_build: nodes"));
     TF_TRY(require_device(cells, "tf_helmholtz_build: cells"));
     tf_helmholtz_s *h = new tf_helmholtz_s;
+    cudaGetDevice(&h->device);
     h->nn = n_nodes, h->nc = n_cells, h->dim = dim, h->R = R;
     cudaStream_t s = (cudaStream_t)stream;
     const tf_status st = (dim == 2) ? hz_build<2>(nodes, n_nodes, cells, n_cells, R, s, h)
@@ -696,7 +698,7 @@ static tf_status hz_check(tf_helmholtz h, double rtol, int maxit, const char *wh
         set_error("%s: need rtol > 0 and maxit >= 1", who);
         return TF_ERR_INVALID;
     }
-    return TF_OK;
+    return require_current_device(h->device, who);
 }
 
 TF_API tf_status tf_helmholtz_filter(tf_helmholtz h, const double *sigma, double *out, double rtol, int maxit,

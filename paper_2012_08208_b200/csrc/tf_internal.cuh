@@ -134,6 +134,8 @@ struct DeviceInfo {
 tf_status device_info(DeviceInfo *di);
 // TF_ERR_INVALID unless p is a non-NULL device (or managed) pointer
 tf_status require_device(const void *p, const char *name);
+// TF_ERR_INVALID unless the current CUDA device is `device` (a handle's build device)
+tf_status require_current_device(int device, const char *who);
 
 // ------------------------------------------------------------------ grid of the cell list
 struct Grid {
@@ -183,6 +185,7 @@ struct StencilGeom {
 
 // ------------------------------------------------------------------ the handle
 struct tf_filter_s {
+    int device = -1;  // the CUDA device current at build time; every call must use it
     int64_t n = 0, nnz = 0;
     int dim = 0;
     double rmin = 0;
