@@ -311,8 +311,8 @@ def run_ours(args):
 
     # correctness guard on the timed path (one row sample, cheap)
     res = {}
-    if not args.no_e2e and rank == 0:
-        res["e2e"] = run_e2e(tf, c, x, dc, rmin, applies, n, nnz, dim, args)
+    if not args.no_e2e:  # every rank (its own GPU and host buffers); max time over ranks
+        res["e2e"] = run_e2e(tf, c, x, dc, rmin, applies, n, nnz, dim, args, dist, ws, device)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         v, times, desc = oracle_sample(c, x, dc, rmin, applies, args.cpu_rows, 1, args.config)
@@ -356,9 +356,11 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(tf, c, x, dc, rmin, applies, n, nnz, dim, args):
+def run_e2e(tf, c, x, dc, rmin, applies, n, nnz, dim, args, dist=None, ws=1, device=None):
     """Same step through the C ABI's host-buffer variants: H2D of centroids / x / dc from
-    pinned memory and D2H of every filtered field inside the timed region."""
+    pinned memory and D2H of every filtered field inside the timed region. Under torchrun every
+    rank runs it on its own GPU; each step is bracketed by a barrier and timed as the max over
+    ranks, and the value is the whole-job aggregate (like `value`)."""
     import torch
     cp = torch.from_numpy(c).pin_memory().numpy()
     xp = torch.from_numpy(x).pin_memory().numpy()
@@ -376,16 +378,18 @@ def run_e2e(tf, c, x, dc, rmin, applies, n, nnz, dim, args):
     torch.cuda.synchronize()
     ts = []
     for _ in range(args.e2e_steps):
+        if dist is not None:
+            dist.barrier()
         t0 = time.perf_counter()
         step()
         torch.cuda.synchronize()
-        ts.append(time.perf_counter() - t0)
+        ts.append(reduce_max(time.perf_counter() - t0, dist, device))
     t = statistics.median(ts)
     h2d = 8 * dim * n + applies * (16 * n)
     d2h = applies * (8 * n + 8 * n)
-    return {"value": step_bytes(n, nnz, dim, applies) / t / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "seconds_per_step": t,
-            "timer": "host wall clock around the blocking C-ABI *_host calls"}
+    return {"value": aggregate(step_bytes(n, nnz, dim, applies), ws, t) / 1e9, "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "seconds_per_step": t,
+            "timer": "host wall clock around the blocking C-ABI *_host calls, max over ranks"}
 
 
 # ------------------------------------------------------------------ reference arm (the oracle)
