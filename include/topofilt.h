@@ -160,6 +160,14 @@ TF_API tf_status tf_sensitivity_filter_energy(tf_filter h, const double *x, cons
 /* tf_density_filter -- out_i = (sum_j W_ij x_j) / Hs_i. Same conventions. */
 TF_API tf_status tf_density_filter(tf_filter h, const double *x, double *out, void *stream);
 
+/* tf_filter_both -- both filters of one iteration in ONE pass over H (the CSR streams from HBM
+ * once; each entry gathers t_j = x_j*dc_j and x_j): sens_out as tf_sensitivity_filter,
+ * dens_out as tf_density_filter, bitwise (same per-row summation order).
+ *   x, dc, sens_out, dens_out: device fp64 [n]; the outputs must not overlap each other, x or dc.
+ * Asynchronous on `stream`. Stencil handles run the two stencil passes. */
+TF_API tf_status tf_filter_both(tf_filter h, const double *x, const double *dc, double *sens_out, double *dens_out,
+                                void *stream);
+
 /* tf_free -- release everything the handle owns (synchronises the device). NULL: no-op. */
 TF_API void tf_free(tf_filter h);
 

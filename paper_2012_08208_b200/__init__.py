@@ -28,7 +28,7 @@ EXPORTS = [
     "tf_free", "tf_last_error", "tf_build_filter_host", "tf_sensitivity_filter_host",
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
     "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update", "tf_sensitivity_filter_energy",
-    "tf_filter_iteration_host",
+    "tf_filter_iteration_host", "tf_filter_both",
     # include/topofilt_helmholtz.h (NEXT-3)
     "tf_helmholtz_build", "tf_helmholtz_filter", "tf_helmholtz_sensitivity", "tf_helmholtz_view",
     "tf_helmholtz_free",
@@ -91,6 +91,7 @@ def _load():
         "tf_oc_update": ([P, P, I64, D, D, D, D, D, P, P, P, P], I32),
         "tf_sensitivity_filter_energy": ([P, P, P, D, P, P], I32),
         "tf_filter_iteration_host": ([P, P, P, P, P, P], I32),
+        "tf_filter_both": ([P, P, P, P, P, P], I32),
         "tf_helmholtz_build": ([P, I64, P, I64, I32, D, P, PP], I32),
         "tf_helmholtz_filter": ([P, P, P, D, I32, P, P], I32),
         "tf_helmholtz_sensitivity": ([P, P, P, P, D, I32, P, P], I32),
@@ -185,6 +186,10 @@ class Filter:
         tf_density_filter(self, x, out, stream)
         return out
 
+    def both(self, x, dc, sens_out=None, dens_out=None, stream=None):
+        """Both filters in one pass over H; returns (sensitivity, density)."""
+        return tf_filter_both(self, x, dc, sens_out, dens_out, stream)
+
     def csr(self):
         """Zero-copy torch views (rowptr int64, cols int32, vals f64, hs f64) tied to this handle."""
         import torch
@@ -273,6 +278,19 @@ def tf_sensitivity_filter_energy(f: Filter, x, U, penal: float, out=None, stream
                                              _dptr(U, "U", torch.float64, f.n), float(penal),
                                              _dptr(out, "out", torch.float64, f.n), _stream_ptr(stream)))
     return out
+
+
+def tf_filter_both(f: Filter, x, dc, sens_out=None, dens_out=None, stream=None):
+    """Sensitivity and density filter in one pass over H (bitwise equal to the separate calls)."""
+    import torch
+    if sens_out is None:
+        sens_out = torch.empty_like(x)
+    if dens_out is None:
+        dens_out = torch.empty_like(x)
+    _check(_lib.tf_filter_both(f.handle, _dptr(x, "x", torch.float64, f.n), _dptr(dc, "dc", torch.float64, f.n),
+                               _dptr(sens_out, "sens_out", torch.float64, f.n),
+                               _dptr(dens_out, "dens_out", torch.float64, f.n), _stream_ptr(stream)))
+    return sens_out, dens_out
 
 
 def tf_density_filter(f: Filter, x, out, stream=None):

@@ -380,6 +380,18 @@ tf_status tf_density_filter(tf_filter h, const double *x, double *out, void *str
     return launch_density(h, x, out, (cudaStream_t)stream);
 }
 
+tf_status tf_filter_both(tf_filter h, const double *x, const double *dc, double *sens_out, double *dens_out,
+                         void *stream) {
+    TF_TRY(check_apply(h, x, dc, sens_out, true));
+    TF_TRY(check_apply(h, x, nullptr, dens_out, false));
+    const size_t bytes = (size_t)h->n * sizeof(double);
+    if (overlaps(dens_out, dc, bytes) || overlaps(sens_out, dens_out, bytes)) {
+        set_error("tf_filter_both: outputs must not overlap each other, x or dc");
+        return TF_ERR_INVALID;
+    }
+    return launch_both(h, x, dc, sens_out, dens_out, (cudaStream_t)stream);
+}
+
 // Device staging for the *_host calls: stream-ordered pool allocations on the caller's stream
 // (every later use is on that stream or on the side stream after an event recorded on it).
 static tf_status ensure_host_scratch(tf_filter h, cudaStream_t s, bool second_out) {

@@ -138,7 +138,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // shared counter (dynamic balance, no block-wide barriers); each row is reduced by G lanes
 // that issue U predicated (col, val) shared loads and U x/dc gathers before accumulating,
 // and the group leader writes out[r] directly.
-template <bool SENS, int G, int U>
+// MODE 0: density; 1: sensitivity; 2: both filters in one pass over H (sensitivity -> out,
+// density -> out2): the CSR streams once, each entry gathers t_j and x_j.
+template <int MODE, int G, int U>
 __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int64_t *__restrict__ rowptr,
                                                                       const int32_t *__restrict__ cols,
                                                                       const double *__restrict__ vals,
@@ -146,11 +148,13 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                                                                       const double *__restrict__ x,
                                                                       const double *__restrict__ dc,
                                                                       double *__restrict__ out,
+                                                                      double *__restrict__ out2,
                                                                       const int32_t *__restrict__ rb,
                                                                       const int64_t *__restrict__ wlo,
                                                                       int64_t nwin, double *tbuf, int64_t n,
                                                                       double penal, int energy, int64_t wbeg,
                                                                       int64_t wend, int tpass) {
+    constexpr bool SENS = MODE != 0, BOTH = MODE == 2;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *svals = reinterpret_cast<double *>(smem_raw);                           // [kStages][kStage]
     int64_t *srow = reinterpret_cast<int64_t *>(svals + kStages * kStage);          // [kStages][kRowCap]
@@ -214,6 +218,13 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                 const double xi = __ldg(x + i);
                 tbuf[i] = xi * ((-penal * pow(xi, penal - 1.0)) * __ldg(dc + i));
             }
+        } else if (BOTH) {
+            // (t, x) interleaved: one 16-byte gather per entry serves both filters
+            double2 *tx = reinterpret_cast<double2 *>(tbuf);
+            for (int64_t i = (int64_t)blockIdx.x * kThreads + tid; i < n; i += (int64_t)gridDim.x * kThreads) {
+                const double xi = __ldg(x + i);
+                tx[i] = make_double2(xi * __ldg(dc + i), xi);
+            }
         } else {
             for (int64_t i = (int64_t)blockIdx.x * kThreads + tid; i < n; i += (int64_t)gridDim.x * kThreads)
                 tbuf[i] = __ldg(x + i) * __ldg(dc + i);
@@ -222,6 +233,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
     }
     // t was written in this launch: read it with plain cached loads, never the read-only path
     const double *gsrc = SENS ? tbuf : x;
+    const double2 *gtx = reinterpret_cast<const double2 *>(tbuf);  // BOTH: (t, x) pairs
     constexpr int RPW = 32 / G;  // rows per warp claim
     const int sub = lane & (G - 1);
     int it = 0;
@@ -242,7 +254,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                 rbase = __shfl_sync(0xffffffffu, rbase, 0);
                 if (rbase >= R) break;
                 const int rr = rbase + lane / G;
-                double acc = 0.0, hs_r = 1.0, x_r = 1.0;
+                double acc = 0.0, acc2 = 0.0, hs_r = 1.0, x_r = 1.0;
                 if (rr < R) {
                     const int r = r0 + rr;
                     if (sub == 0) hs_r = hs[r], x_r = x[r];  // epilogue operands, issued early
@@ -256,20 +268,42 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                         j[u] = (i < e) ? sc[i] : -1;
                         v[u] = (i < e) ? sv[i] : 0.0;
                     }
+                    if (BOTH) {
+                        double xg[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        t[u] = (j[u] >= 0) ? __ldca(gsrc + j[u]) : 0.0;
+                        for (int u = 0; u < U; ++u) {
+                            const double2 p = (j[u] >= 0) ? __ldca(gtx + j[u]) : make_double2(0.0, 0.0);
+                            t[u] = p.x;
+                            xg[u] = p.y;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) acc2 = fma(v[u], xg[u], acc2);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) t[u] = (j[u] >= 0) ? __ldca(gsrc + j[u]) : 0.0;
+                    }
 #pragma unroll
                     for (int u = 0; u < U; ++u) acc = fma(v[u], t[u], acc);
                     for (int i = s + sub + U * G; i < e; i += G) {  // rows longer than U*G
                         const int32_t jj = sc[i];
-                        const double tt = __ldca(gsrc + jj);
-                        acc = fma(sv[i], tt, acc);
+                        if (BOTH) {
+                            const double2 p = __ldca(gtx + jj);
+                            acc = fma(sv[i], p.x, acc);
+                            acc2 = fma(sv[i], p.y, acc2);
+                        } else {
+                            acc = fma(sv[i], __ldca(gsrc + jj), acc);
+                        }
                     }
                 }
 #pragma unroll
-                for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (sub == 0 && rr < R) out[r0 + rr] = finish<SENS>(acc, hs_r, x_r);
+                for (int o = G / 2; o > 0; o >>= 1) {
+                    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                    if (BOTH) acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+                }
+                if (sub == 0 && rr < R) {
+                    out[r0 + rr] = finish<SENS>(acc, hs_r, x_r);
+                    if (BOTH) out2[r0 + rr] = finish<false>(acc2, hs_r, x_r);
+                }
             }
         } else {
             // window too large to stage (long rows): a whole warp per row, from global memory
@@ -280,14 +314,25 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                 if (rr >= R) break;
                 const int r = r0 + rr;
                 const int64_t s = rowptr[r], e = rowptr[r + 1];
-                double acc = 0.0;
+                double acc = 0.0, acc2 = 0.0;
                 for (int64_t k = s + lane; k < e; k += 32) {
                     const int32_t jj = cols[k];
-                    const double tt = __ldca(gsrc + jj);
-                    acc = fma(vals[k], tt, acc);
+                    if (BOTH) {
+                        const double2 p = __ldca(gtx + jj);
+                        acc = fma(vals[k], p.x, acc);
+                        acc2 = fma(vals[k], p.y, acc2);
+                    } else {
+                        acc = fma(vals[k], __ldca(gsrc + jj), acc);
+                    }
                 }
-                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (lane == 0) out[r] = finish<SENS>(acc, hs[r], x[r]);
+                for (int o = 16; o > 0; o >>= 1) {
+                    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                    if (BOTH) acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+                }
+                if (lane == 0) {
+                    out[r] = finish<SENS>(acc, hs[r], x[r]);
+                    if (BOTH) out2[r] = finish<false>(acc2, hs[r], x[r]);
+                }
             }
         }
         __syncwarp();
@@ -298,11 +343,13 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
 // Windows [wbeg, wend) of the plan. SENS: tbuf == nullptr -> per-call scratch, t pass and a
 // cooperative launch (the normal API); tbuf given -> tpass selects whether this launch computes
 // t (cooperative) or reuses it (ordinary launch; the row-range chunks of the host pipeline).
-template <bool SENS, int G, int U>
-tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s,
-                         double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf_ext, int tpass) {
+template <int MODE, int G, int U>
+tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc, double *out, double *out2,
+                         cudaStream_t s, double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf_ext,
+                         int tpass) {
+    constexpr bool SENS = MODE != 0;
     const size_t smem = (size_t)kStages * (kStage * (sizeof(double) + sizeof(int32_t)) + kRowCap * sizeof(int64_t));
-    auto kern = k_spmv<SENS, G, U>;
+    auto kern = k_spmv<MODE, G, U>;
     // per-instantiation, per-device attribute (dynamic shared memory above 48 KB needs the
     // opt-in on every device the process launches on) and co-resident blocks per SM (a
     // cooperative grid must not exceed it); cached after the first launch on each device
@@ -336,10 +383,11 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
     if (SENS && (tbuf_ext == nullptr || tpass)) {
         // per-call scratch (stream-ordered) unless the caller owns it: concurrent applies on
         // different streams stay safe
-        if (!tbuf_ext) TF_TRY(dalloc(&tbuf, (size_t)n, s, "sensitivity scratch t = x*dc"));
+        if (!tbuf_ext) TF_TRY(dalloc(&tbuf, (size_t)n * (MODE == 2 ? 2 : 1), s, "sensitivity scratch t = x*dc"));
         tpass = 1;
         void *args[] = {(void *)&rowptr, (void *)&cols, (void *)&vals,  (void *)&hs,     (void *)&x,
-                        (void *)&dc,     (void *)&out,  (void *)&rb,    (void *)&wlo,    (void *)&nwin,
+                        (void *)&dc,     (void *)&out,  (void *)&out2,  (void *)&rb,     (void *)&wlo,
+                        (void *)&nwin,
                         (void *)&tbuf,   (void *)&n,    (void *)&penal, (void *)&energy, (void *)&wbeg,
                         (void *)&wend,   (void *)&tpass};
         cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads + 32), args, smem, s);
@@ -351,31 +399,33 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
         }
         return TF_OK;
     }
-    kern<<<grid, kThreads + 32, smem, s>>>(rowptr, cols, vals, hs, x, dc, out, rb, wlo, nwin, tbuf, n, penal, energy,
-                                           wbeg, wend, 0);
+    kern<<<grid, kThreads + 32, smem, s>>>(rowptr, cols, vals, hs, x, dc, out, out2, rb, wlo, nwin, tbuf, n, penal,
+                                           energy, wbeg, wend, 0);
     TF_LAUNCH_CHECK();
     return TF_OK;
 }
 
-template <bool SENS, int G>
-tf_status launch_spmv_g(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s,
-                        double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf, int tpass) {
-    if (h->plan.unroll >= 8) return launch_spmv_gu<SENS, G, 8>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
-    return launch_spmv_gu<SENS, G, 4>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
+template <int MODE, int G>
+tf_status launch_spmv_g(const tf_filter_s *h, const double *x, const double *dc, double *out, double *out2,
+                        cudaStream_t s, double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf,
+                        int tpass) {
+    if (h->plan.unroll >= 8)
+        return launch_spmv_gu<MODE, G, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
+    return launch_spmv_gu<MODE, G, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
 }
 
-template <bool SENS>
+template <int MODE>
 tf_status launch_spmv(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s,
                       double penal = 0.0, int energy = 0, int64_t wbeg = 0, int64_t wend = -1,
-                      double *tbuf = nullptr, int tpass = 1) {
+                      double *tbuf = nullptr, int tpass = 1, double *out2 = nullptr) {
     if (wend < 0) wend = h->plan.nblocks;
     switch (h->plan.group) {
-        case 1: return launch_spmv_g<SENS, 1>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
-        case 2: return launch_spmv_g<SENS, 2>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
-        case 4: return launch_spmv_g<SENS, 4>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
-        case 8: return launch_spmv_g<SENS, 8>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
-        case 16: return launch_spmv_g<SENS, 16>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
-        default: return launch_spmv_g<SENS, 32>(h, x, dc, out, s, penal, energy, wbeg, wend, tbuf, tpass);
+        case 1: return launch_spmv_g<MODE, 1>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
+        case 2: return launch_spmv_g<MODE, 2>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
+        case 4: return launch_spmv_g<MODE, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
+        case 8: return launch_spmv_g<MODE, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
+        case 16: return launch_spmv_g<MODE, 16>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
+        default: return launch_spmv_g<MODE, 32>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
     }
 }
 
@@ -498,12 +548,12 @@ tf_status ensure_chunk_plan(tf_filter_s *h, cudaStream_t s) {
 }
 
 tf_status launch_density_range(const tf_filter_s *h, const double *x, double *out, int chunk, cudaStream_t s) {
-    return launch_spmv<false>(h, x, nullptr, out, s, 0.0, 0, h->plan.chunk_w[chunk], h->plan.chunk_w[chunk + 1]);
+    return launch_spmv<0>(h, x, nullptr, out, s, 0.0, 0, h->plan.chunk_w[chunk], h->plan.chunk_w[chunk + 1]);
 }
 
 tf_status launch_sensitivity_range(const tf_filter_s *h, const double *x, const double *dc, double *out, double *tbuf,
                                    int chunk, int tpass, cudaStream_t s) {
-    return launch_spmv<true>(h, x, dc, out, s, 0.0, 0, h->plan.chunk_w[chunk], h->plan.chunk_w[chunk + 1], tbuf,
+    return launch_spmv<1>(h, x, dc, out, s, 0.0, 0, h->plan.chunk_w[chunk], h->plan.chunk_w[chunk + 1], tbuf,
                              tpass);
 }
 
@@ -511,18 +561,28 @@ tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double
                              cudaStream_t s) {
     NvtxRange r("tf_apply/sensitivity");
     if (h->stencil.K > 0) return launch_stencil(h, x, dc, out, true, s);
-    return launch_spmv<true>(h, x, dc, out, s);
+    return launch_spmv<1>(h, x, dc, out, s);
 }
 
 tf_status launch_sensitivity_energy(const tf_filter_s *h, const double *x, const double *U, double penal,
                                     double *out, cudaStream_t s) {
-    return launch_spmv<true>(h, x, U, out, s, penal, 1);
+    return launch_spmv<1>(h, x, U, out, s, penal, 1);
+}
+
+tf_status launch_both(const tf_filter_s *h, const double *x, const double *dc, double *sens_out, double *dens_out,
+                      cudaStream_t s) {
+    NvtxRange r("tf_apply/both");
+    if (h->stencil.K > 0) {
+        TF_TRY(launch_stencil(h, x, dc, sens_out, true, s));
+        return launch_stencil(h, x, nullptr, dens_out, false, s);
+    }
+    return launch_spmv<2>(h, x, dc, sens_out, s, 0.0, 0, 0, -1, nullptr, 1, dens_out);
 }
 
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s) {
     NvtxRange r("tf_apply/density");
     if (h->stencil.K > 0) return launch_stencil(h, x, nullptr, out, false, s);
-    return launch_spmv<false>(h, x, nullptr, out, s);
+    return launch_spmv<0>(h, x, nullptr, out, s);
 }
 
 }  // namespace tf

@@ -239,6 +239,9 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s);
 tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double *dc, double *out,
                              cudaStream_t s);
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s);
+// both filters in one pass over H (sensitivity -> sens_out, density -> dens_out)
+tf_status launch_both(const tf_filter_s *h, const double *x, const double *dc, double *sens_out, double *dens_out,
+                      cudaStream_t s);
 // row-range chunk i of the plan (host pipeline); the sensitivity chunk 0 computes t = x*dc into
 // tbuf (cooperative), later chunks reuse it
 tf_status ensure_chunk_plan(tf_filter_s *h, cudaStream_t s);

@@ -316,6 +316,45 @@ def test_iteration_host_pipeline(tf, case):
         np.testing.assert_array_equal(d2, want_d)
 
 
+@pytest.mark.parametrize("case", ["c1", "c2", "c4", "ragged_long_rows", "stencil_c3"])
+def test_filter_both_bitwise(tf, case):
+    """tf_filter_both (one pass over H, two gathers per entry) equals the separate sensitivity and
+    density calls bitwise, incl. the unstaged long-row path; and the oracle at 1e-10."""
+    if case == "ragged_long_rows":
+        rng = np.random.default_rng(9)
+        n = 6000
+        lens = rng.integers(1, 40, size=n)
+        lens[[10, 3000]] = [12000, 7000]
+        rowptr = np.zeros(n + 1, np.int64)
+        rowptr[1:] = np.cumsum(lens)
+        cols = np.concatenate([np.sort(rng.choice(n, size=l, replace=l > n)) for l in lens]).astype(np.int32)
+        vals = rng.uniform(0, 2, size=rowptr[-1])
+        hs = np.add.reduceat(vals, rowptr[:-1])
+        ref = oracle.CSR(rowptr, cols, vals, hs)
+        f = tf.tf_filter_from_csr(rowptr, cols, vals, hs)
+        x, dc = inputs_for(n, 615)
+    elif case == "stencil_c3":
+        c, x, dc, rmin = synth.workload(3)
+        f = tf.tf_build_stencil(3, 160, 80, 80, 1.0, rmin)
+        ref = None
+    else:
+        c, x, dc, rmin = synth.workload(int(case[1]))
+        f = tf.tf_build_filter(dev(c), rmin)
+        ref = oracle.build_celllist(c, rmin)
+    xd, dcd = dev(x), dev(dc)
+    s, d = f.both(xd, dcd)
+    assert torch.equal(s, f.sensitivity(xd, dcd))
+    assert torch.equal(d, f.density(xd))
+    if ref is not None:
+        assert_rel(s.cpu().numpy(), oracle.apply_sensitivity(ref, x, dc), RTOL_OUT, "both: sensitivity")
+        assert_rel(d.cpu().numpy(), oracle.apply_density(ref, x), RTOL_OUT, "both: density")
+    with pytest.raises(tf.TopofiltError):
+        f.both(xd, dcd, sens_out=dcd)
+    o = torch.empty_like(xd)
+    with pytest.raises(tf.TopofiltError):
+        f.both(xd, dcd, sens_out=o, dens_out=o)
+
+
 def test_streams_concurrent_applies(tf):
     c, x, dc, rmin = synth.workload(3)
     f = tf.tf_build_filter(dev(c), rmin)

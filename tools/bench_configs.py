@@ -201,7 +201,35 @@ def helmholtz_rows():
         h.close()
 
 
+def both_rows():
+    """tf_filter_both: both filters in one pass over H, against the two separate calls (cold L2).
+    Algorithmic bytes: 12 nnz + 8(N+1) + 40N (CSR once; x, dc, Hs read; two outputs written)."""
+    dev = torch.device("cuda:0")
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+    for cfg in (3, 4, 5):
+        c, x, dc, rmin = bench.load_workload(cfg)[:4]
+        n = c.shape[0]
+        f = tf.tf_build_filter(torch.from_numpy(c).to(dev), rmin)
+        xd, dd = torch.from_numpy(x).to(dev), torch.from_numpy(dc).to(dev)
+        so, do = torch.empty_like(xd), torch.empty_like(xd)
+        f.both(xd, dd, so, do)
+        tb = timed(lambda: f.both(xd, dd, so, do), 10, flush=flush)
+
+        def sep():
+            f.sensitivity(xd, dd, out=so)
+            f.density(xd, out=do)
+        ts = timed(sep, 10, flush=flush)
+        byt = 12 * f.nnz + 8 * (n + 1) + 40 * n
+        print(json.dumps({"both_config": cfg, "n": n, "nnz": f.nnz, "both_us_cold": tb * 1e6,
+                          "separate_us_cold": ts * 1e6, "speedup": ts / tb, "both_gbs": byt / tb / 1e9,
+                          "both_frac_8tbs": byt / tb / 1e9 / HBM, "iters_per_s": 1.0 / tb}), flush=True)
+        f.close()
+
+
 if __name__ == "__main__":
+    if os.environ.get("BOTH_ONLY"):
+        both_rows()
+        sys.exit(0)
     if os.environ.get("HELM_ONLY"):
         helmholtz_rows()
         sys.exit(0)
@@ -217,3 +245,4 @@ if __name__ == "__main__":
     graph_rows()
     oc_rows()
     helmholtz_rows()
+    both_rows()
