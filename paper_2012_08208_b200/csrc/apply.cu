@@ -6,19 +6,22 @@
 //                Hadamard product, the max floor and the division fused in)
 //   density      out_i = (sum_k vals[k] * x[cols[k]]) / Hs_i   (BASELINE.json north_star)
 //
-// Work split: the nnz stream is cut into windows of kWindow entries; block b owns the rows
-// whose first entry falls in window b (row-block table rb[], built once per filter by
-// make_apply_plan). Per block:
-//   1. one thread issues two TMA bulk copies (cp.async.bulk, mbarrier completion) that
-//      stage the block's contiguous cols/vals range in shared memory -- the CSR stream never
-//      touches the LSU/L1 data pipe, which is left to the x/dc gathers (the measured
-//      bottleneck of an LDG-staged version);
-//   2. G lanes per row (G from the average row length) read their row's cols/vals from
-//      shared memory, gather x (and dc) through L1, and accumulate in registers; a
-//      G-lane xor-shuffle tree gives the row sum (deterministic, no atomics);
-//   3. one thread per row applies the elementwise epilogue with coalesced hs/x loads.
-// Rows that make a block's range exceed the staging capacity are reduced one at a time by
-// the whole block straight from global memory.
+// Work split: the nnz stream is cut into windows of kWindow entries; window w owns the rows
+// whose first entry falls in it (row-block table rb[] and 16-byte aligned staging ranges wlo[],
+// built once per filter by make_apply_plan). k_spmv is persistent and warp-specialised:
+//   * a producer warp streams the block's windows (w = blockIdx.x + k*gridDim.x) into a
+//     kStages-deep shared-memory ring with TMA bulk copies (cp.async.bulk, mbarrier
+//     completion, L2 evict_first) of cols/vals/rowptr -- the CSR stream never touches the
+//     LSU/L1 data pipe, which is left to the gathers;
+//   * kCW consumer warps claim 32/G rows at a time from a per-stage counter (dynamic balance),
+//     G lanes per row read cols/vals from shared memory, issue U gathers before accumulating,
+//     reduce with a G-lane xor-shuffle tree (deterministic) and write the fused epilogue;
+//   * sensitivity: a cooperative launch first forms t = x o dc (one gather per entry instead of
+//     two) and grid-syncs; the producer's first kStages copies overlap that pass;
+//   * MODE 2 (tf_filter_both): (t, x) pairs, one 16-byte gather per entry, two accumulators;
+//   * [wbeg, wend) window ranges serve the host pipeline's row-range chunks.
+// Windows whose staging range exceeds the ring capacity (long rows) are reduced one row per
+// warp straight from global memory.
 //
 // Roofline: HBM. Algorithmic bytes per apply = 12*nnz + 8(N+1) + 32N (sensitivity) or
 // + 24N (density); gathers of x/dc hit L2/L1 (neighbour columns are index-local).
