@@ -11,13 +11,19 @@
 //   a2 k_bbox_*     bounding box + finiteness check (host reads 7 doubles back)
 //   a3 k_keys       bin key per centroid, key = (kz*ny + ky)*nx + kx
 //   a4 radix sort (radix.cu), k_cellstart, k_gather_sorted (SoA copy of sorted centroids)
-//   a5 k_count      warp per query bin: exact fp64 pair test, ballot/popc -> row lengths
+//   a5 k_count      block per query bin: the 3^(dim-1) candidate x-triples staged once as
+//                   bin-local fp32 SoA; each warp sweeps two queries at a time with packed
+//                   f32x2 math (per-lane counts); pairs inside the proven fp32 error band are
+//                   decided by the exact fp64 test (R4b) -> row lengths
 //   a6 scan (scan.cu) -> rowptr; nnz read back (the one data-dependent host sync)
-//   a7 k_fill       block per query bin: the 3^dim candidate bins are staged in shared
-//                   memory IN ASCENDING ID ORDER (merge-rank of the per-bin sorted runs),
-//                   so ballot compaction emits every row's columns already ascending;
-//                   weights fp64 with Hs fused. Neighbourhoods larger than the shared
-//                   memory capacity take a global-memory path plus k_rowsort.
+//   a7 k_fill       block per query bin: the candidates are staged and sorted by id with a
+//                   block-wide shared-memory radix sort, so ballot compaction emits every
+//                   row's columns already ascending; phase A (packed fp32 sweep) lists the
+//                   candidates that may lie inside rmin, phase B decides them exactly in fp64
+//                   and writes cols, weights and Hs. Neighbourhoods larger than the shared
+//                   memory capacity take a global-memory path plus k_rowsort. An always-on
+//                   invariant flags any row whose fill length differs from its count.
+// Phase boundaries are traceable with TOPOFILT_TRACE=1 (ms per phase on stderr).
 //
 // Exactness (R2-R4): the pair test and weight use the caller's centroid bytes,
 // d2 = (dx*dx + dy*dy) + dz*dz with __dmul_rn/__dadd_rn (never contracted to FMA),
