@@ -113,6 +113,19 @@ TF_API tf_status tf_build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, d
                                   void *stream, tf_filter *out);
 
 /* tf_filter_nnz -- stored entries of a CSR filter, or those of the equivalent CSR of a stencil. */
+/* tf_build_lattice -- matrix-free filter on a periodic lattice with several cells per cube (row a10
+ * generalised): cell index ntypes*((k*ny + j)*nx + i) + t with centroid h*((i, j, k) + o_t), e.g.
+ * BoxMesh tetrahedra (6 per cube, PAPER.md:330-333 meshes) or triangulated squares (2 per square).
+ * The weight depends only on (s, t, cube offset), so per source type a host-built table of
+ * (offset, target type, w) replaces the stored rows (same fp64 pair test and weight as
+ * tf_build_filter on those centroids); Hs is recomputed with boundary truncation.
+ *   type_offsets_host: HOST fp64 [ntypes x dim], each component in [0, 1) (fractions of h).
+ * Applies, host variants and tf_filter_both work as for any handle; tf_filter_view returns
+ * TF_ERR_INVALID (no CSR is stored); tf_filter_nnz gives the equivalent CSR's nonzeros.
+ * Errors: TF_ERR_INVALID (dim, sizes, ntypes not in [1, 8], offsets outside [0, 1), rmin/h not
+ * finite > 0, more than 4096 offsets or a halo tile beyond shared memory). */
+TF_API tf_status tf_build_lattice(int dim, int64_t nx, int64_t ny, int64_t nz, double h, int ntypes,
+                                  const double *type_offsets_host, double rmin, void *stream, tf_filter *out);
 TF_API int64_t tf_filter_nnz(tf_filter h);
 
 /*

@@ -28,7 +28,7 @@ EXPORTS = [
     "tf_free", "tf_last_error", "tf_build_filter_host", "tf_sensitivity_filter_host",
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
     "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update", "tf_sensitivity_filter_energy",
-    "tf_filter_iteration_host", "tf_filter_both",
+    "tf_filter_iteration_host", "tf_filter_both", "tf_build_lattice",
     # include/topofilt_helmholtz.h (NEXT-3)
     "tf_helmholtz_build", "tf_helmholtz_filter", "tf_helmholtz_sensitivity", "tf_helmholtz_view",
     "tf_helmholtz_free",
@@ -92,6 +92,7 @@ def _load():
         "tf_sensitivity_filter_energy": ([P, P, P, D, P, P], I32),
         "tf_filter_iteration_host": ([P, P, P, P, P, P], I32),
         "tf_filter_both": ([P, P, P, P, P, P], I32),
+        "tf_build_lattice": ([I32, I64, I64, I64, D, I32, P, D, P, PP], I32),
         "tf_helmholtz_build": ([P, I64, P, I64, I32, D, P, PP], I32),
         "tf_helmholtz_filter": ([P, P, P, D, I32, P, P], I32),
         "tf_helmholtz_sensitivity": ([P, P, P, P, D, I32, P, P], I32),
@@ -194,6 +195,9 @@ class Filter:
         """Zero-copy torch views (rowptr int64, cols int32, vals f64, hs f64) tied to this handle."""
         import torch
         v = self._v
+        if v is None:  # matrix-free handle: the C ABI reports it (TF_ERR_INVALID)
+            v = tf_view()
+            _check(_lib.tf_filter_view(self.handle, ctypes.byref(v)))
         mk = lambda p, n, t: torch.as_tensor(_CudaArray(p, (n,), t), device="cuda")
         return (mk(v.rowptr, self.n + 1, "<i8"), mk(v.cols, self.nnz, "<i4"),
                 mk(v.vals, self.nnz, "<f8"), mk(v.hs, self.n, "<f8"))
@@ -249,6 +253,20 @@ def tf_build_stencil(dim: int, nx: int, ny: int, nz: int, h: float, rmin: float,
     _check(_lib.tf_build_stencil(int(dim), int(nx), int(ny), int(nz), float(h), float(rmin), _stream_ptr(stream),
                                  ctypes.byref(hnd)))
     n = int(nx) * int(ny) * (int(nz) if dim == 3 else 1)
+    return Filter(hnd, stencil=(int(dim), float(rmin), n))
+
+
+def tf_build_lattice(dim: int, nx: int, ny: int, nz: int, h: float, type_offsets, rmin: float,
+                     stream=None) -> Filter:
+    """Matrix-free filter on a periodic lattice: cell T*((k*ny + j)*nx + i) + t at h*((i,j,k) + o_t)."""
+    o = np.ascontiguousarray(type_offsets, dtype=np.float64)
+    if o.ndim != 2 or o.shape[1] != dim:
+        raise ValueError("type_offsets must be [ntypes, dim]")
+    hnd = ctypes.c_void_p()
+    _check(_lib.tf_build_lattice(int(dim), int(nx), int(ny), int(nz), float(h), int(o.shape[0]),
+                                 o.ctypes.data_as(ctypes.c_void_p), float(rmin), _stream_ptr(stream),
+                                 ctypes.byref(hnd)))
+    n = int(nx) * int(ny) * (int(nz) if dim == 3 else 1) * int(o.shape[0])
     return Filter(hnd, stencil=(int(dim), float(rmin), n))
 
 

@@ -149,6 +149,7 @@ static void destroy(tf_filter_s *h) {
     if (h->plan.wlo) cudaFreeAsync(h->plan.wlo, 0);
     if (h->stencil_off) cudaFreeAsync(h->stencil_off, 0);
     if (h->stencil_w) cudaFreeAsync(h->stencil_w, 0);
+    if (h->lattice_table) cudaFreeAsync(h->lattice_table, 0);
     if (h->hx) cudaFreeAsync(h->hx, 0);
     if (h->hdc) cudaFreeAsync(h->hdc, 0);
     if (h->hout) cudaFreeAsync(h->hout, 0);
@@ -306,6 +307,55 @@ tf_status tf_build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h
         return TF_OK;
     } catch (...) {
         set_error("tf_build_stencil: unexpected host exception");
+        return TF_ERR_NOMEM;
+    }
+}
+
+tf_status tf_build_lattice(int dim, int64_t nx, int64_t ny, int64_t nz, double h, int ntypes,
+                           const double *type_offsets_host, double rmin, void *stream, tf_filter *out) {
+    try {
+        if (!out) {
+            set_error("out is NULL");
+            return TF_ERR_INVALID;
+        }
+        *out = nullptr;
+        if (dim != 2 && dim != 3) {
+            set_error("dim must be 2 or 3 (got %d)", dim);
+            return TF_ERR_INVALID;
+        }
+        if (ntypes < 1 || ntypes > kMaxTypes || !type_offsets_host) {
+            set_error("ntypes must be in [1, %d] with a host array of ntypes*dim offsets", kMaxTypes);
+            return TF_ERR_INVALID;
+        }
+        for (int i = 0; i < ntypes * dim; ++i)
+            if (!(type_offsets_host[i] >= 0.0 && type_offsets_host[i] < 1.0)) {
+                set_error("type offsets must lie in [0, 1) (entry %d)", i);
+                return TF_ERR_INVALID;
+            }
+        const int64_t nzz = (dim == 3) ? nz : 1;
+        if (nx < 1 || ny < 1 || nzz < 1 || nx * ny * nzz * ntypes >= (int64_t)0x7fffffff) {
+            set_error("lattice dimensions must be >= 1 with nx*ny*nz*ntypes < 2^31-1");
+            return TF_ERR_INVALID;
+        }
+        if (!isfinite(rmin) || !(rmin > 0.0) || !isfinite(h) || !(h > 0.0)) {
+            set_error("rmin and h must be finite and > 0");
+            return TF_ERR_INVALID;
+        }
+        tf_filter_s *f = new (std::nothrow) tf_filter_s();
+        if (!f) return TF_ERR_NOMEM;
+        cudaGetDevice(&f->device);
+        f->n = nx * ny * nzz * ntypes;
+        f->dim = dim;
+        f->rmin = rmin;
+        tf_status st = build_lattice(dim, nx, ny, nzz, h, ntypes, type_offsets_host, rmin, (cudaStream_t)stream, f);
+        if (st != TF_OK) {
+            destroy(f);
+            return st;
+        }
+        *out = f;
+        return TF_OK;
+    } catch (...) {
+        set_error("tf_build_lattice: unexpected host exception");
         return TF_ERR_NOMEM;
     }
 }

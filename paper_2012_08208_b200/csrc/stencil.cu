@@ -17,6 +17,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <new>
 #include <vector>
 
 #include "tf_internal.cuh"
@@ -88,7 +89,205 @@ __global__ void __launch_bounds__(256) k_stencil(StencilGeom sg, const int4 *__r
     out[g] = SENS ? acc / (hs * fmax(1e-3, __ldg(x + g))) : acc / hs;
 }
 
+// ------------------------------------------------------------------ periodic lattices (T types)
+// Cells T*cube + s at h*((i,j,k) + o_s) (BoxMesh-style tetrahedra: T = 6; triangulated squares:
+// T = 2). The weight between type s at cube c and type t at cube c + d depends only on
+// (s, t, d), so per source type a table of (d, t, w) replaces the stored rows. The block stages
+// t = x*dc of its haloed tile ONE ARRAY PER TYPE ([T][HZ][HY][HX]: a warp's lanes read 32
+// consecutive cubes of one type, conflict-free), and each warp computes one (row, type) item
+// of 32 cubes at a time, so every lane of the warp walks the same offset list (broadcast
+// shared-memory reads). Tiles away from the grid boundary skip the in-grid mask: their row sum
+// is the type's full sum hs_full_t, bitwise the masked offset-order sum (fma(w, 1, h) = h + w).
+// One 16-byte entry per offset (tile index delta = type * plane + cube delta, cube delta for the
+// mask, weight), precomputed at build for the tile shape: every lane of a warp reads the same
+// entry, so each offset costs one broadcast shared-memory wavefront besides the tile read.
+constexpr int kLatMaxOffs = 4096;
+struct __align__(16) LatEntry {
+    int delta, mdelta;
+    double w;
+};
+
+template <bool SENS, int DIM, int RC, int TT>
+__global__ void __launch_bounds__(256) k_lattice(StencilGeom sg, const LatEntry *__restrict__ tab,
+                                                 const double *__restrict__ hs_cell, const double *__restrict__ x,
+                                                 const double *__restrict__ dc, double *__restrict__ out) {
+    extern __shared__ double tile[];
+    constexpr int TY = (DIM == 3) ? 4 : 8, TZ = (DIM == 3) ? 2 : 1;
+    const int T = TT ? TT : sg.T;
+    const int R = RC ? RC : sg.R;
+    const int HX = kTX + 2 * R, HY = TY + 2 * R, HZ = (DIM == 3) ? TZ + 2 * R : 1;
+    const int plane = HX * HY * HZ;
+    const int bx0 = blockIdx.x * kTX, by0 = blockIdx.y * TY, bz0 = (DIM == 3) ? blockIdx.z * TZ : 0;
+    const int nx = (int)sg.nx, ny = (int)sg.ny, nz = (int)sg.nz;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rows = HY * HZ;
+    // stage t (0 outside the grid: out-of-grid neighbours add fma(w, 0, acc) = acc exactly)
+    for (int row = warp; row < rows; row += 8) {
+        const int hy = row % HY, hz = row / HY;
+        const int gy = by0 + hy - R, gz = (DIM == 3) ? bz0 + hz - R : 0;
+        const bool rok = gy >= 0 && gy < ny && gz >= 0 && gz < nz;
+        const int64_t rbase = ((int64_t)gz * ny + gy) * nx;
+        // the row's HX cubes x T types are contiguous in global memory: coalesced
+        for (int e = lane; e < HX * T; e += 32) {
+            const int hx = e / T, t = e - hx * T;
+            const int gx = bx0 + hx - R;
+            double v = 0.0;
+            if (rok && gx >= 0 && gx < nx) {
+                const int64_t g = (rbase + gx) * T + t;
+                v = SENS ? __ldg(x + g) * __ldg(dc + g) : __ldg(x + g);
+            }
+            tile[(size_t)t * plane + row * HX + hx] = v;
+        }
+    }
+    LatEntry *s_tab = reinterpret_cast<LatEntry *>(tile + (((size_t)T * plane + 1) & ~(size_t)1));
+    for (int o = threadIdx.x; o < sg.K; o += 256) s_tab[o] = tab[o];
+    __syncthreads();
+    // items: (pair of rows, type); one table read serves the two rows' tile reads
+    constexpr int NP = TY * TZ / 2;
+    for (int item = warp; item < NP * T; item += 8) {
+        const int s = item % T, p = item / T;
+        const int ri0 = 2 * p, ri1 = 2 * p + 1;
+        const int ly0 = ri0 % TY, lz0 = ri0 / TY, ly1 = ri1 % TY, lz1 = ri1 / TY;
+        const int c0 = (((DIM == 3) ? lz0 + R : 0) * HY + (ly0 + R)) * HX + (lane + R);
+        const int c1 = (((DIM == 3) ? lz1 + R : 0) * HY + (ly1 + R)) * HX + (lane + R);
+        const int o0 = sg.kstart[s], o1 = sg.kstart[s + 1];
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+        for (int o = o0; o < o1; ++o) {
+            const LatEntry e = s_tab[o];
+            a0 = fma(e.w, tile[c0 + e.delta], a0);
+            a1 = fma(e.w, tile[c1 + e.delta], a1);
+        }
+        const int gx = bx0 + lane;
+        auto finish = [&](double acc, int ly, int lz) {
+            const int gy = by0 + ly, gz = bz0 + lz;
+            if (gx >= nx || gy >= ny || gz >= nz) return;
+            const int64_t g = (((int64_t)gz * ny + gy) * nx + gx) * T + s;
+            // interior cells: the type's full row sum; near the boundary: the truncated sum built once
+            const bool inner = gx >= R && gx + R < nx && gy >= R && gy + R < ny && (DIM == 2 || (gz >= R && gz + R < nz));
+            const double hs = inner ? sg.hs_full_t[s] : __ldg(hs_cell + g);
+            out[g] = SENS ? acc / (hs * fmax(1e-3, __ldg(x + g))) : acc / hs;
+        };
+        finish(a0, ly0, lz0);
+        finish(a1, ly1, lz1);
+    }
+}
+
+// Row sums with boundary truncation, once per lattice handle: in offset order, only in-grid
+// neighbours (bitwise the interior full sum where nothing is truncated).
+template <int DIM>
+__global__ void k_lattice_hs(StencilGeom sg, const int4 *__restrict__ offs, const double *__restrict__ w,
+                             double *__restrict__ hs) {
+    const int64_t n = sg.nx * sg.ny * sg.nz * sg.T;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cube = g / sg.T;
+        const int s = (int)(g - cube * sg.T);
+        const int64_t cx = cube % sg.nx, cy = (cube / sg.nx) % sg.ny, cz = cube / (sg.nx * sg.ny);
+        double h = 0.0;
+        for (int o = sg.kstart[s]; o < sg.kstart[s + 1]; ++o) {
+            const int4 q = offs[o];
+            const int64_t ax = cx + q.x, ay = cy + q.y, az = cz + q.z;
+            if (ax >= 0 && ax < sg.nx && ay >= 0 && ay < sg.ny && az >= 0 && az < sg.nz) h += w[o];
+        }
+        hs[g] = h;
+    }
+}
+
 }  // namespace
+
+tf_status build_lattice(int dim, int64_t nx, int64_t ny, int64_t nz, double h, int ntypes, const double *o,
+                        double rmin, cudaStream_t s, tf_filter_s *f) {
+    // per source type s: every (target type t, cube offset d) with d2 < rmin^2, the same fp64
+    // pair expression as the CSR build on centroids h*(cube + o): delta = h*(d + o_t - o_s)
+    const double r2 = rmin * rmin;
+    const int Rs = (int)floor(rmin / h) + 2;
+    std::vector<int4> off;
+    std::vector<double> w;
+    StencilGeom &sg = f->stencil;
+    sg.T = ntypes;
+    const int zr = (dim == 3) ? Rs : 0;
+    for (int st = 0; st < ntypes; ++st) {
+        sg.kstart[st] = (int)off.size();
+        double hsum = 0.0;
+        for (int tt = 0; tt < ntypes; ++tt)
+            for (int c = -zr; c <= zr; ++c)
+                for (int b = -Rs; b <= Rs; ++b)
+                    for (int a = -Rs; a <= Rs; ++a) {
+                        const double ox = o[tt * dim + 0] - o[st * dim + 0], oy = o[tt * dim + 1] - o[st * dim + 1];
+                        const double oz = (dim == 3) ? o[tt * dim + 2] - o[st * dim + 2] : 0.0;
+                        const volatile double dx = ((double)a + ox) * h, dy = ((double)b + oy) * h;
+                        const volatile double dz = ((double)c + oz) * h;
+                        const volatile double dxx = dx * dx, dyy = dy * dy, dzz = dz * dz;
+                        const volatile double s2 = dxx + dyy;
+                        const double d2 = (dim == 3) ? (double)(s2 + dzz) : (double)s2;
+                        if (!(d2 < r2)) continue;
+                        double ww = rmin;
+                        if (d2 > 0.0) {
+                            const volatile double sq = sqrt(d2);
+                            ww = rmin - sq;
+                        }
+                        if (ww < 0) ww = 0;
+                        off.push_back(make_int4(a, b, c, tt));
+                        w.push_back(ww);
+                        hsum += ww;  // offset order: the kernel's masked sum is bitwise this
+                    }
+        sg.hs_full_t[st] = hsum;
+    }
+    sg.kstart[ntypes] = (int)off.size();
+    if ((int)off.size() > kLatMaxOffs) {
+        set_error("lattice radius too large (%zu offsets > %d); use tf_build_filter", off.size(), kLatMaxOffs);
+        return TF_ERR_INVALID;
+    }
+    int Rk = 0;
+    for (const int4 &q : off) Rk = std::max(Rk, std::max(abs(q.x), std::max(abs(q.y), abs(q.z))));
+    const int TY = (dim == 3) ? 4 : 8, TZ = (dim == 3) ? 2 : 1;
+    const int HX = kTX + 2 * Rk, HY = TY + 2 * Rk;
+    const size_t plane = (size_t)HX * HY * (dim == 3 ? TZ + 2 * Rk : 1);
+    const size_t smem = sizeof(double) * (plane * ntypes + 1) + sizeof(LatEntry) * off.size();
+    std::vector<LatEntry> tab(off.size());
+    for (size_t o = 0; o < off.size(); ++o) {
+        const int md = ((dim == 3) ? off[o].z * HY * HX : 0) + off[o].y * HX + off[o].x;
+        tab[o].mdelta = md;
+        tab[o].delta = off[o].w * (int)plane + md;
+        tab[o].w = w[o];
+    }
+    if (smem > 200 * 1024) {
+        set_error("lattice halo tile too large for shared memory (rmin/h or types); use tf_build_filter");
+        return TF_ERR_INVALID;
+    }
+    sg.dim = dim;
+    sg.nx = nx, sg.ny = ny, sg.nz = (dim == 3) ? nz : 1;
+    sg.R = Rk;
+    sg.K = (int)off.size();
+    sg.ty = TY;
+    sg.tz = TZ;
+    sg.h = h;
+    sg.hs_full = 0.0;
+    TF_TRY(dev_alloc(&f->lattice_table, sizeof(LatEntry) * tab.size(), s, "lattice offset table"));
+    TF_CUDA_TRY(cudaMemcpyAsync(f->lattice_table, tab.data(), sizeof(LatEntry) * tab.size(), cudaMemcpyHostToDevice,
+                                s));
+    TF_TRY(dalloc(&f->stencil_off, off.size(), s, "lattice offsets"));
+    TF_TRY(dalloc(&f->stencil_w, w.size(), s, "lattice weights"));
+    TF_CUDA_TRY(cudaMemcpyAsync(f->stencil_off, off.data(), sizeof(int4) * off.size(), cudaMemcpyHostToDevice, s));
+    TF_CUDA_TRY(cudaMemcpyAsync(f->stencil_w, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice, s));
+    const int64_t ncell = nx * ny * sg.nz * ntypes;
+    TF_TRY(dalloc(&f->hs, (size_t)ncell, s, "lattice row sums"));
+    {
+        DeviceInfo di;
+        TF_TRY(device_info(&di));
+        const unsigned blocks = (unsigned)std::min<int64_t>((ncell + 255) / 256, (int64_t)di.sms * 16);
+        if (dim == 3) k_lattice_hs<3><<<blocks, 256, 0, s>>>(sg, f->stencil_off, f->stencil_w, f->hs);
+        else k_lattice_hs<2><<<blocks, 256, 0, s>>>(sg, f->stencil_off, f->stencil_w, f->hs);
+        TF_LAUNCH_CHECK();
+    }
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    int64_t nnz = 0;  // the equivalent CSR's nonzeros
+    for (const int4 &q : off)
+        nnz += std::max<int64_t>(0, nx - abs(q.x)) * std::max<int64_t>(0, ny - abs(q.y)) *
+               std::max<int64_t>(0, sg.nz - abs(q.z));
+    f->nnz = nnz;
+    return TF_OK;
+}
 
 tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, double rmin, cudaStream_t s,
                         tf_filter_s *f) {
@@ -149,9 +348,40 @@ tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, d
     return TF_OK;
 }
 
+static tf_status launch_lattice(const tf_filter_s *f, const double *x, const double *dc, double *out, bool sens,
+                                cudaStream_t s) {
+    const StencilGeom &sg = f->stencil;
+    const int TY = sg.ty, TZ = (sg.dim == 3) ? sg.tz : 1, R = sg.R;
+    const size_t plane = (size_t)(kTX + 2 * R) * (TY + 2 * R) * ((sg.dim == 3) ? TZ + 2 * R : 1);
+    const size_t smem = sizeof(double) * (plane * sg.T + 1) + sizeof(LatEntry) * (size_t)sg.K;
+    const LatEntry *tab = reinterpret_cast<const LatEntry *>(f->lattice_table);
+    dim3 grid((unsigned)((sg.nx + kTX - 1) / kTX), (unsigned)((sg.ny + TY - 1) / TY),
+              (unsigned)((sg.dim == 3) ? (sg.nz + TZ - 1) / TZ : 1));
+    auto go = [&](auto kern) -> tf_status {
+        TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, 256, smem, s>>>(sg, tab, f->hs, x, dc, out);
+        TF_LAUNCH_CHECK();
+        return TF_OK;
+    };
+    // specialisations: (3D, R 2, 6 types) = BoxMesh tetrahedra at rmin 1.5h; (2D, 2 types) = triangles
+    if (sg.dim == 3 && R == 2 && sg.T == 6)
+        return sens ? go(k_lattice<true, 3, 2, 6>) : go(k_lattice<false, 3, 2, 6>);
+    if (sg.dim == 2 && sg.T == 2) {
+        switch (R) {
+            case 1: return sens ? go(k_lattice<true, 2, 1, 2>) : go(k_lattice<false, 2, 1, 2>);
+            case 2: return sens ? go(k_lattice<true, 2, 2, 2>) : go(k_lattice<false, 2, 2, 2>);
+            case 3: return sens ? go(k_lattice<true, 2, 3, 2>) : go(k_lattice<false, 2, 3, 2>);
+            default: break;
+        }
+    }
+    if (sg.dim == 3) return sens ? go(k_lattice<true, 3, 0, 0>) : go(k_lattice<false, 3, 0, 0>);
+    return sens ? go(k_lattice<true, 2, 0, 0>) : go(k_lattice<false, 2, 0, 0>);
+}
+
 tf_status launch_stencil(const tf_filter_s *f, const double *x, const double *dc, double *out, bool sens,
                          cudaStream_t s) {
     const StencilGeom &sg = f->stencil;
+    if (sg.T > 1) return launch_lattice(f, x, dc, out, sens, s);
     const int TY = sg.ty, TZ = (sg.dim == 3) ? sg.tz : 1, R = sg.R;
     const size_t smem = 2 * sizeof(double) * (size_t)(kTX + 2 * R) * (TY + 2 * R) * ((sg.dim == 3) ? TZ + 2 * R : 1) +
                         sizeof(int) * ((sg.K + 1) & ~1) + sizeof(double) * sg.K;

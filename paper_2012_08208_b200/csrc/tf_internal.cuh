@@ -171,6 +171,7 @@ struct ApplyPlan {
 constexpr int kMaxChunks = 8;
 
 // ------------------------------------------------------------------ matrix-free stencil (a10)
+constexpr int kMaxTypes = 8;  // cells per lattice cube (tf_build_lattice)
 struct StencilGeom {
     int dim = 0;
     int64_t nx = 0, ny = 0, nz = 0;
@@ -179,6 +180,11 @@ struct StencilGeom {
     int ty = 4, tz = 2;
     double h = 0;
     double hs_full = 0;  // row sum of an interior cell (all offsets in the grid)
+    // periodic lattices (T > 1 types per cube, cell = T*cube + type): offsets of type s are
+    // [kstart[s], kstart[s+1]) as (dx, dy, dz, target type); hs_full_t = interior row sums
+    int T = 1;
+    int kstart[kMaxTypes + 1] = {};
+    double hs_full_t[kMaxTypes] = {};
 };
 
 }  // namespace tf
@@ -206,6 +212,8 @@ struct tf_filter_s {
     tf::StencilGeom stencil;
     int4 *stencil_off = nullptr;
     double *stencil_w = nullptr;
+    // periodic lattice handles: the device offset table (16-byte entries for the tile shape)
+    void *lattice_table = nullptr;
 };
 
 namespace tf {
@@ -229,6 +237,8 @@ tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, d
                         tf_filter_s *f);
 tf_status launch_stencil(const tf_filter_s *f, const double *x, const double *dc, double *out, bool sens,
                          cudaStream_t s);
+tf_status build_lattice(int dim, int64_t nx, int64_t ny, int64_t nz, double h, int ntypes, const double *type_offsets,
+                        double rmin, cudaStream_t s, tf_filter_s *f);
 
 // oc.cu (NEXT-1)
 tf_status oc_update(const double *x, const double *dc, int64_t n, double volfrac, double move, double l1,

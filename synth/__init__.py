@@ -136,6 +136,27 @@ def kuhn_tets(nx: int, ny: int, nz: int) -> np.ndarray:
     return out.reshape(ncube * 6, 3)
 
 
+def tri_lattice_offsets(pattern: str = "right") -> np.ndarray:
+    """Type offsets (fractions of h) of tri_grid's two triangles per square, in its t order
+    (vertex means: "right" t0 = (2/3, 1/3), t1 = (1/3, 2/3); "left" t0 = (1/3, 1/3), t1 = (2/3, 2/3))."""
+    if pattern == "right":
+        return np.array([[2.0 / 3.0, 1.0 / 3.0], [1.0 / 3.0, 2.0 / 3.0]])
+    if pattern == "left":
+        return np.array([[1.0 / 3.0, 1.0 / 3.0], [2.0 / 3.0, 2.0 / 3.0]])
+    raise ValueError("periodic with two types per square: 'right' or 'left'")
+
+
+def kuhn_lattice_offsets() -> np.ndarray:
+    """Type offsets of kuhn_tets' six tetrahedra per cube, in its t order: (2 e_s1 + e_s2 + 1)/4."""
+    out = []
+    for s in _PERMS:
+        o = np.ones(3)
+        o[s[0]] += 2.0
+        o[s[1]] += 1.0
+        out.append(o / 4.0)
+    return np.array(out)
+
+
 def tri_mesh(nx: int, ny: int, pattern: str = "right", jitter: float = 0.0, stream: int = 0):
     """Nodes and cells of the tri_grid triangulation (same cell order and vertex order, so the
     vertex means are tri_grid's centroids when jitter = 0). Node index j*(nx+1) + i at (i, j);

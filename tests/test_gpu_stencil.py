@@ -85,3 +85,75 @@ def test_stencil_host_variant_and_errors(tf):
         tf.tf_build_stencil(3, 3, 3, 3, 1.0, 50.0)  # too many offsets
     with pytest.raises(tf.TopofiltError):
         tf.tf_build_stencil(3, 3, 3, 3, 0.0, 1.5)
+
+
+# ------------------------------------------------------------------ periodic lattices (tf_build_lattice)
+
+def lattice_cells(kind, nx, ny, nz):
+    if kind == "kuhn":
+        return synth.kuhn_tets(nx, ny, nz), synth.kuhn_lattice_offsets(), 3
+    return synth.tri_grid(nx, ny, kind), synth.tri_lattice_offsets(kind), 2
+
+
+LATTICE_CASES = [
+    # (kind, nx, ny, nz, rmin)
+    ("right", 300, 100, 1, 2.5),    # config 2
+    ("left", 41, 13, 1, 1.7),
+    ("right", 3, 2, 1, 4.0),         # every cell near the boundary, reach > grid
+    ("kuhn", 20, 12, 10, 1.5),       # config 5's lattice, scaled down
+    ("kuhn", 9, 7, 5, 2.2),
+    ("kuhn", 2, 2, 1, 1.5),          # boundary-only tiles
+    ("kuhn", 4, 3, 3, 0.3),          # diagonal only
+]
+
+
+@pytest.mark.parametrize("kind,nx,ny,nz,rmin", LATTICE_CASES)
+def test_lattice_matches_oracle(tf, kind, nx, ny, nz, rmin):
+    """Both filters of the matrix-free lattice vs the oracle's CSR of the same centroids (1e-10);
+    equivalent nnz exact; the device CSR path on the same centroids agrees too."""
+    c, offs, dim = lattice_cells(kind, nx, ny, nz)
+    n = c.shape[0]
+    ref = oracle.build_celllist(c, rmin)
+    f = tf.tf_build_lattice(dim, nx, ny, nz, 1.0, offs, rmin)
+    assert f.n == n and f.nnz == ref.nnz
+    x = synth.uniform(41, 0, n, 0.001, 1.0)
+    dc = (-3.0 * (x * x)) * synth.uniform(42, 0, n, 0.5, 1.5)
+    xs, dcs = torch.from_numpy(x).cuda(), torch.from_numpy(dc).cuda()
+    s = f.sensitivity(xs, dcs).cpu().numpy()
+    d = f.density(xs).cpu().numpy()
+    assert_rel(s, oracle.apply_sensitivity(ref, x, dc), RTOL_OUT, "lattice sens")
+    assert_rel(d, oracle.apply_density(ref, x), RTOL_OUT, "lattice dens")
+    sb, db = f.both(xs, dcs)
+    assert np.array_equal(sb.cpu().numpy(), s) and np.array_equal(db.cpu().numpy(), d)
+    s2, d2 = tf.tf_filter_iteration_host(f, x, dc)
+    assert np.array_equal(s2, s) and np.array_equal(d2, d)
+    f.close()
+
+
+def test_lattice_config5_vs_csr(tf):
+    """Config 5 (12M Kuhn tets): the lattice filters agree with the stored-CSR path on every
+    cell (1e-10 relative) and the equivalent nnz is the lattice count 1,030,251,952."""
+    c, x, dc, rmin = synth.workload(5)
+    xs, dcs = torch.from_numpy(x).cuda(), torch.from_numpy(dc).cuda()
+    f = tf.tf_build_lattice(3, 200, 100, 100, 1.0, synth.kuhn_lattice_offsets(), rmin)
+    assert f.nnz == 1_030_251_952
+    s_l, d_l = f.sensitivity(xs, dcs).cpu().numpy(), f.density(xs).cpu().numpy()
+    f.close()
+    g = tf.tf_build_filter(torch.from_numpy(c).cuda(), rmin)
+    s_c, d_c = g.sensitivity(xs, dcs).cpu().numpy(), g.density(xs).cpu().numpy()
+    g.close()
+    assert_rel(s_l, s_c, RTOL_OUT, "c5 lattice vs CSR sens")
+    assert_rel(d_l, d_c, RTOL_OUT, "c5 lattice vs CSR dens")
+
+
+def test_lattice_rejects_bad_args(tf):
+    o = synth.kuhn_lattice_offsets()
+    for args in [(3, 4, 4, 4, 1.0, np.zeros((0, 3)), 1.5), (3, 4, 4, 4, 1.0, np.zeros((9, 3)), 1.5),
+                 (3, 4, 4, 4, 1.0, o + 0.5, 1.5), (3, 4, 4, 4, 1.0, -o, 1.5), (3, 4, 4, 4, 0.0, o, 1.5),
+                 (3, 4, 4, 4, 1.0, o, 40.0), (3, 0, 4, 4, 1.0, o, 1.5)]:
+        with pytest.raises(tf.TopofiltError):
+            tf.tf_build_lattice(*args)
+    f = tf.tf_build_lattice(3, 4, 4, 4, 1.0, o, 1.5)
+    with pytest.raises(tf.TopofiltError):
+        tf.tf_filter_view(f)
+    f.close()

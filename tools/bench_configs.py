@@ -201,6 +201,33 @@ def helmholtz_rows():
         h.close()
 
 
+def lattice_rows():
+    """Matrix-free periodic lattice (tf_build_lattice) vs the stored CSR on configs 2 and 5
+    (cold L2): the same filters without streaming H (x, dc, out only: 24 B/cell sensitivity)."""
+    dev = torch.device("cuda:0")
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+    for cfg, (nx, ny, nz, offs, dim) in ((2, (300, 100, 1, synth.tri_lattice_offsets("right"), 2)),
+                                         (5, (200, 100, 100, synth.kuhn_lattice_offsets(), 3))):
+        c, x, dc, rmin = synth.workload(cfg)
+        xd, dd = torch.from_numpy(x).to(dev), torch.from_numpy(dc).to(dev)
+        out = torch.empty_like(xd)
+        f = tf.tf_build_lattice(dim, nx, ny, nz, 1.0, offs, rmin)
+        f.sensitivity(xd, dd, out=out)
+        ls = timed(lambda: f.sensitivity(xd, dd, out=out), 10, flush=flush)
+        ld = timed(lambda: f.density(xd, out=out), 10, flush=flush)
+        g = tf.tf_build_filter(torch.from_numpy(c).to(dev), rmin)
+        g.sensitivity(xd, dd, out=out)
+        cs = timed(lambda: g.sensitivity(xd, dd, out=out), 10, flush=flush)
+        cd = timed(lambda: g.density(xd, out=out), 10, flush=flush)
+        n = x.shape[0]
+        print(json.dumps({"lattice_config": cfg, "n": n, "nnz_equiv": f.nnz, "types": int(offs.shape[0]),
+                          "sens_us_cold": ls * 1e6, "dens_us_cold": ld * 1e6, "csr_sens_us_cold": cs * 1e6,
+                          "csr_dens_us_cold": cd * 1e6, "sens_speedup": cs / ls, "dens_speedup": cd / ld,
+                          "sens_own_gbs": 24 * n / ls / 1e9, "dens_own_gbs": 16 * n / ld / 1e9}), flush=True)
+        f.close()
+        g.close()
+
+
 def both_rows():
     """tf_filter_both: both filters in one pass over H, against the two separate calls (cold L2).
     Algorithmic bytes: 12 nnz + 8(N+1) + 40N (CSR once; x, dc, Hs read; two outputs written)."""
@@ -227,6 +254,9 @@ def both_rows():
 
 
 if __name__ == "__main__":
+    if os.environ.get("LATTICE_ONLY"):
+        lattice_rows()
+        sys.exit(0)
     if os.environ.get("BOTH_ONLY"):
         both_rows()
         sys.exit(0)
@@ -246,3 +276,4 @@ if __name__ == "__main__":
     oc_rows()
     helmholtz_rows()
     both_rows()
+    lattice_rows()
