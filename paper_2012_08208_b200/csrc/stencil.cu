@@ -183,6 +183,11 @@ __global__ void k_lattice_hs(StencilGeom sg, const int4 *__restrict__ offs, cons
         const int64_t cube = g / sg.T;
         const int s = (int)(g - cube * sg.T);
         const int64_t cx = cube % sg.nx, cy = (cube / sg.nx) % sg.ny, cz = cube / (sg.nx * sg.ny);
+        const int R = sg.R;
+        if (cx >= R && cx + R < sg.nx && cy >= R && cy + R < sg.ny && (DIM == 2 || (cz >= R && cz + R < sg.nz))) {
+            hs[g] = sg.hs_full_t[s];  // nothing truncated: the full offset-order sum
+            continue;
+        }
         double h = 0.0;
         for (int o = sg.kstart[s]; o < sg.kstart[s + 1]; ++o) {
             const int4 q = offs[o];
@@ -363,9 +368,15 @@ static tf_status launch_lattice(const tf_filter_s *f, const double *x, const dou
         TF_LAUNCH_CHECK();
         return TF_OK;
     };
-    // specialisations: (3D, R 2, 6 types) = BoxMesh tetrahedra at rmin 1.5h; (2D, 2 types) = triangles
-    if (sg.dim == 3 && R == 2 && sg.T == 6)
-        return sens ? go(k_lattice<true, 3, 2, 6>) : go(k_lattice<false, 3, 2, 6>);
+    // specialisations: (3D, 6 types) = BoxMesh tetrahedra (reach 1 cube at rmin <= 1.5h: type
+    // offsets differ by <= h/2 per axis), (2D, 2 types) = triangulated squares
+    if (sg.dim == 3 && sg.T == 6) {
+        switch (R) {
+            case 1: return sens ? go(k_lattice<true, 3, 1, 6>) : go(k_lattice<false, 3, 1, 6>);
+            case 2: return sens ? go(k_lattice<true, 3, 2, 6>) : go(k_lattice<false, 3, 2, 6>);
+            default: break;
+        }
+    }
     if (sg.dim == 2 && sg.T == 2) {
         switch (R) {
             case 1: return sens ? go(k_lattice<true, 2, 1, 2>) : go(k_lattice<false, 2, 1, 2>);
