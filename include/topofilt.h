@@ -219,6 +219,11 @@ TF_API tf_status tf_filter_from_csr(const int64_t *rowptr_host, const int32_t *c
                              void *stream, tf_filter *out);
 
 /* Number of CUDA kernels this library has launched in this process (monotone counter). */
+/* tf_halo_pack -- dst[i] = src[idx[i]], i < m (device arrays; idx int32 in [0, n_src)): gathers the
+ * boundary values a slab shard sends to a neighbour (NEXT-4). Asynchronous.
+ * Errors: TF_ERR_INVALID (NULL / host pointers, m < 0). m = 0 is a no-op. */
+TF_API tf_status tf_halo_pack(const double *src, const int32_t *idx, int64_t m, double *dst, void *stream);
+
 TF_API uint64_t tf_kernel_launches(void);
 
 /* TEST HOOK: make every single device allocation larger than `bytes` fail with

@@ -28,7 +28,7 @@ EXPORTS = [
     "tf_free", "tf_last_error", "tf_build_filter_host", "tf_sensitivity_filter_host",
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
     "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update", "tf_sensitivity_filter_energy",
-    "tf_filter_iteration_host", "tf_filter_both", "tf_build_lattice",
+    "tf_filter_iteration_host", "tf_filter_both", "tf_build_lattice", "tf_halo_pack",
     # include/topofilt_helmholtz.h (NEXT-3)
     "tf_helmholtz_build", "tf_helmholtz_filter", "tf_helmholtz_sensitivity", "tf_helmholtz_view",
     "tf_helmholtz_free",
@@ -93,6 +93,7 @@ def _load():
         "tf_filter_iteration_host": ([P, P, P, P, P, P], I32),
         "tf_filter_both": ([P, P, P, P, P, P], I32),
         "tf_build_lattice": ([I32, I64, I64, I64, D, I32, P, D, P, PP], I32),
+        "tf_halo_pack": ([P, P, I64, P, P], I32),
         "tf_helmholtz_build": ([P, I64, P, I64, I32, D, P, PP], I32),
         "tf_helmholtz_filter": ([P, P, P, D, I32, P, P], I32),
         "tf_helmholtz_sensitivity": ([P, P, P, P, D, I32, P, P], I32),

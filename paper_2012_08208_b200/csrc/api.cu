@@ -235,6 +235,18 @@ int tf_version(void) { return TOPOFILT_VERSION; }
 
 const char *tf_last_error(void) { return g_err; }
 
+tf_status tf_halo_pack(const double *src, const int32_t *idx, int64_t m, double *dst, void *stream) {
+    if (m < 0) {
+        set_error("tf_halo_pack: m must be >= 0");
+        return TF_ERR_INVALID;
+    }
+    if (m == 0) return TF_OK;
+    TF_TRY(require_device(src, "tf_halo_pack: src"));
+    TF_TRY(require_device(idx, "tf_halo_pack: idx"));
+    TF_TRY(require_device(dst, "tf_halo_pack: dst"));
+    return launch_halo_pack(src, idx, m, dst, (cudaStream_t)stream);
+}
+
 uint64_t tf_kernel_launches(void) { return g_launches.load(); }
 
 void tf_debug_set_alloc_limit(uint64_t bytes) { g_alloc_limit.store(bytes); }

@@ -550,6 +550,20 @@ tf_status ensure_chunk_plan(tf_filter_s *h, cudaStream_t s) {
     return TF_OK;
 }
 
+__global__ void k_halo_pack(const double *__restrict__ src, const int32_t *__restrict__ idx, int64_t m,
+                            double *__restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+tf_status launch_halo_pack(const double *src, const int32_t *idx, int64_t m, double *dst, cudaStream_t s) {
+    if (m <= 0) return TF_OK;
+    const unsigned grid = (unsigned)std::min<int64_t>((m + 255) / 256, 148 * 8);
+    k_halo_pack<<<grid, 256, 0, s>>>(src, idx, m, dst);
+    TF_LAUNCH_CHECK();
+    return TF_OK;
+}
+
 tf_status launch_density_range(const tf_filter_s *h, const double *x, double *out, int chunk, cudaStream_t s) {
     return launch_spmv<0>(h, x, nullptr, out, s, 0.0, 0, h->plan.chunk_w[chunk], h->plan.chunk_w[chunk + 1]);
 }

@@ -255,6 +255,7 @@ tf_status launch_both(const tf_filter_s *h, const double *x, const double *dc, d
 // row-range chunk i of the plan (host pipeline); the sensitivity chunk 0 computes t = x*dc into
 // tbuf (cooperative), later chunks reuse it
 tf_status ensure_chunk_plan(tf_filter_s *h, cudaStream_t s);
+tf_status launch_halo_pack(const double *src, const int32_t *idx, int64_t m, double *dst, cudaStream_t s);
 tf_status launch_density_range(const tf_filter_s *h, const double *x, double *out, int chunk, cudaStream_t s);
 tf_status launch_hadamard_piece(const tf_filter_s *h, const double *x, const double *dc, double *t, int piece,
                                 cudaStream_t s);

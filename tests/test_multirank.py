@@ -84,3 +84,51 @@ def test_reference_arm_rank_gating(tmp_path):
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _halo_worker(rank, world, port, q):
+    """NEXT-4 transport: each rank sends the owned values its neighbours' halos need and
+    receives its own halo through DistTransport (batch_isend_irecv) over gloo."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2012_08208_b200 import sharded
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c = synth.random_points(906, 3000, 3, 0.0, 12.0)
+    xg = synth.uniform(907, 0, c.shape[0], 0.0, 1.0)
+    plan = sharded.make_plans(c, world, 1.4)[rank]
+    x_owned = torch.from_numpy(xg[plan.owned])
+    # the GPU path packs with tf_halo_pack; here the same gather on CPU tensors
+    sends = {j: [x_owned[torch.from_numpy(idx.astype(np.int64))].contiguous()] for j, idx in plan.send_to.items()}
+    x_loc = torch.zeros(plan.n_owned + plan.n_halo, dtype=torch.float64)
+    x_loc[:plan.n_owned] = x_owned
+    recvs = {}
+    for j, g in plan.halo_from.items():
+        o = plan.halo_offset(j)
+        recvs[j] = [x_loc[o:o + g.shape[0]]]
+    sharded.DistTransport().exchange(sends, recvs)
+    ok = bool(np.array_equal(x_loc.numpy(), xg[plan.local_ids()]))
+    q.put((rank, ok, plan.n_halo, sorted(plan.halo_from)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_exchange_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, ok, nh, srcs in res:
+        assert ok and nh > 0 and rank not in srcs
