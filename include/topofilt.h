@@ -22,7 +22,8 @@
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *     Work is stream-ordered; apply calls are asynchronous (no host sync).
  *   - A handle is bound to the CUDA device that was current when it was built; calls on it
- *     must be made with that device current (TF_ERR_INVALID otherwise).
+ *     must be made with that device current (TF_ERR_INVALID otherwise); tf_free works from any
+ *     device.
  *   - Every call returns tf_status; nothing throws or aborts across the ABI.
  *     On a non-OK status tf_last_error() returns a thread-local message.
  *   - Sizes: 1 <= n < 2^31 - 1 (int32 column indices); nnz < 2^63.

@@ -139,6 +139,7 @@ static bool overlaps(const void *a, const void *b, size_t bytes) {
 
 static void destroy(tf_filter_s *h) {
     if (!h) return;
+    DeviceScope on(h->device);  // free on the handle's device, whichever is current
     cudaDeviceSynchronize();
     // stream-ordered allocations go back to the pool; the device is idle after the sync
     if (h->rowptr) cudaFreeAsync(h->rowptr, 0);

@@ -520,6 +520,7 @@ int hz_grid(const DeviceInfo &di, int64_t nn) {
 
 void hz_destroy(tf_helmholtz_s *h) {
     if (!h) return;
+    DeviceScope on(h->device);  // free on the handle's device, whichever is current
     cudaDeviceSynchronize();
     void *ps[] = {h->cells, h->vol, h->inc_ptr, h->inc_cell, h->W, h->rowptr, h->cols,
                   h->valA, h->valM, h->dinv, h->vec, h->parts};

@@ -89,6 +89,20 @@ struct PhaseTrace {
 };
 PhaseTrace &build_trace();
 
+// Makes `device` current for the scope (handle teardown on the handle's own device).
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int device) {
+        cudaGetDevice(&prev);
+        if (device >= 0 && device != prev) cudaSetDevice(device);
+    }
+    ~DeviceScope() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
 // ------------------------------------------------------------------ memory
 // Stream-ordered device allocation with the test-only allocation limit.
 tf_status dev_alloc(void **p, size_t bytes, cudaStream_t s, const char *what);
