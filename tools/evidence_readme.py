@@ -143,6 +143,17 @@ def main(rnd):
             f"config-{r['helmholtz_config']} mesh ({r['cells']:,} cells, {r['nodes']:,} nodes): build {r['build_ms']:.1f} ms, "
             f"solve {r['solve_us_cold']:.0f} µs cold, {r['iterations']} CG iterations "
             f"({100 * r['iteration_frac_8tbs']:.0f}% of 8 TB/s on 12 B/nnz + 112 B/node per iteration)" for r in hz) + ".\n")
+    bo = [r for r in rows if "both_config" in r]
+    if bo:
+        w("Both filters in one pass over H (`tf_filter_both`, bitwise the separate calls), cold: " + "; ".join(
+            f"config {r['both_config']}: {r['both_us_cold']:.0f} µs vs {r['separate_us_cold']:.0f} µs separate "
+            f"({r['speedup']:.2f}×, {100 * r['both_frac_8tbs']:.0f}% of 8 TB/s on its own bytes)" for r in bo) + ".\n")
+    la = [r for r in rows if "lattice_config" in r]
+    if la:
+        w("Matrix-free periodic lattice (`tf_build_lattice`), cold: " + "; ".join(
+            f"config {r['lattice_config']} ({r['types']} cells per cube): sensitivity {r['sens_us_cold']:.0f} µs, "
+            f"density {r['dens_us_cold']:.0f} µs vs stored CSR {r['csr_sens_us_cold']:.0f} / {r['csr_dens_us_cold']:.0f} µs "
+            f"({r['sens_speedup']:.1f}× / {r['dens_speedup']:.1f}×)" for r in la) + ".\n")
     hrep = os.path.join(EV, "ev_hz.ncu-rep")
     if os.path.exists(hrep):
         ncu(["-i", hrep, "--page", "raw", "--csv"], "/tmp/ev_hz_raw.csv")
