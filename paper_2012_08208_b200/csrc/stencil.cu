@@ -210,6 +210,9 @@ tf_status build_lattice(int dim, int64_t nx, int64_t ny, int64_t nz, double h, i
     std::vector<double> w;
     StencilGeom &sg = f->stencil;
     sg.T = ntypes;
+    // one type per cube is a regular grid: k_stencil is faster there (config 3: 34.8 vs 41.0 us,
+    // bitwise the same result; tools/stencil_vs_lattice.py) and reads the same offset table
+    sg.lattice = ntypes > 1;
     const int zr = (dim == 3) ? Rs : 0;
     for (int st = 0; st < ntypes; ++st) {
         sg.kstart[st] = (int)off.size();
@@ -392,7 +395,7 @@ static tf_status launch_lattice(const tf_filter_s *f, const double *x, const dou
 tf_status launch_stencil(const tf_filter_s *f, const double *x, const double *dc, double *out, bool sens,
                          cudaStream_t s) {
     const StencilGeom &sg = f->stencil;
-    if (sg.T > 1) return launch_lattice(f, x, dc, out, sens, s);
+    if (sg.lattice) return launch_lattice(f, x, dc, out, sens, s);
     const int TY = sg.ty, TZ = (sg.dim == 3) ? sg.tz : 1, R = sg.R;
     const size_t smem = 2 * sizeof(double) * (size_t)(kTX + 2 * R) * (TY + 2 * R) * ((sg.dim == 3) ? TZ + 2 * R : 1) +
                         sizeof(int) * ((sg.K + 1) & ~1) + sizeof(double) * sg.K;

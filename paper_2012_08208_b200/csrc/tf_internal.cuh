@@ -197,6 +197,7 @@ struct StencilGeom {
     // periodic lattices (T > 1 types per cube, cell = T*cube + type): offsets of type s are
     // [kstart[s], kstart[s+1]) as (dx, dy, dz, target type); hs_full_t = interior row sums
     int T = 1;
+    bool lattice = false;  // built by tf_build_lattice (k_lattice), else k_stencil
     int kstart[kMaxTypes + 1] = {};
     double hs_full_t[kMaxTypes] = {};
 };
