@@ -524,8 +524,8 @@ constexpr int kListCap = 128;  // per-warp compacted candidate list (phase A -> 
 template <int DIM, bool FULL>
 __device__ __forceinline__ void fill_flush(const SortedPts &P, const uint32_t *skey, const uint32_t *sp,
                                            const int32_t *list, int nl, int lo, double qx, double qy, double qz,
-                                           double r2, double rmin, int64_t base, int &wpos, double &hsum,
-                                           int32_t *__restrict__ cols, double *__restrict__ vals) {
+                                           double r2, double rmin, int &wpos, double &hsum,
+                                           int32_t *__restrict__ colsq, double *__restrict__ valsq) {
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     for (int e0 = 0; e0 < nl; e0 += 32) {
@@ -538,10 +538,10 @@ __device__ __forceinline__ void fill_flush(const SortedPts &P, const uint32_t *s
         const uint32_t bal = __ballot_sync(0xffffffffu, ok);
         const double w = weight_of(rmin, d2);
         if (ok) {
-            const int64_t k = base + wpos + __popc(bal & lt);
+            const int k = wpos + __popc(bal & lt);  // row-relative: the row's base is hoisted
             TF_DCHECK(t >= 0 && p >= 0);
-            cols[k] = (int32_t)skey[t] + lo;
-            vals[k] = w;
+            colsq[k] = (int32_t)skey[t] + lo;
+            valsq[k] = w;
             hsum += w;
         }
         wpos += __popc(bal);
@@ -635,6 +635,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
             const f2u qx2 = f2_pack(fq.x, fq.x), qy2 = f2_pack(fq.y, fq.y), qz2 = f2_pack(fq.z, fq.z);
             const int32_t qid = P.id[q];
             const int64_t base = rowptr[qid];
+            int32_t *colsq = cols + base;
+            double *valsq = vals + base;
             int wpos = 0, nl = 0;
             double hsum = 0.0;
             for (int k0 = 0; k0 < CP / 2; k0 += 32) {  // warp-uniform trip count
@@ -652,8 +654,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
                     // flush whole 32-entry chunks only; the < 32 tail moves to the front
                     const int full = nl & ~31;
                     __syncwarp();
-                    fill_flush<DIM, true>(P, skey, sp, list, full, lo, qx, qy, qz, r2, rmin, base, wpos, hsum, cols,
-                                          vals);
+                    fill_flush<DIM, true>(P, skey, sp, list, full, lo, qx, qy, qz, r2, rmin, wpos, hsum, colsq,
+                                          valsq);
                     const int tail = nl - full;
                     const int moved = (lane < tail) ? list[full + lane] : 0;
                     __syncwarp();
@@ -663,7 +665,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const 
                 }
             }
             __syncwarp();
-            fill_flush<DIM, false>(P, skey, sp, list, nl, lo, qx, qy, qz, r2, rmin, base, wpos, hsum, cols, vals);
+            fill_flush<DIM, false>(P, skey, sp, list, nl, lo, qx, qy, qz, r2, rmin, wpos, hsum, colsq, valsq);
             __syncwarp();
             for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
             if (lane == 0) {
