@@ -178,11 +178,15 @@ struct ApplyPlan {
     // row-range chunks of the host pipeline: windows [chunk_w[i], chunk_w[i+1]) cover rows
     // [chunk_r[i], chunk_r[i+1])
     int nchunks = -1;  // -1: not computed yet
-    int64_t chunk_w[9] = {};
-    int32_t chunk_r[9] = {};
-    int32_t chunk_maxcol[8] = {};  // largest column read by chunk i (-1: none)
+    int64_t chunk_w[17] = {};
+    int32_t chunk_r[17] = {};
+    int32_t chunk_maxcol[16] = {};  // largest column read by chunk i (-1: none)
 };
-constexpr int kMaxChunks = 8;
+#ifndef TF_HOST_CHUNKS
+#define TF_HOST_CHUNKS 8
+#endif
+constexpr int kMaxChunks = TF_HOST_CHUNKS;  // <= 16 (array sizes above)
+static_assert(kMaxChunks >= 1 && kMaxChunks <= 16, "host pipeline chunks");
 
 // ------------------------------------------------------------------ matrix-free stencil (a10)
 constexpr int kMaxTypes = 8;  // cells per lattice cube (tf_build_lattice)
