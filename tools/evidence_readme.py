@@ -168,6 +168,17 @@ def main(rnd):
         w(f"Helmholtz apply kernel under ncu (`k_hz_apply_ncu_summary.txt`): {hb['gpu__time_duration.sum']:.3f} ms, "
           f"DRAM {hb['dram__bytes_read.sum']:.2f} GB read + {hb['dram__bytes_write.sum']:.2f} GB written, "
           f"{hb.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 0):.0f}% of DRAM peak.\n")
+    mrep = os.path.join(EV, "ev_mf.ncu-rep")
+    if os.path.exists(mrep):
+        ncu(["-i", mrep, "--page", "raw", "--csv"], "/tmp/ev_mf_raw.csv")
+        with open(os.path.join(dst, "matrix_free_ncu_summary.txt"), "w") as f:
+            subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), "/tmp/ev_mf_raw.csv"],
+                           stdout=f, check=True)
+        mb = summary_blocks(os.path.join(dst, "matrix_free_ncu_summary.txt"))
+        w("Matrix-free kernels under ncu (`matrix_free_ncu_summary.txt`, one sensitivity apply each): " + "; ".join(
+            f"{b['name'].split('(')[0].split('::')[-1]}: {b['gpu__time_duration.sum']:.1f} "
+            f"{'us' if b['gpu__time_duration.sum'] > 5 else 'ms'}, DRAM {b['dram__bytes_read.sum']:.1f} MB/GB read"
+            for b in mb) + " (vs the stored-CSR k_spmv sensitivity above).\n")
     probe = os.path.join(EV, "ev_helm_probe.log")
     if os.path.exists(probe):
         shutil.copy(probe, os.path.join(dst, "helm_probe.log"))
