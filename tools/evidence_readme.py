@@ -32,6 +32,7 @@ def summary_blocks(path):
             if len(parts) >= 2:
                 try:
                     cur[parts[0]] = float(parts[1])
+                    cur[parts[0] + "_unit"] = parts[2] if len(parts) > 2 else ""
                 except ValueError:
                     pass
     return blocks
@@ -177,8 +178,8 @@ def main(rnd):
         mb = summary_blocks(os.path.join(dst, "matrix_free_ncu_summary.txt"))
         w("Matrix-free kernels under ncu (`matrix_free_ncu_summary.txt`, one sensitivity apply each): " + "; ".join(
             f"{b['name'].split('(')[0].split('::')[-1]}: {b['gpu__time_duration.sum']:.1f} "
-            f"{'us' if b['gpu__time_duration.sum'] > 5 else 'ms'}, DRAM {b['dram__bytes_read.sum']:.1f} MB/GB read"
-            for b in mb) + " (vs the stored-CSR k_spmv sensitivity above).\n")
+            f"{b['gpu__time_duration.sum_unit']}, DRAM {b['dram__bytes_read.sum']:.1f} "
+            f"{b['dram__bytes_read.sum_unit']} read" for b in mb) + " (vs the stored-CSR k_spmv sensitivity above).\n")
     probe = os.path.join(EV, "ev_helm_probe.log")
     if os.path.exists(probe):
         shutil.copy(probe, os.path.join(dst, "helm_probe.log"))
