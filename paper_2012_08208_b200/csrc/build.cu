@@ -553,7 +553,12 @@ __device__ __forceinline__ void fill_flush(const SortedPts &P, const uint32_t *s
 // warp list of candidates that may lie inside rmin; phase B: exact fp64 test on the original
 // centroid bytes, weight, CSR write, Hs.
 template <int DIM, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_fill(SortedPts P, Grid g, const int64_t *__restrict__ rowptr,
+#ifdef TF_FILL_MINB
+#define TF_FILL_BOUNDS __launch_bounds__(WARPS * 32, TF_FILL_MINB)
+#else
+#define TF_FILL_BOUNDS __launch_bounds__(WARPS * 32)
+#endif
+__global__ void TF_FILL_BOUNDS k_fill(SortedPts P, Grid g, const int64_t *__restrict__ rowptr,
                                                      int32_t *__restrict__ cols, double *__restrict__ vals,
                                                      double *__restrict__ hs, int cap,
                                                      int32_t *__restrict__ large_rows,
@@ -854,6 +859,9 @@ tf_status launch_fill(const SortedPts &P, const Grid &g, tf_filter_s *h, int cap
                       int32_t *stats, cudaStream_t s) {
     const size_t smem = (size_t)cap * FillSmem::bytes_per();
     TF_CUDA_TRY(cudaFuncSetAttribute(k_fill<DIM, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+#ifdef TF_FILL_CARVEOUT
+    TF_CUDA_TRY(cudaFuncSetAttribute(k_fill<DIM, WARPS>, cudaFuncAttributePreferredSharedMemoryCarveout, TF_FILL_CARVEOUT));
+#endif
     k_fill<DIM, WARPS><<<(unsigned)g.nbins, WARPS * 32, smem, s>>>(P, g, h->rowptr, h->cols, h->vals, h->hs,
                                                                    cap, large_rows, stats);
     TF_LAUNCH_CHECK();
