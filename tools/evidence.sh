@@ -17,4 +17,4 @@ timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_
 timeout 300 python tools/helm_probe.py > gpurun_out/ev_helm_probe.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hz_apply -c 1 -o gpurun_out/ev_hz python tools/helm_probe.py ncu > gpurun_out/ev_ncu_hz.log 2>&1; echo ncu_hz=$?
 timeout 300 python tools/matrix_free_probe.py > gpurun_out/ev_mf_probe.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_stencil|k_lattice<" -c 2 -o gpurun_out/ev_mf python tools/matrix_free_probe.py > gpurun_out/ev_ncu_mf.log 2>&1; echo ncu_mf=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^(k_stencil|k_lattice)$" -c 2 -o gpurun_out/ev_mf python tools/matrix_free_probe.py > gpurun_out/ev_ncu_mf.log 2>&1; echo ncu_mf=$?
