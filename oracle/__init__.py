@@ -45,6 +45,10 @@ def lib():
         L.or_bf_rowptr.restype = I64
         L.or_bf_fill.argtypes = [P, I64, ctypes.c_int, ctypes.c_double, P, P, P, P]
         L.or_bf_fill.restype = None
+        L.or_bf_rows_rowptr.argtypes = [P, I64, ctypes.c_int, ctypes.c_double, P, I64, P]
+        L.or_bf_rows_rowptr.restype = I64
+        L.or_bf_rows_fill.argtypes = [P, I64, ctypes.c_int, ctypes.c_double, P, I64, P, P, P, P]
+        L.or_bf_rows_fill.restype = None
         L.or_cl_create.argtypes = [P, I64, ctypes.c_int, ctypes.c_double, ctypes.c_double]
         L.or_cl_create.restype = P
         L.or_cl_free.argtypes = [P]
@@ -114,6 +118,21 @@ def build_bruteforce(c: np.ndarray, rmin: float) -> CSR:
     hs = np.empty(n, dtype=np.float64)
     lib().or_bf_fill(_p(c), n, dim, float(rmin), _p(rowptr), _p(cols), _p(vals), _p(hs))
     return CSR(rowptr, cols, vals, hs)
+
+
+def build_bruteforce_rows(c: np.ndarray, rmin: float, rows: np.ndarray) -> CSR:
+    """O1 on the listed rows only, each tested against all N points."""
+    c = _c64(c)
+    n, dim = c.shape
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    m = rows.shape[0]
+    rowptr = np.empty(m + 1, dtype=np.int64)
+    nnz = lib().or_bf_rows_rowptr(_p(c), n, dim, float(rmin), _p(rows), m, _p(rowptr))
+    cols = np.empty(nnz, dtype=np.int32)
+    vals = np.empty(nnz, dtype=np.float64)
+    hs = np.empty(m, dtype=np.float64)
+    lib().or_bf_rows_fill(_p(c), n, dim, float(rmin), _p(rows), m, _p(rowptr), _p(cols), _p(vals), _p(hs))
+    return CSR(rowptr, cols, vals, hs, rows)
 
 
 class CellList:

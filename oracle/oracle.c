@@ -98,6 +98,44 @@ void or_bf_fill(const double *c, int64_t n, int dim, double rmin, const int64_t 
     }
 }
 
+/* O1 on a subset of rows ("random rows of configs 3/4/5 over all N"): output row r
+ * is global row rows[r], tested against all n points in ascending j -- the same loop as
+ * or_bf_rowptr / or_bf_fill restricted to the listed rows. */
+int64_t or_bf_rows_rowptr(const double *c, int64_t n, int dim, double rmin, const int64_t *rows, int64_t m,
+                          int64_t *rowptr)
+{
+    double r2 = rmin * rmin;
+    rowptr[0] = 0;
+    for (int64_t r = 0; r < m; ++r) {
+        int64_t i = rows[r], cnt = 0;
+        for (int64_t j = 0; j < n; ++j)
+            if (pair_d2(c, dim, i, j) < r2) ++cnt;
+        rowptr[r + 1] = rowptr[r] + cnt;
+    }
+    return rowptr[m];
+}
+
+void or_bf_rows_fill(const double *c, int64_t n, int dim, double rmin, const int64_t *rows, int64_t m,
+                     const int64_t *rowptr, int32_t *cols, double *vals, double *hs)
+{
+    double r2 = rmin * rmin;
+    for (int64_t r = 0; r < m; ++r) {
+        int64_t i = rows[r], k = rowptr[r];
+        double sum = 0.0;
+        for (int64_t j = 0; j < n; ++j) {
+            double d2 = pair_d2(c, dim, i, j);
+            if (d2 < r2) {
+                double w = weight(rmin, d2);
+                cols[k] = (int32_t)j;
+                vals[k] = w;
+                sum = sum + w;
+                ++k;
+            }
+        }
+        hs[r] = sum;
+    }
+}
+
 /* ------------------------------------------------------------------ O2 cell list */
 
 typedef struct {

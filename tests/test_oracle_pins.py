@@ -281,3 +281,20 @@ def test_sampled_rows_match_full():
     for k, r in enumerate(rows):
         np.testing.assert_array_equal(full.cols[full.rowptr[r]:full.rowptr[r + 1]],
                                       sub.cols[sub.rowptr[k]:sub.rowptr[k + 1]])
+
+
+@pytest.mark.parametrize("cfg,count", [(3, 60), (4, 60), (5, 40)])
+def test_bruteforce_rows_large_configs(cfg, count):
+    """seeded rows of configs 3-5, each tested by brute force against ALL N
+    points, equal the cell list's rows bit for bit (structure, weights, Hs)."""
+    c = synth.centroids(cfg)
+    rmin = synth.CONFIGS[cfg]["rmin"]
+    rows = np.sort(synth.sample_rows(cfg, c.shape[0], count))
+    bf = oracle.build_bruteforce_rows(c, rmin, rows)
+    cl = oracle.CellList(c, rmin)
+    ref = cl.rows(rows)
+    cl.close()
+    np.testing.assert_array_equal(bf.rowptr, ref.rowptr)
+    np.testing.assert_array_equal(bf.cols, ref.cols)
+    np.testing.assert_array_equal(bf.vals, ref.vals)
+    np.testing.assert_array_equal(bf.hs, ref.hs)
