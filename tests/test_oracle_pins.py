@@ -283,7 +283,7 @@ def test_sampled_rows_match_full():
                                       sub.cols[sub.rowptr[k]:sub.rowptr[k + 1]])
 
 
-@pytest.mark.parametrize("cfg,count", [(3, 60), (4, 60), (5, 40)])
+@pytest.mark.parametrize("cfg,count", [(3, 1000), (4, 1000), (5, 400)])  # c5: 400 x 12M tests ~ 45 s
 def test_bruteforce_rows_large_configs(cfg, count):
     """seeded rows of configs 3-5, each tested by brute force against ALL N
     points, equal the cell list's rows bit for bit (structure, weights, Hs)."""
