@@ -12,8 +12,10 @@
 // sensitivity filter, 16 N for density) instead of 12 nnz + ... for the CSR.
 //
 // Kernel: one block per (32 x TY x TZ) tile; the block stages t = x*dc (or x) of the tile
-// plus its halo of radius R in shared memory with coalesced loads, then each thread sums its
-// cell's K offsets from shared memory (offset table: handle-owned device memory, broadcast reads).
+// plus its halo of radius R in shared memory with coalesced loads (0 outside the grid), then
+// each thread sums its cell's K offsets from shared memory (offset table: handle-owned device
+// memory, broadcast reads). Row sums: the full offset-order sum for cells whose neighbours are
+// all in the grid, the truncated sum built once per handle (k_lattice_hs) near the boundary.
 #include <math.h>
 
 #include <algorithm>
@@ -32,19 +34,18 @@ constexpr int kTX = 32;
 // RC = compile-time halo radius (1..4) or 0 for a runtime radius (general fallback)
 template <bool SENS, int DIM, int RC>
 __global__ void __launch_bounds__(256) k_stencil(StencilGeom sg, const int4 *__restrict__ offs,
-                                                 const double *__restrict__ wts, const double *__restrict__ x,
-                                                 const double *__restrict__ dc, double *__restrict__ out) {
+                                                 const double *__restrict__ wts, const double *__restrict__ hs_cell,
+                                                 const double *__restrict__ x, const double *__restrict__ dc,
+                                                 double *__restrict__ out) {
     extern __shared__ double tile[];
     constexpr int TY = (DIM == 3) ? 4 : 8, TZ = (DIM == 3) ? 2 : 1;
     const int R = RC ? RC : sg.R;
     const int HX = kTX + 2 * R, HY = TY + 2 * R, HZ = (DIM == 3) ? TZ + 2 * R : 1;
     const int bx0 = blockIdx.x * kTX, by0 = blockIdx.y * TY, bz0 = (DIM == 3) ? blockIdx.z * TZ : 0;
     const int nx = (int)sg.nx, ny = (int)sg.ny, nz = (int)sg.nz;
-    // stage t over the haloed tile, one x-row per warp iteration (coalesced; no divisions), and
-    // a 0/1 in-grid mask: out-of-grid neighbours then contribute fma(w, 0, .) = exactly nothing,
-    // so every cell runs the same branch-free loop and the truncated Hs is bitwise the checked sum
+    // stage t over the haloed tile, one x-row per warp iteration (coalesced; no divisions);
+    // out-of-grid neighbours stage 0 and add fma(w, 0, acc) = acc exactly
     const int rows = HY * HZ;
-    double *mask = tile + rows * HX;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int row = warp; row < rows; row += 8) {
         const int hy = row % HY, hz = row / HY;
@@ -53,18 +54,16 @@ __global__ void __launch_bounds__(256) k_stencil(StencilGeom sg, const int4 *__r
         const int64_t rbase = ((int64_t)gz * ny + gy) * nx;
         for (int hx = lane; hx < HX; hx += 32) {
             const int gx = bx0 + hx - R;
-            double t = 0.0, m = 0.0;
+            double t = 0.0;
             if (rok && gx >= 0 && gx < nx) {
                 const int64_t g = rbase + gx;
                 t = SENS ? __ldg(x + g) * __ldg(dc + g) : __ldg(x + g);
-                m = 1.0;
             }
             tile[row * HX + hx] = t;
-            mask[row * HX + hx] = m;
         }
     }
     // offset table -> shared memory as tile-index deltas
-    int *s_delta = reinterpret_cast<int *>(mask + rows * HX);
+    int *s_delta = reinterpret_cast<int *>(tile + rows * HX);
     double *s_w = reinterpret_cast<double *>(s_delta + ((sg.K + 1) & ~1));
     for (int o = threadIdx.x; o < sg.K; o += 256) {
         const int4 off = __ldg(offs + o);
@@ -77,15 +76,14 @@ __global__ void __launch_bounds__(256) k_stencil(StencilGeom sg, const int4 *__r
     const int gx = bx0 + lx, gy = by0 + ly, gz = bz0 + lz;
     if (gx >= nx || gy >= ny || gz >= nz) return;
     const int center = (((DIM == 3) ? lz + R : 0) * HY + (ly + R)) * HX + (lx + R);
-    double acc = 0.0, hs = 0.0;
+    double acc = 0.0;
 #pragma unroll 9
-    for (int o = 0; o < sg.K; ++o) {
-        const double w = s_w[o];
-        const int si = center + s_delta[o];
-        acc = fma(w, tile[si], acc);
-        hs = fma(w, mask[si], hs);  // w*1 = w and w*0 = 0 exactly: the offset-order in-grid sum
-    }
+    for (int o = 0; o < sg.K; ++o) acc = fma(s_w[o], tile[center + s_delta[o]], acc);
     const int64_t g = ((int64_t)gz * ny + gy) * nx + gx;
+    // row sum: the full offset-order sum for cells with every neighbour in the grid, else the
+    // truncated offset-order sum built once per handle (k_lattice_hs) -- bitwise the same
+    const bool inner = gx >= R && gx + R < nx && gy >= R && gy + R < ny && (DIM == 2 || (gz >= R && gz + R < nz));
+    const double hs = inner ? sg.hs_full : __ldg(hs_cell + g);
     out[g] = SENS ? acc / (hs * fmax(1e-3, __ldg(x + g))) : acc / hs;
 }
 
@@ -270,7 +268,7 @@ tf_status build_lattice(int dim, int64_t nx, int64_t ny, int64_t nz, double h, i
     sg.ty = TY;
     sg.tz = TZ;
     sg.h = h;
-    sg.hs_full = 0.0;
+    sg.hs_full = sg.hs_full_t[0];  // used by k_stencil when one type per cube routes there
     TF_TRY(dev_alloc(&f->lattice_table, sizeof(LatEntry) * tab.size(), s, "lattice offset table"));
     TF_CUDA_TRY(cudaMemcpyAsync(f->lattice_table, tab.data(), sizeof(LatEntry) * tab.size(), cudaMemcpyHostToDevice,
                                 s));
@@ -339,13 +337,28 @@ tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, d
     sg.tz = (dim == 3) ? 2 : 1;
     sg.h = h;
     double hs_full = 0.0;
-    for (double ww : w) hs_full += ww;  // full-stencil row sum (diagnostic)
+    for (double ww : w) hs_full += ww;  // full-stencil row sum in offset order (interior cells)
     sg.hs_full = hs_full;
+    sg.T = 1;
+    sg.kstart[0] = 0;
+    sg.kstart[1] = (int)off.size();
+    sg.hs_full_t[0] = hs_full;
     // handle-owned device copy of the offset table (read-only; concurrent applies are safe)
     TF_TRY(dalloc(&f->stencil_off, off.size(), s, "stencil offsets"));
     TF_TRY(dalloc(&f->stencil_w, w.size(), s, "stencil weights"));
     TF_CUDA_TRY(cudaMemcpyAsync(f->stencil_off, off.data(), sizeof(int4) * off.size(), cudaMemcpyHostToDevice, s));
     TF_CUDA_TRY(cudaMemcpyAsync(f->stencil_w, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice, s));
+    // truncated row sums of the boundary cells (offset order), once per handle
+    const int64_t ncell = nx * ny * sg.nz;
+    TF_TRY(dalloc(&f->hs, (size_t)ncell, s, "stencil row sums"));
+    {
+        DeviceInfo di;
+        TF_TRY(device_info(&di));
+        const unsigned blocks = (unsigned)std::min<int64_t>((ncell + 255) / 256, (int64_t)di.sms * 16);
+        if (dim == 3) k_lattice_hs<3><<<blocks, 256, 0, s>>>(sg, f->stencil_off, f->stencil_w, f->hs);
+        else k_lattice_hs<2><<<blocks, 256, 0, s>>>(sg, f->stencil_off, f->stencil_w, f->hs);
+        TF_LAUNCH_CHECK();
+    }
     TF_CUDA_TRY(cudaStreamSynchronize(s));
     // nnz of the equivalent CSR: every offset times the cells whose neighbour is in the grid
     int64_t nnz = 0;
@@ -397,13 +410,13 @@ tf_status launch_stencil(const tf_filter_s *f, const double *x, const double *dc
     const StencilGeom &sg = f->stencil;
     if (sg.lattice) return launch_lattice(f, x, dc, out, sens, s);
     const int TY = sg.ty, TZ = (sg.dim == 3) ? sg.tz : 1, R = sg.R;
-    const size_t smem = 2 * sizeof(double) * (size_t)(kTX + 2 * R) * (TY + 2 * R) * ((sg.dim == 3) ? TZ + 2 * R : 1) +
+    const size_t smem = sizeof(double) * (size_t)(kTX + 2 * R) * (TY + 2 * R) * ((sg.dim == 3) ? TZ + 2 * R : 1) +
                         sizeof(int) * ((sg.K + 1) & ~1) + sizeof(double) * sg.K;
     dim3 grid((unsigned)((sg.nx + kTX - 1) / kTX), (unsigned)((sg.ny + TY - 1) / TY),
               (unsigned)((sg.dim == 3) ? (sg.nz + TZ - 1) / TZ : 1));
     auto go = [&](auto kern) -> tf_status {
         TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<grid, 256, smem, s>>>(sg, f->stencil_off, f->stencil_w, x, dc, out);
+        kern<<<grid, 256, smem, s>>>(sg, f->stencil_off, f->stencil_w, f->hs, x, dc, out);
         TF_LAUNCH_CHECK();
         return TF_OK;
     };
