@@ -323,7 +323,7 @@ tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, d
     }
     int Rk = 0;
     for (const int4 &o : off) Rk = std::max(Rk, std::max(abs(o.x), std::max(abs(o.y), abs(o.z))));
-    const size_t halo = 2 * sizeof(double) * (size_t)(32 + 2 * Rk) * ((dim == 3 ? 4 : 8) + 2 * Rk) * (dim == 3 ? 2 + 2 * Rk : 1);
+    const size_t halo = sizeof(double) * (size_t)(32 + 2 * Rk) * ((dim == 3 ? 4 : 8) + 2 * Rk) * (dim == 3 ? 2 + 2 * Rk : 1);
     if (halo + 12 * off.size() > 200 * 1024) {
         set_error("stencil halo tile too large for shared memory (rmin/h too big); use tf_build_filter");
         return TF_ERR_INVALID;
