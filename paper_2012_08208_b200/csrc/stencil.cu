@@ -100,6 +100,13 @@ __global__ void __launch_bounds__(256) k_stencil(StencilGeom sg, const int4 *__r
 // mask, weight), precomputed at build for the tile shape: every lane of a warp reads the same
 // entry, so each offset costs one broadcast shared-memory wavefront besides the tile read.
 constexpr int kLatMaxOffs = 4096;
+#ifndef TF_LAT_TZ
+#define TF_LAT_TZ 4   // lattice tile depth (cubes) in 3D (swept: 2/4/8 x rows 2/4/8 -> 4, 4)
+#endif
+#ifndef TF_LAT_RPI
+#define TF_LAT_RPI 4  // rows per warp item (one table read serves this many tile reads)
+#endif
+constexpr int kLatTZ = TF_LAT_TZ, kLatRPI = TF_LAT_RPI;
 struct __align__(16) LatEntry {
     int delta, mdelta;
     double w;
@@ -110,7 +117,7 @@ __global__ void __launch_bounds__(256) k_lattice(StencilGeom sg, const LatEntry 
                                                  const double *__restrict__ hs_cell, const double *__restrict__ x,
                                                  const double *__restrict__ dc, double *__restrict__ out) {
     extern __shared__ double tile[];
-    constexpr int TY = (DIM == 3) ? 4 : 8, TZ = (DIM == 3) ? 2 : 1;
+    constexpr int TY = (DIM == 3) ? 4 : 8, TZ = (DIM == 3) ? kLatTZ : 1;
     const int T = TT ? TT : sg.T;
     const int R = RC ? RC : sg.R;
     const int HX = kTX + 2 * R, HY = TY + 2 * R, HZ = (DIM == 3) ? TZ + 2 * R : 1;
@@ -140,34 +147,38 @@ __global__ void __launch_bounds__(256) k_lattice(StencilGeom sg, const LatEntry 
     LatEntry *s_tab = reinterpret_cast<LatEntry *>(tile + (((size_t)T * plane + 1) & ~(size_t)1));
     for (int o = threadIdx.x; o < sg.K; o += 256) s_tab[o] = tab[o];
     __syncthreads();
-    // items: (pair of rows, type); one table read serves the two rows' tile reads
-    constexpr int NP = TY * TZ / 2;
+    // items: (kLatRPI rows, type); one table read serves the rows' tile reads
+    constexpr int RPI = kLatRPI;
+    constexpr int NP = TY * TZ / RPI;
     for (int item = warp; item < NP * T; item += 8) {
         const int s = item % T, p = item / T;
-        const int ri0 = 2 * p, ri1 = 2 * p + 1;
-        const int ly0 = ri0 % TY, lz0 = ri0 / TY, ly1 = ri1 % TY, lz1 = ri1 / TY;
-        const int c0 = (((DIM == 3) ? lz0 + R : 0) * HY + (ly0 + R)) * HX + (lane + R);
-        const int c1 = (((DIM == 3) ? lz1 + R : 0) * HY + (ly1 + R)) * HX + (lane + R);
+        int ly[RPI], lz[RPI], c[RPI];
+        double a[RPI];
+#pragma unroll
+        for (int q = 0; q < RPI; ++q) {
+            const int ri = RPI * p + q;
+            ly[q] = ri % TY, lz[q] = ri / TY;
+            c[q] = (((DIM == 3) ? lz[q] + R : 0) * HY + (ly[q] + R)) * HX + (lane + R);
+            a[q] = 0.0;
+        }
         const int o0 = sg.kstart[s], o1 = sg.kstart[s + 1];
-        double a0 = 0.0, a1 = 0.0;
 #pragma unroll 4
         for (int o = o0; o < o1; ++o) {
             const LatEntry e = s_tab[o];
-            a0 = fma(e.w, tile[c0 + e.delta], a0);
-            a1 = fma(e.w, tile[c1 + e.delta], a1);
+#pragma unroll
+            for (int q = 0; q < RPI; ++q) a[q] = fma(e.w, tile[c[q] + e.delta], a[q]);
         }
         const int gx = bx0 + lane;
-        auto finish = [&](double acc, int ly, int lz) {
-            const int gy = by0 + ly, gz = bz0 + lz;
-            if (gx >= nx || gy >= ny || gz >= nz) return;
+#pragma unroll
+        for (int q = 0; q < RPI; ++q) {
+            const int gy = by0 + ly[q], gz = bz0 + lz[q];
+            if (gx >= nx || gy >= ny || gz >= nz) continue;
             const int64_t g = (((int64_t)gz * ny + gy) * nx + gx) * T + s;
             // interior cells: the type's full row sum; near the boundary: the truncated sum built once
             const bool inner = gx >= R && gx + R < nx && gy >= R && gy + R < ny && (DIM == 2 || (gz >= R && gz + R < nz));
             const double hs = inner ? sg.hs_full_t[s] : __ldg(hs_cell + g);
-            out[g] = SENS ? acc / (hs * fmax(1e-3, __ldg(x + g))) : acc / hs;
-        };
-        finish(a0, ly0, lz0);
-        finish(a1, ly1, lz1);
+            out[g] = SENS ? a[q] / (hs * fmax(1e-3, __ldg(x + g))) : a[q] / hs;
+        }
     }
 }
 
@@ -246,7 +257,7 @@ tf_status build_lattice(int dim, int64_t nx, int64_t ny, int64_t nz, double h, i
     }
     int Rk = 0;
     for (const int4 &q : off) Rk = std::max(Rk, std::max(abs(q.x), std::max(abs(q.y), abs(q.z))));
-    const int TY = (dim == 3) ? 4 : 8, TZ = (dim == 3) ? 2 : 1;
+    const int TY = (dim == 3) ? 4 : 8, TZ = (dim == 3) ? kLatTZ : 1;
     const int HX = kTX + 2 * Rk, HY = TY + 2 * Rk;
     const size_t plane = (size_t)HX * HY * (dim == 3 ? TZ + 2 * Rk : 1);
     const size_t smem = sizeof(double) * (plane * ntypes + 1) + sizeof(LatEntry) * off.size();
