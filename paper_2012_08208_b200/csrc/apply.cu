@@ -35,6 +35,10 @@
 
 #include "tf_internal.cuh"
 
+#ifndef TF_APPLY_PREFETCH
+#define TF_APPLY_PREFETCH 0  // L2 prefetch distance in rounds (0: off)
+#endif
+
 namespace tf {
 namespace {
 
@@ -107,6 +111,10 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
             "r"(smem_addr(dst)),
         "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
         : "memory");
+}
+// L2 prefetch of a global range (no shared memory, no completion): raises the bytes in flight
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     uint32_t done = 0;
@@ -193,6 +201,18 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
             } else {
                 mbar_arrive(&full[st]);  // nothing staged: consumers read global memory
             }
+#if TF_APPLY_PREFETCH > 0
+            {  // L2 prefetch of this block's window TF_APPLY_PREFETCH rounds ahead
+                const int64_t wp = w + (int64_t)TF_APPLY_PREFETCH * gridDim.x;
+                if (wp < wend) {
+                    const int64_t pa = wlo[wp], pn = wlo[wp + 1 + nwin] - pa;
+                    if (pn > 0 && pn <= kStage) {
+                        bulk_prefetch_l2(vals + pa, (uint32_t)pn * 8u);
+                        bulk_prefetch_l2(cols + pa, (uint32_t)pn * 4u);
+                    }
+                }
+            }
+#endif
         };
         // prologue: the first kStages windows need no empty-wait (overlaps the t pass)
         if (lane == 0)
