@@ -112,10 +112,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
         : "memory");
 }
+#if TF_APPLY_PREFETCH > 0
 // L2 prefetch of a global range (no shared memory, no completion): raises the bytes in flight
 __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     uint32_t done = 0;
     while (!done) {
