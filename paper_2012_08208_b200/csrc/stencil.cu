@@ -38,7 +38,9 @@ __global__ void __launch_bounds__(256) k_stencil(StencilGeom sg, const int4 *__r
                                                  const double *__restrict__ x, const double *__restrict__ dc,
                                                  double *__restrict__ out) {
     extern __shared__ double tile[];
-    constexpr int TY = (DIM == 3) ? 4 : 8, TZ = (DIM == 3) ? 2 : 1;
+    // 32 x TY x TZ cells per block, two per thread (the second kStHalf rows further along the
+    // last axis), so each broadcast offset/weight read serves two tile reads
+    constexpr int TY = (DIM == 3) ? 4 : 16, TZ = (DIM == 3) ? 4 : 1;
     const int R = RC ? RC : sg.R;
     const int HX = kTX + 2 * R, HY = TY + 2 * R, HZ = (DIM == 3) ? TZ + 2 * R : 1;
     const int bx0 = blockIdx.x * kTX, by0 = blockIdx.y * TY, bz0 = (DIM == 3) ? blockIdx.z * TZ : 0;
@@ -71,20 +73,33 @@ __global__ void __launch_bounds__(256) k_stencil(StencilGeom sg, const int4 *__r
         s_w[o] = __ldg(wts + o);
     }
     __syncthreads();
-    // one cell per thread: (lx, ly, lz) = (threadIdx.x % 32, ...)
-    const int lx = threadIdx.x & 31, ly = (threadIdx.x >> 5) % TY, lz = (threadIdx.x >> 5) / TY;
-    const int gx = bx0 + lx, gy = by0 + ly, gz = bz0 + lz;
-    if (gx >= nx || gy >= ny || gz >= nz) return;
+    // two cells per thread: (lx, ly, lz) and the cell half a tile further along the last axis
+    const int lx = threadIdx.x & 31;
+    const int ly = (DIM == 3) ? (threadIdx.x >> 5) % TY : (threadIdx.x >> 5);
+    const int lz = (DIM == 3) ? (threadIdx.x >> 5) / TY : 0;
+    const int step = (DIM == 3) ? (TZ / 2) * HY * HX : (TY / 2) * HX;  // tile offset of the 2nd cell
     const int center = (((DIM == 3) ? lz + R : 0) * HY + (ly + R)) * HX + (lx + R);
-    double acc = 0.0;
+    double a0 = 0.0, a1 = 0.0;
 #pragma unroll 9
-    for (int o = 0; o < sg.K; ++o) acc = fma(s_w[o], tile[center + s_delta[o]], acc);
-    const int64_t g = ((int64_t)gz * ny + gy) * nx + gx;
-    // row sum: the full offset-order sum for cells with every neighbour in the grid, else the
-    // truncated offset-order sum built once per handle (k_lattice_hs) -- bitwise the same
-    const bool inner = gx >= R && gx + R < nx && gy >= R && gy + R < ny && (DIM == 2 || (gz >= R && gz + R < nz));
-    const double hs = inner ? sg.hs_full : __ldg(hs_cell + g);
-    out[g] = SENS ? acc / (hs * fmax(1e-3, __ldg(x + g))) : acc / hs;
+    for (int o = 0; o < sg.K; ++o) {
+        const double w = s_w[o];
+        const int si = center + s_delta[o];
+        a0 = fma(w, tile[si], a0);
+        a1 = fma(w, tile[si + step], a1);
+    }
+    const int gx = bx0 + lx;
+    for (int q = 0; q < 2; ++q) {
+        const int gy = by0 + ly + ((DIM == 2 && q) ? TY / 2 : 0);
+        const int gz = bz0 + lz + ((DIM == 3 && q) ? TZ / 2 : 0);
+        if (gx >= nx || gy >= ny || gz >= nz) continue;
+        const int64_t g = ((int64_t)gz * ny + gy) * nx + gx;
+        // row sum: the full offset-order sum for cells with every neighbour in the grid, else the
+        // truncated offset-order sum built once per handle (k_lattice_hs) -- bitwise the same
+        const bool inner = gx >= R && gx + R < nx && gy >= R && gy + R < ny && (DIM == 2 || (gz >= R && gz + R < nz));
+        const double hs = inner ? sg.hs_full : __ldg(hs_cell + g);
+        const double acc = q ? a1 : a0;
+        out[g] = SENS ? acc / (hs * fmax(1e-3, __ldg(x + g))) : acc / hs;
+    }
 }
 
 // ------------------------------------------------------------------ periodic lattices (T types)
@@ -276,8 +291,9 @@ tf_status build_lattice(int dim, int64_t nx, int64_t ny, int64_t nz, double h, i
     sg.nx = nx, sg.ny = ny, sg.nz = (dim == 3) ? nz : 1;
     sg.R = Rk;
     sg.K = (int)off.size();
-    sg.ty = TY;
-    sg.tz = TZ;
+    // tile shape of the kernel that runs: k_lattice, or k_stencil for one type per cube
+    sg.ty = sg.lattice ? TY : ((dim == 3) ? 4 : 16);
+    sg.tz = sg.lattice ? TZ : ((dim == 3) ? 4 : 1);
     sg.h = h;
     sg.hs_full = sg.hs_full_t[0];  // used by k_stencil when one type per cube routes there
     TF_TRY(dev_alloc(&f->lattice_table, sizeof(LatEntry) * tab.size(), s, "lattice offset table"));
@@ -334,7 +350,7 @@ tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, d
     }
     int Rk = 0;
     for (const int4 &o : off) Rk = std::max(Rk, std::max(abs(o.x), std::max(abs(o.y), abs(o.z))));
-    const size_t halo = sizeof(double) * (size_t)(32 + 2 * Rk) * ((dim == 3 ? 4 : 8) + 2 * Rk) * (dim == 3 ? 2 + 2 * Rk : 1);
+    const size_t halo = sizeof(double) * (size_t)(32 + 2 * Rk) * ((dim == 3 ? 4 : 16) + 2 * Rk) * (dim == 3 ? 4 + 2 * Rk : 1);
     if (halo + 12 * off.size() > 200 * 1024) {
         set_error("stencil halo tile too large for shared memory (rmin/h too big); use tf_build_filter");
         return TF_ERR_INVALID;
@@ -344,8 +360,8 @@ tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, d
     sg.nx = nx, sg.ny = ny, sg.nz = (dim == 3) ? nz : 1;
     sg.R = Rk;
     sg.K = (int)off.size();
-    sg.ty = (dim == 3) ? 4 : 8;  // must match the kernel's TY/TZ
-    sg.tz = (dim == 3) ? 2 : 1;
+    sg.ty = (dim == 3) ? 4 : 16;  // must match the kernel's TY/TZ
+    sg.tz = (dim == 3) ? 4 : 1;
     sg.h = h;
     double hs_full = 0.0;
     for (double ww : w) hs_full += ww;  // full-stencil row sum in offset order (interior cells)
