@@ -64,11 +64,18 @@ def dist_env():
 
 
 def init_dist(backend):
+    """Process group for N > 1 (None at N = 1). NCCL: the rank's GPU (LOCAL_RANK) is made current
+    and bound to the group first, so every collective (barriers included) runs on it."""
     import torch.distributed as dist
-    ws, rank, _ = dist_env()
+    ws, rank, local = dist_env()
     if ws > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group(backend=backend, rank=rank, world_size=ws)
+        kw = {}
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+            kw["device_id"] = torch.device("cuda", local)
+        dist.init_process_group(backend=backend, rank=rank, world_size=ws, **kw)
     return dist if ws > 1 else None
 
 
@@ -227,9 +234,9 @@ def oracle_sample(c, x, dc, rmin, applies, rows_per_step, steps, seed_cfg, threa
 
 def run_ours(args):
     import torch
-    dist = init_dist("nccl")
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
+    dist = init_dist("nccl")
     device = torch.device("cuda", local)
     import paper_2012_08208_b200 as tf
 
