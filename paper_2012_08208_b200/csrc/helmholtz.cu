@@ -23,7 +23,8 @@
 //   P2  s~_c = mean of u over the cell's nodes (/ max(1e-3, x_c) for the sensitivity use)
 // CSR rows and incidence lists use 2 lanes x 4 loads in flight; 5 blocks/SM (48 registers).
 // Swept on config 5 (tools/helm_probe.py): per CG iteration 120 us at (2, 4, 5) vs 164 at
-// (4, 4, -), 151 at (1, 8, -), 205 at (2, 2, -); more registers cost more than they hide.
+// (4, 4, -), 143 at (4, 4, 5), 151 at (1, 8, -), 198 at (8, 2, 5), 205 at (2, 2, -); more registers
+// cost more than they hide.
 #include <cooperative_groups.h>
 #include <math.h>
 
