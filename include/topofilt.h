@@ -70,7 +70,16 @@ typedef struct {
     const double *hs;     /* [n], Hs_i = sum_j W_ij */
 } tf_view;
 
-/* Build statistics (diagnostics; all host values). */
+/* Which build path produced a handle (tf_build_info.path). */
+#define TF_PATH_CELL_LIST 0      /* uniform cell list + radix sort + count/fill (any centroids) */
+#define TF_PATH_LATTICE_TESTED 1 /* lattice-ordered centroids: per-type candidate table, every
+                                    candidate decided by the exact fp64 pair test */
+#define TF_PATH_LATTICE_EXACT 2  /* lattice-ordered centroids exactly on a dyadic grid: the pair
+                                    test and weight of each table entry are position-independent
+                                    and evaluated once on the host (R22) */
+
+/* Build statistics (diagnostics; all host values). For lattice-path builds, bins = cubes per
+ * axis, nbins = cubes, max_candidates = the largest per-type table, bin_side = 0. */
 typedef struct {
     double bin_side;      /* cell-list bin side s >= rmin*(1+1e-6) */
     int64_t bins[3];      /* bins per dimension (bins[2] = 1 in 2D) */
@@ -79,7 +88,7 @@ typedef struct {
     int64_t large_rows;   /* rows whose bin neighbourhood exceeded the shared-memory path
                              (built unsorted, then sorted by the row-sort kernel) */
     int32_t radix_passes;
-    int32_t reserved;
+    int32_t path;         /* TF_PATH_* */
 } tf_build_info;
 
 /*
@@ -88,14 +97,35 @@ typedef struct {
  *   n:         number of cells, 1 <= n < 2^31 - 1.
  *   dim:       2 or 3.
  *   rmin:      filter radius, finite and > 0 (rmin <= 0 is invalid).
- *   stream:    cudaStream_t; the call synchronises this stream twice (bounding box
- *              and nnz readback) and returns a complete handle.
+ *   stream:    cudaStream_t; the call synchronises this stream a few times (lattice
+ *              detection, bounding box, nnz readback) and returns a complete handle.
  *   out:       receives the handle (set to NULL on failure).
  * Errors: TF_ERR_INVALID (arguments, non-finite centroid), TF_ERR_NOMEM, TF_ERR_CUDA,
  *         TF_ERR_OVERFLOW.
  */
 TF_API tf_status tf_build_filter(const double *centroids, int64_t n, int dim, double rmin,
                           void *stream, tf_filter *out);
+
+/*
+ * tf_build_filter_ex -- tf_build_filter with a path choice (the result is the same CSR and Hs
+ * on every path: same pairs, bitwise the same weights; Hs within rounding of the order).
+ *   flags = TF_BUILD_AUTO: tf_build_filter's behaviour. Centroids ordered as a cube lattice --
+ *     cell T*((k*ny + j)*nx + i) + t (1 <= T <= 8 cells per cube, x fastest; FEniCS
+ *     BoxMesh/RectangleMesh order) -- within 5% of the spacing of
+ *     c[t] + (i hx, j hy, k hz) are detected from a prefix and verified on the device over every
+ *     centroid; their rows are then built from a per-type offset table (no cell list, no sort):
+ *     TF_PATH_LATTICE_EXACT when every coordinate is exactly on the lattice and on a dyadic grid,
+ *     else TF_PATH_LATTICE_TESTED. Anything else takes the cell list (TF_PATH_CELL_LIST).
+ *     Detection costs a few small device-to-host copies (synchronising `stream`).
+ *   flags = TF_BUILD_CELL_LIST: always the cell list.
+ *   flags = TF_BUILD_LATTICE: the lattice path or TF_ERR_INVALID (tests, benchmarks).
+ * Other arguments and errors as tf_build_filter; TF_ERR_INVALID for unknown flags.
+ */
+#define TF_BUILD_AUTO 0
+#define TF_BUILD_CELL_LIST 1
+#define TF_BUILD_LATTICE 2
+TF_API tf_status tf_build_filter_ex(const double *centroids, int64_t n, int dim, double rmin, int flags,
+                                    void *stream, tf_filter *out);
 
 /*
  * tf_build_stencil -- matrix-free filter for a regular grid (

@@ -24,7 +24,7 @@ _STATUS = {0: "TF_OK", 1: "TF_ERR_INVALID", 2: "TF_ERR_NOMEM", 3: "TF_ERR_CUDA",
 
 # Every symbol include/topofilt.h declares (checked by tests/test_abi.py).
 EXPORTS = [
-    "tf_build_filter", "tf_filter_view", "tf_build_stats", "tf_sensitivity_filter", "tf_density_filter",
+    "tf_build_filter", "tf_build_filter_ex", "tf_filter_view", "tf_build_stats", "tf_sensitivity_filter", "tf_density_filter",
     "tf_free", "tf_last_error", "tf_build_filter_host", "tf_sensitivity_filter_host",
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
     "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update", "tf_sensitivity_filter_energy",
@@ -33,6 +33,11 @@ EXPORTS = [
     "tf_helmholtz_build", "tf_helmholtz_filter", "tf_helmholtz_sensitivity", "tf_helmholtz_view",
     "tf_helmholtz_free",
 ]
+
+
+# tf_build_filter_ex flags (TF_BUILD_*) and tf_build_info.path values (TF_PATH_*)
+BUILD_FLAGS = {"auto": 0, "cell_list": 1, "lattice": 2}
+BUILD_PATHS = {0: "cell_list", 1: "lattice_tested", 2: "lattice_exact"}
 
 
 class TopofiltError(RuntimeError):
@@ -50,7 +55,7 @@ class tf_view(ctypes.Structure):
 class tf_build_info(ctypes.Structure):
     _fields_ = [("bin_side", ctypes.c_double), ("bins", ctypes.c_int64 * 3), ("nbins", ctypes.c_int64),
                 ("max_candidates", ctypes.c_int64), ("large_rows", ctypes.c_int64),
-                ("radix_passes", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("radix_passes", ctypes.c_int32), ("path", ctypes.c_int32)]
 
 
 class tf_helmholtz_info(ctypes.Structure):
@@ -73,6 +78,7 @@ def _load():
     PP = ctypes.POINTER(ctypes.c_void_p)
     sig = {
         "tf_build_filter": ([P, I64, I32, D, P, PP], I32),
+        "tf_build_filter_ex": ([P, I64, I32, D, I32, P, PP], I32),
         "tf_build_filter_host": ([P, I64, I32, D, P, PP], I32),
         "tf_filter_view": ([P, ctypes.POINTER(tf_view)], I32),
         "tf_build_stats": ([P, ctypes.POINTER(tf_build_info)], I32),
@@ -208,7 +214,7 @@ class Filter:
         _check(_lib.tf_build_stats(self.handle, ctypes.byref(info)))
         return {"bin_side": info.bin_side, "bins": list(info.bins), "nbins": info.nbins,
                 "max_candidates": info.max_candidates, "large_rows": info.large_rows,
-                "radix_passes": info.radix_passes}
+                "radix_passes": info.radix_passes, "path": BUILD_PATHS[info.path]}
 
     def sensitivity_host(self, x: np.ndarray, dc: np.ndarray, out: np.ndarray | None = None, stream=None):
         return tf_sensitivity_filter_host(self, x, dc, out, stream)
@@ -236,15 +242,21 @@ class Filter:
 
 # ------------------------------------------------------------------ C-ABI-named functions
 
-def tf_build_filter(centroids, rmin: float, stream=None) -> Filter:
-    """Build H (CSR) and Hs from device centroids [N, dim] float64."""
+def tf_build_filter(centroids, rmin: float, stream=None, path: str = "auto") -> Filter:
+    """Build H (CSR) and Hs from device centroids [N, dim] float64.
+    path: "auto" (tf_build_filter: lattice detection, else the cell list), "cell_list" or
+    "lattice" (tf_build_filter_ex with TF_BUILD_CELL_LIST / TF_BUILD_LATTICE)."""
     import torch
     if centroids.dim() != 2:
         raise ValueError("centroids must be [N, dim]")
     n, dim = centroids.shape
     h = ctypes.c_void_p()
-    _check(_lib.tf_build_filter(_dptr(centroids, "centroids", torch.float64), n, dim, float(rmin),
-                                _stream_ptr(stream), ctypes.byref(h)))
+    ptr = _dptr(centroids, "centroids", torch.float64)
+    if path == "auto":
+        _check(_lib.tf_build_filter(ptr, n, dim, float(rmin), _stream_ptr(stream), ctypes.byref(h)))
+    else:
+        _check(_lib.tf_build_filter_ex(ptr, n, dim, float(rmin), BUILD_FLAGS[path], _stream_ptr(stream),
+                                       ctypes.byref(h)))
     return Filter(h)
 
 

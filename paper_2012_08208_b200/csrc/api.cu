@@ -190,7 +190,7 @@ static tf_status check_build_args(int64_t n, int dim, double rmin, tf_filter *ou
     return TF_OK;
 }
 
-static tf_status build_common(const double *c, int64_t n, int dim, double rmin, cudaStream_t s,
+static tf_status build_common(const double *c, int64_t n, int dim, double rmin, int flags, cudaStream_t s,
                               tf_filter *out) {
     tf_filter_s *h = new (std::nothrow) tf_filter_s();
     if (!h) {
@@ -206,7 +206,7 @@ static tf_status build_common(const double *c, int64_t n, int dim, double rmin, 
     h->dim = dim;
     h->rmin = rmin;
     build_trace().begin(s);
-    tf_status st = build_filter_device(c, n, dim, rmin, s, h);
+    tf_status st = build_filter_device(c, n, dim, rmin, flags, s, h);
     h->cols_ascending = true;  // the fill writes every row's columns ascending
     if (st == TF_OK) st = make_apply_plan(h, s);
     build_trace().mark("apply_plan", s);
@@ -257,9 +257,25 @@ tf_status tf_build_filter(const double *centroids, int64_t n, int dim, double rm
     try {
         TF_TRY(check_build_args(n, dim, rmin, out));
         TF_TRY(require_device(centroids, "centroids"));
-        return build_common(centroids, n, dim, rmin, (cudaStream_t)stream, out);
+        return build_common(centroids, n, dim, rmin, TF_BUILD_AUTO, (cudaStream_t)stream, out);
     } catch (...) {
         set_error("tf_build_filter: unexpected host exception");
+        return TF_ERR_NOMEM;
+    }
+}
+
+tf_status tf_build_filter_ex(const double *centroids, int64_t n, int dim, double rmin, int flags, void *stream,
+                             tf_filter *out) {
+    try {
+        TF_TRY(check_build_args(n, dim, rmin, out));
+        if (flags != TF_BUILD_AUTO && flags != TF_BUILD_CELL_LIST && flags != TF_BUILD_LATTICE) {
+            set_error("tf_build_filter_ex: unknown flags %d", flags);
+            return TF_ERR_INVALID;
+        }
+        TF_TRY(require_device(centroids, "centroids"));
+        return build_common(centroids, n, dim, rmin, flags, (cudaStream_t)stream, out);
+    } catch (...) {
+        set_error("tf_build_filter_ex: unexpected host exception");
         return TF_ERR_NOMEM;
     }
 }
@@ -277,7 +293,7 @@ tf_status tf_build_filter_host(const double *centroids_host, int64_t n, int dim,
         TF_TRY(dc.alloc((size_t)n * dim, s, "centroids (device copy)"));
         TF_CUDA_TRY(cudaMemcpyAsync(dc.p, centroids_host, (size_t)n * dim * sizeof(double),
                                     cudaMemcpyHostToDevice, s));
-        return build_common(dc.p, n, dim, rmin, s, out);
+        return build_common(dc.p, n, dim, rmin, TF_BUILD_AUTO, s, out);
     } catch (...) {
         set_error("tf_build_filter_host: unexpected host exception");
         return TF_ERR_NOMEM;

@@ -40,28 +40,6 @@
 namespace tf {
 namespace {
 
-template <int DIM>
-__device__ __forceinline__ double pair_d2(double ax, double ay, double az, double bx, double by,
-                                          double bz) {
-    const double dx = __dsub_rn(ax, bx);
-    const double dy = __dsub_rn(ay, by);
-    double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-    if (DIM == 3) {
-        const double dz = __dsub_rn(az, bz);
-        d2 = __dadd_rn(d2, __dmul_rn(dz, dz));
-    }
-    return d2;
-}
-
-// w = max(0, rmin - sqrt(d2)). d2 == 0 (every row's diagonal) sits outside the fast range of
-// the correctly rounded sqrt sequence and would send the whole warp through its slow-path
-// call once per row; sqrt(0) = 0 exactly, so feed it a safe argument and select rmin.
-__device__ __forceinline__ double weight_of(double rmin, double d2) {
-    const double r = __dsqrt_rn(d2 > 0.0 ? d2 : 1.0);
-    double w = (d2 > 0.0) ? __dsub_rn(rmin, r) : rmin;
-    return w < 0.0 ? 0.0 : w;
-}
-
 // ------------------------------------------------------------------ a2: bounding box
 // part[b*7 + 0..2] = min, [3..5] = max, [6] = non-finite flag (as double)
 __global__ void __launch_bounds__(256) k_bbox_partial(const double *__restrict__ c, int64_t n, int dim,
@@ -870,8 +848,18 @@ tf_status launch_fill(const SortedPts &P, const Grid &g, tf_filter_s *h, int cap
 
 }  // namespace
 
-tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, cudaStream_t s,
+tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, int flags, cudaStream_t s,
                               tf_filter_s *h) {
+    if (flags != TF_BUILD_CELL_LIST) {
+        bool used = false;
+        TF_TRY(build_lattice_csr(c, n, dim, rmin, s, h, &used));
+        if (used) return TF_OK;
+        if (flags == TF_BUILD_LATTICE) {
+            set_error("tf_build_filter_ex: TF_BUILD_LATTICE but the centroids are not a verified cube lattice");
+            return TF_ERR_INVALID;
+        }
+    }
+    h->info.path = TF_PATH_CELL_LIST;
     DeviceInfo di;
     TF_TRY(device_info(&di));
     const int threads = 256;

@@ -1,0 +1,632 @@
+// lattice_build.cu -- structured-mesh path of tf_build_filter (SURVEY.md 8(a) rows a5-a7 on
+// lattice-ordered centroids).
+//
+// The paper's meshes are FEniCS BoxMesh / RectangleMesh lattices: cell
+// T*((k*ny + j)*nx + i) + t of a cube grid with T cells per cube (1 quad/hex, 2 triangles,
+// 6 Kuhn tetrahedra), so cell centroids repeat with the cube. For such inputs the cell list is
+// not needed to find the neighbours of a row: they lie in the cubes within a reach R of the
+// row's cube, and, ordered by (dz, dy, dx, target type), their indices ASCEND -- the CSR column
+// order W is stored in (PAPER.md:442-445 builds the same W densely).
+//
+// Detection (host, from a prefix of the centroids + a few probes) proposes a model
+//   L(cell) = c[t] + (i*hx, j*hy, k*hz)        (c[t] = the actual centroid of cell t of cube 0)
+// and k_lat_verify measures, over EVERY centroid, dev = max |c - L| per component, finiteness,
+// and whether the input is "exact" (every coordinate on a dyadic grid 2^-e, |coordinate| <=
+// 2^50 quanta, and exactly equal to L). The rows are then built from a per-type table of (column delta,
+// cube offset[, weight]) entries, sorted by column delta:
+//   * tested mode (any dev): the table lists every (offset, type) whose nominal distance is below
+//     rmin + 2*sqrt(dim)*dev + slack -- a superset of every true neighbour (R21) -- and
+//     each candidate is decided by the exact fp64 pair test on the caller's bytes (pair_d2, the
+//     oracle's expression), with the weight w = max(0, rmin - sqrt(d2)) as in the cell-list path;
+//   * exact mode (dev = 0 on a dyadic grid): every pair difference c_j - c_i is exact in fp64 and
+//     equals the entry's nominal vector, so d2 (the same uncontracted expression on the same
+//     operands) -- hence the test and the weight -- depends only on the table entry (DESIGN.md
+//     R22); the host evaluates the oracle's expression once per entry and rows are written from
+//     the table with no per-pair arithmetic (interior rows: a copy of the table; Hs = the table's
+//     sum in ascending column order).
+// Rows whose cube lies within R of the grid boundary drop the out-of-grid entries (ballot
+// compaction keeps the order). Count -> scan -> nnz readback -> fill, like the cell-list path.
+// Anything that does not verify falls back to the cell list (tf_build_filter), or is rejected
+// with TF_ERR_INVALID when the caller requires this path (TF_BUILD_LATTICE).
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "tf_internal.cuh"
+
+namespace tf {
+namespace {
+
+constexpr int kLatMaxTable = 6144;  // table entries over all types (16 B each, in shared memory)
+constexpr int kLatMaxReach = 100;   // cube offsets are stored as int8 (+128 bias)
+
+struct LatEntry {
+    int32_t delta;  // column - row (the same for every row of this type)
+    int32_t off;    // (dx + 128) | (dy + 128) << 8 | (dz + 128) << 16
+    double w;       // exact mode: the weight; tested mode: unused
+};
+
+struct LatDev {
+    int64_t n;
+    int T, nx, ny, nz;
+    int R[3];
+    int kstart[kMaxTypes + 1];
+    double hs_full[kMaxTypes];  // exact mode: interior row sums (ascending-column order)
+    double rmin, r2;
+};
+
+struct LatVerifyArgs {
+    int dim, T;
+    uint32_t nx, ny;
+    double c0[kMaxTypes][3];
+    double h[3];
+    double q;  // 2^e of the dyadic grid candidate (0: none)
+};
+
+// ------------------------------------------------------------------ device kernels
+__global__ void k_lat_probe(const double *__restrict__ c, int dim, const int64_t *__restrict__ idx, int m,
+                            double *__restrict__ out) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < m; p += gridDim.x * blockDim.x)
+        for (int d = 0; d < dim; ++d) out[p * 3 + d] = c[idx[p] * dim + d];
+}
+
+// out[0] = max deviation (bits of a non-negative double), out[1] = flags (1: non-finite, 2: not
+// exact: some coordinate is off the 2^-e grid, beyond 2^50 quanta, or not exactly the model value)
+__global__ void __launch_bounds__(256) k_lat_verify(const double *__restrict__ c, int64_t n, LatVerifyArgs a,
+                                                    unsigned long long *__restrict__ out) {
+    __shared__ double sc0[kMaxTypes][3];
+    if (threadIdx.x < kMaxTypes * 3) sc0[threadIdx.x / 3][threadIdx.x % 3] = a.c0[threadIdx.x / 3][threadIdx.x % 3];
+    __syncthreads();
+    double dev = 0.0;
+    unsigned flags = 0;
+    for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < n; id += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = (uint32_t)id;
+        const uint32_t t = u % (uint32_t)a.T, cube = u / (uint32_t)a.T;
+        const uint32_t i = cube % a.nx, rr = cube / a.nx;
+        const uint32_t idx[3] = {i, rr % a.ny, rr / a.ny};
+        for (int d = 0; d < a.dim; ++d) {
+            const double v = c[id * a.dim + d];
+            const double L = fma((double)idx[d], a.h[d], sc0[t][d]);
+            if (!isfinite(v)) flags |= 1u;
+            dev = fmax(dev, fabs(v - L));
+            const double s = v * a.q;
+            if (!(a.q > 0.0 && s == rint(s) && fabs(s) <= 1125899906842624.0 && v == L)) flags |= 2u;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+        flags |= __shfl_xor_sync(0xffffffffu, flags, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&out[0], (unsigned long long)__double_as_longlong(dev));
+        if (flags) atomicOr(&out[1], (unsigned long long)flags);
+    }
+}
+
+template <int DIM>
+__device__ __forceinline__ bool lat_interior(const LatDev &m, int i, int j, int k) {
+    return i >= m.R[0] && i < m.nx - m.R[0] && j >= m.R[1] && j < m.ny - m.R[1] &&
+           (DIM == 2 || (k >= m.R[2] && k < m.nz - m.R[2]));
+}
+
+template <int DIM>
+__device__ __forceinline__ bool lat_in_grid(const LatDev &m, int off, int i, int j, int k) {
+    const int dx = (off & 255) - 128, dy = ((off >> 8) & 255) - 128, dz = ((off >> 16) & 255) - 128;
+    return (unsigned)(i + dx) < (unsigned)m.nx && (unsigned)(j + dy) < (unsigned)m.ny &&
+           (DIM == 2 || (unsigned)(k + dz) < (unsigned)m.nz);
+}
+
+// Exact mode row lengths: thread per row; interior rows take the table size, boundary rows
+// count their in-grid entries.
+template <int DIM>
+__global__ void __launch_bounds__(256) k_lat_count_exact(LatDev m, const LatEntry *__restrict__ tab,
+                                                         int32_t *__restrict__ counts) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m.n; r += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = (uint32_t)r;
+        const int t = (int)(u % (uint32_t)m.T);
+        const uint32_t cube = u / (uint32_t)m.T;
+        const int i = (int)(cube % (uint32_t)m.nx);
+        const uint32_t rr = cube / (uint32_t)m.nx;
+        const int j = (int)(rr % (uint32_t)m.ny), k = (int)(rr / (uint32_t)m.ny);
+        const int ks = m.kstart[t], ke = m.kstart[t + 1];
+        int cnt = ke - ks;
+        if (!lat_interior<DIM>(m, i, j, k)) {
+            cnt = 0;
+            for (int e = ks; e < ke; ++e) cnt += lat_in_grid<DIM>(m, tab[e].off, i, j, k) ? 1 : 0;
+        }
+        counts[r] = cnt;
+    }
+}
+
+// Warp per 32 consecutive rows (decoded once, then stepped), lanes over the row's table entries.
+// FILL = false: row lengths (tested mode); FILL = true: cols / vals / Hs at rowptr.
+template <int DIM, bool EXACT, bool FILL>
+__global__ void __launch_bounds__(256) k_lat_rows(const double *__restrict__ c, LatDev m,
+                                                  const LatEntry *__restrict__ gtab, int ntab,
+                                                  const int64_t *__restrict__ rowptr, int32_t *__restrict__ counts,
+                                                  int32_t *__restrict__ cols, double *__restrict__ vals,
+                                                  double *__restrict__ hs, int32_t *__restrict__ flag) {
+    extern __shared__ __align__(16) unsigned char lat_smem[];
+    LatEntry *stab = reinterpret_cast<LatEntry *>(lat_smem);
+    __shared__ int skst[kMaxTypes + 1];
+    __shared__ double shs[kMaxTypes];
+    for (int e = threadIdx.x; e < ntab; e += blockDim.x) stab[e] = gtab[e];
+    if (threadIdx.x <= kMaxTypes) skst[threadIdx.x] = m.kstart[threadIdx.x];
+    if (threadIdx.x < kMaxTypes) shs[threadIdx.x] = m.hs_full[threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int64_t ntasks = (m.n + 31) / 32;
+    const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t task = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; task < ntasks; task += wstride) {
+        const int64_t r0 = task * 32;
+        const int nr = (int)(m.n - r0 < 32 ? m.n - r0 : 32);
+        const uint32_t u = (uint32_t)r0;
+        int t = (int)(u % (uint32_t)m.T);
+        const uint32_t cube = u / (uint32_t)m.T;
+        int i = (int)(cube % (uint32_t)m.nx);
+        const uint32_t rr = cube / (uint32_t)m.nx;
+        int j = (int)(rr % (uint32_t)m.ny), k = (int)(rr / (uint32_t)m.ny);
+        int64_t rp_lane = 0, rp_end = 0;
+        if (FILL) {
+            if (lane < nr) rp_lane = rowptr[r0 + lane];
+            rp_end = rowptr[r0 + nr];
+        }
+        for (int q = 0; q < nr; ++q) {
+            const int64_t r = r0 + q;
+            const int ks = skst[t], K = skst[t + 1] - ks;
+            const bool interior = lat_interior<DIM>(m, i, j, k);
+            int64_t base = 0, end = 0;
+            if (FILL) {
+                base = __shfl_sync(0xffffffffu, rp_lane, q);
+                const int64_t nxt = __shfl_sync(0xffffffffu, rp_lane, (q + 1) & 31);
+                end = (q + 1 < nr) ? nxt : rp_end;
+            }
+            if (EXACT && interior) {
+                if (FILL) {
+                    int32_t *cq = cols + base;
+                    double *vq = vals + base;
+                    for (int e = lane; e < K; e += 32) {
+                        const LatEntry en = stab[ks + e];
+                        cq[e] = (int32_t)(r + en.delta);
+                        vq[e] = en.w;
+                    }
+                    if (lane == 0) {
+                        hs[r] = shs[t];
+                        if (base + K != end) atomicOr(flag, 1);
+                    }
+                } else if (lane == 0) {
+                    counts[r] = K;
+                }
+            } else {
+                double qx = 0.0, qy = 0.0, qz = 0.0;
+                if (!EXACT) {
+                    qx = c[r * DIM];
+                    qy = c[r * DIM + 1];
+                    if (DIM == 3) qz = c[r * DIM + 2];
+                }
+                int wpos = 0;
+                double hsum = 0.0;
+                for (int e0 = 0; e0 < K; e0 += 32) {
+                    const int e = e0 + lane;
+                    bool ok = e < K;
+                    LatEntry en{0, 0, 0.0};
+                    if (ok) en = stab[ks + e];
+                    if (ok && !interior) ok = lat_in_grid<DIM>(m, en.off, i, j, k);
+                    double d2 = 0.0;
+                    if (!EXACT && ok) {
+                        const int64_t p = r + en.delta;
+                        d2 = pair_d2<DIM>(qx, qy, qz, c[p * DIM], c[p * DIM + 1], (DIM == 3) ? c[p * DIM + 2] : 0.0);
+                        ok = d2 < m.r2;
+                    }
+                    const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+                    if (FILL && ok) {
+                        const double w = EXACT ? en.w : weight_of(m.rmin, d2);
+                        const int64_t kk = base + wpos + __popc(bal & lt);
+                        cols[kk] = (int32_t)(r + en.delta);
+                        vals[kk] = w;
+                        hsum += w;
+                    }
+                    wpos += __popc(bal);
+                }
+                if (FILL) {
+                    for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
+                    if (lane == 0) {
+                        hs[r] = hsum;
+                        if (base + wpos != end) atomicOr(flag, 1);
+                    }
+                } else if (lane == 0) {
+                    counts[r] = wpos;
+                }
+            }
+            if (++t == m.T) {
+                t = 0;
+                if (++i == m.nx) {
+                    i = 0;
+                    if (++j == m.ny) j = 0, ++k;
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host: detection
+struct LatModel {
+    int dim = 0, T = 0;
+    int64_t nx = 0, ny = 1, nz = 1;
+    double c0[kMaxTypes][3] = {};
+    double h[3] = {0, 0, 0};
+};
+
+// Row structure from a prefix A[P x dim]: T cells per cube, nx cubes per row with spacing hx
+// along x, and the step D from row 0 to row 1 (along y, or along z when ny = 1). Returns 1 on
+// success, 0 if the input is not lattice-ordered, -1 if the prefix is too short to decide.
+int detect_rows(const double *A, int64_t P, int64_t n, int dim, LatModel *M, double D[3]) {
+    auto at = [&](int64_t id, int d) { return A[id * dim + d]; };
+    bool need_more = false;
+    for (int T = 1; T <= kMaxTypes; ++T) {
+        if (2 * T > n) break;
+        if (2 * T > P) {
+            need_more = true;
+            break;
+        }
+        const double hx = at(T, 0) - at(0, 0);
+        if (!(hx > 0.0) || !isfinite(hx)) continue;
+        const double tol = 1e-6 * hx;
+        // cube m of row 0 matches cube 0 shifted by m*hx along x
+        auto cube_on_row = [&](int64_t base, const double *shift) {
+            for (int t = 0; t < T; ++t)
+                for (int d = 0; d < dim; ++d)
+                    if (!(fabs(at(base + t, d) - (at(t, d) + shift[d])) <= tol)) return false;
+            return true;
+        };
+        int64_t m = 1;
+        const int64_t lim = std::min(P, n);
+        bool ok = true;
+        for (; T * (m + 1) <= lim; ++m) {
+            const double sh[3] = {(double)m * hx, 0.0, 0.0};
+            if (!cube_on_row(T * m, sh)) break;
+        }
+        int64_t nx;
+        if (T * m == n) {
+            nx = m;  // a single row
+        } else if (T * (m + 1) > lim) {
+            if (lim < n) need_more = true;  // prefix exhausted inside row 0
+            continue;
+        } else {
+            nx = m;
+        }
+        if (nx < 2 || n % (T * nx) != 0) continue;
+        D[0] = D[1] = D[2] = 0.0;
+        if (n > T * nx) {
+            if (2 * T * nx > P) {
+                need_more = true;
+                continue;
+            }
+            for (int d = 0; d < dim; ++d) D[d] = at(T * nx, d) - at(0, d);
+            const bool along_y = D[1] > 0.0 && fabs(D[0]) <= tol && (dim == 2 || fabs(D[2]) <= tol);
+            const bool along_z = dim == 3 && D[2] > 0.0 && fabs(D[0]) <= tol && fabs(D[1]) <= tol;
+            if (!along_y && !along_z) continue;
+            if (along_y) D[0] = D[2] = 0.0;
+            else D[0] = D[1] = 0.0;
+            for (int64_t i = 0; i < nx && ok; ++i) {
+                const double sh[3] = {(double)i * hx + D[0], D[1], D[2]};
+                ok = cube_on_row(T * nx + T * i, sh);
+            }
+            if (!ok) continue;
+        }
+        M->dim = dim;
+        M->T = T;
+        M->nx = nx;
+        M->h[0] = hx;
+        for (int t = 0; t < T; ++t)
+            for (int d = 0; d < dim; ++d) M->c0[t][d] = at(t, d);
+        return 1;
+    }
+    return need_more ? -1 : 0;
+}
+
+tf_status copy_prefix(const double *c, int64_t P, int dim, cudaStream_t s, std::vector<double> &A) {
+    A.resize((size_t)P * dim);
+    TF_CUDA_TRY(cudaMemcpyAsync(A.data(), c, (size_t)P * dim * sizeof(double), cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    return TF_OK;
+}
+
+// Full model (T, nx, ny, nz, spacings) or found = false.
+tf_status detect_model(const double *c, int64_t n, int dim, cudaStream_t s, LatModel *M, bool *found) {
+    *found = false;
+    std::vector<double> A;
+    double D[3];
+    int64_t P = std::min<int64_t>(n, 4096);
+    TF_TRY(copy_prefix(c, P, dim, s, A));
+    int st = detect_rows(A.data(), P, n, dim, M, D);
+    if (st < 0 && P < n) {
+        P = std::min<int64_t>(n, 1 << 16);
+        TF_TRY(copy_prefix(c, P, dim, s, A));
+        st = detect_rows(A.data(), P, n, dim, M, D);
+    }
+    if (st <= 0) return TF_OK;
+    const int64_t rowlen = (int64_t)M->T * M->nx;
+    const int64_t rows = n / rowlen;  // ny*nz
+    const double tol = 1e-6 * M->h[0];
+    if (rows == 1) {
+        M->ny = M->nz = 1;
+        M->h[1] = M->h[2] = M->h[0];
+    } else if (dim == 2) {
+        M->ny = rows;
+        M->nz = 1;
+        M->h[1] = D[1];
+        M->h[2] = M->h[0];
+    } else if (D[2] > 0.0) {  // 3D with one row per layer
+        M->ny = 1;
+        M->nz = rows;
+        M->h[1] = M->h[0];
+        M->h[2] = D[2];
+    } else {
+        // 3D: ny divides rows; the first divisor d whose row T*nx*d leaves the y line is ny
+        M->h[1] = D[1];
+        std::vector<int64_t> divs;
+        for (int64_t d = 2; d * d <= rows; ++d)
+            if (rows % d == 0) {
+                divs.push_back(d);
+                if (d * d != rows && rows / d < rows) divs.push_back(rows / d);
+            }
+        std::sort(divs.begin(), divs.end());
+        if (divs.size() > 512) return TF_OK;
+        int64_t ny = rows;
+        double hz = M->h[0];
+        if (!divs.empty()) {
+            const int m = (int)divs.size();
+            std::vector<int64_t> idx(m);
+            for (int p = 0; p < m; ++p) idx[p] = rowlen * divs[p];
+            DevBuf<int64_t> didx;
+            DevBuf<double> dout;
+            TF_TRY(didx.alloc(m, s, "lattice probes"));
+            TF_TRY(dout.alloc((size_t)m * 3, s, "lattice probe points"));
+            TF_CUDA_TRY(cudaMemcpyAsync(didx.p, idx.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+            k_lat_probe<<<(m + 127) / 128, 128, 0, s>>>(c, dim, didx.p, m, dout.p);
+            TF_LAUNCH_CHECK();
+            std::vector<double> pts((size_t)m * 3);
+            TF_CUDA_TRY(cudaMemcpyAsync(pts.data(), dout.p, (size_t)m * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            TF_CUDA_TRY(cudaStreamSynchronize(s));
+            for (int p = 0; p < m; ++p) {
+                const double *q = &pts[(size_t)p * 3];
+                const double dx = q[0] - M->c0[0][0], dy = q[1] - M->c0[0][1], dz = q[2] - M->c0[0][2];
+                const bool on_y = fabs(dx) <= tol && fabs(dy - (double)divs[p] * D[1]) <= tol && fabs(dz) <= tol;
+                if (on_y) continue;
+                if (!(fabs(dx) <= tol && fabs(dy) <= tol && dz > 0.0)) return TF_OK;  // not a lattice
+                ny = divs[p];
+                hz = dz;
+                break;
+            }
+        }
+        M->ny = ny;
+        M->nz = rows / ny;
+        M->h[2] = hz;
+    }
+    if (M->nx * M->ny * M->nz * M->T != n) return TF_OK;
+    *found = true;
+    return TF_OK;
+}
+
+// Smallest e <= 60 with v * 2^e an integer for every v (0 if none): the dyadic grid candidate.
+double dyadic_scale(const std::vector<double> &vs) {
+    for (int e = 0; e <= 60; ++e) {
+        const double q = ldexp(1.0, e);
+        bool ok = true;
+        for (double v : vs) {
+            const double s = v * q;
+            if (!(s == rint(s)) || fabs(s) > 9007199254740992.0) {
+                ok = false;
+                break;
+            }
+        }
+        if (ok) return q;
+    }
+    return 0.0;
+}
+
+}  // namespace
+
+tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cudaStream_t s, tf_filter_s *h,
+                            bool *used) {
+    *used = false;
+    if (n < 4) return TF_OK;
+    NvtxRange r_det("tf_build/lattice detect + verify");
+    LatModel M;
+    bool found = false;
+    TF_TRY(detect_model(c, n, dim, s, &M, &found));
+    if (!found) return TF_OK;
+    build_trace().mark("lattice detect", s);
+
+    // ---- verify every centroid against the model
+    LatVerifyArgs va{};
+    va.dim = dim;
+    va.T = M.T;
+    va.nx = (uint32_t)M.nx;
+    va.ny = (uint32_t)M.ny;
+    for (int t = 0; t < M.T; ++t)
+        for (int d = 0; d < 3; ++d) va.c0[t][d] = (d < dim) ? M.c0[t][d] : 0.0;
+    for (int d = 0; d < 3; ++d) va.h[d] = M.h[d];
+    {
+        std::vector<double> vs;
+        for (int t = 0; t < M.T; ++t)
+            for (int d = 0; d < dim; ++d) vs.push_back(M.c0[t][d]);
+        for (int d = 0; d < dim; ++d) vs.push_back(M.h[d]);
+        va.q = dyadic_scale(vs);
+    }
+    DeviceInfo di;
+    TF_TRY(device_info(&di));
+    DevBuf<unsigned long long> vout;
+    TF_TRY(vout.alloc(2, s, "lattice verify"));
+    TF_CUDA_TRY(cudaMemsetAsync(vout.p, 0, 2 * sizeof(unsigned long long), s));
+    const unsigned vgrid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 8);
+    k_lat_verify<<<vgrid, 256, 0, s>>>(c, n, va, vout.p);
+    TF_LAUNCH_CHECK();
+    unsigned long long vres[2];
+    TF_CUDA_TRY(cudaMemcpyAsync(vres, vout.p, sizeof(vres), cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    build_trace().mark("lattice verify", s);
+    if (vres[1] & 1ull) return TF_OK;  // non-finite: the cell-list path reports it
+    double dev;
+    memcpy(&dev, &vres[0], sizeof(dev));
+    double hmin = M.h[0];
+    if (M.nx > 1) hmin = std::min(hmin, M.h[0]);
+    if (dim >= 2 && M.ny > 1) hmin = std::min(hmin, M.h[1]);
+    if (dim == 3 && M.nz > 1) hmin = std::min(hmin, M.h[2]);
+    if (!(dev <= 0.05 * hmin)) return TF_OK;
+    const bool exact = (vres[1] & 2ull) == 0;
+
+    // ---- per-type tables
+    const int64_t nd[3] = {M.nx, M.ny, M.nz};
+    double cmax = 0.0, spread[3] = {0, 0, 0};
+    for (int d = 0; d < dim; ++d) {
+        double lo = M.c0[0][d], hi = M.c0[0][d];
+        for (int t = 1; t < M.T; ++t) lo = std::min(lo, M.c0[t][d]), hi = std::max(hi, M.c0[t][d]);
+        spread[d] = hi - lo;
+        cmax = std::max(cmax, std::max(fabs(lo), fabs(hi)) + (double)nd[d] * M.h[d]);
+    }
+    // tested mode: a true neighbour's nominal distance is < rmin + 2 sqrt(dim) (dev + rounding of L)
+    const double slack = 8.0 * 2.220446049250313e-16 * cmax;
+    const double margin = 2.0 * sqrt((double)dim) * (dev + slack) + 1e-9 * rmin + slack;
+    int R[3] = {0, 0, 0};
+    for (int d = 0; d < dim; ++d) {
+        const double reach = ceil((rmin + margin + spread[d]) / M.h[d]);
+        if (!(reach <= (double)kLatMaxReach)) return TF_OK;
+        R[d] = (int)std::min<int64_t>((int64_t)reach, nd[d] - 1);
+    }
+    int64_t span = 1;
+    for (int d = 0; d < dim; ++d) span *= 2 * R[d] + 1;
+    if (span * M.T * M.T > (int64_t)4 << 20) return TF_OK;
+    const double r2 = rmin * rmin;
+    std::vector<LatEntry> tab;
+    LatDev L{};
+    L.n = n;
+    L.T = M.T;
+    L.nx = (int)M.nx;
+    L.ny = (int)M.ny;
+    L.nz = (int)M.nz;
+    for (int d = 0; d < 3; ++d) L.R[d] = R[d];
+    L.rmin = rmin;
+    L.r2 = r2;
+    int maxK = 0;
+    for (int sty = 0; sty < M.T; ++sty) {
+        L.kstart[sty] = (int)tab.size();
+        std::vector<LatEntry> row;
+        for (int dz = -R[2]; dz <= R[2]; ++dz)
+            for (int dy = -R[1]; dy <= R[1]; ++dy)
+                for (int dx = -R[0]; dx <= R[0]; ++dx)
+                    for (int tt = 0; tt < M.T; ++tt) {
+                        const int dd[3] = {dx, dy, dz};
+                        double v[3] = {0, 0, 0};
+                        for (int d = 0; d < dim; ++d) v[d] = (M.c0[tt][d] - M.c0[sty][d]) + (double)dd[d] * M.h[d];
+                        // the oracle's expression, never contracted: in exact mode v is exactly the
+                        // pair difference, so this is the d2 the oracle computes (R22)
+                        volatile double p0 = v[0] * v[0], p1 = v[1] * v[1], p2 = v[2] * v[2];
+                        double d2 = p0 + p1;
+                        if (dim == 3) d2 = d2 + p2;
+                        LatEntry en;
+                        en.delta = (int32_t)((int64_t)M.T * (((int64_t)dz * M.ny + dy) * M.nx + dx) + (tt - sty));
+                        en.off = (dx + 128) | ((dy + 128) << 8) | ((dz + 128) << 16);
+                        en.w = 0.0;
+                        if (exact) {
+                            if (!(d2 < r2)) continue;
+                            double w = (d2 > 0.0) ? rmin - sqrt(d2) : rmin;
+                            en.w = w < 0.0 ? 0.0 : w;
+                        } else {
+                            if (!(sqrt(d2) < rmin + margin)) continue;
+                        }
+                        row.push_back(en);
+                    }
+        std::sort(row.begin(), row.end(), [](const LatEntry &a, const LatEntry &b) { return a.delta < b.delta; });
+        double hsf = 0.0;
+        for (const LatEntry &e : row) hsf += e.w;
+        L.hs_full[sty] = hsf;
+        maxK = std::max(maxK, (int)row.size());
+        tab.insert(tab.end(), row.begin(), row.end());
+        if ((int64_t)tab.size() > kLatMaxTable) return TF_OK;
+    }
+    L.kstart[M.T] = (int)tab.size();
+    for (int t = M.T + 1; t <= kMaxTypes; ++t) L.kstart[t] = L.kstart[M.T];
+    const int ntab = (int)tab.size();
+    DevBuf<LatEntry> dtab;
+    TF_TRY(dtab.alloc(ntab, s, "lattice table"));
+    TF_CUDA_TRY(cudaMemcpyAsync(dtab.p, tab.data(), ntab * sizeof(LatEntry), cudaMemcpyHostToDevice, s));
+    build_trace().mark("lattice table", s);
+
+    // ---- count -> scan -> nnz
+    NvtxRange r_rows("tf_build/lattice count + scan + fill");
+    DevBuf<int32_t> counts, flag;
+    TF_TRY(counts.alloc(n, s, "row counts"));
+    TF_TRY(flag.alloc(1, s, "lattice fill flag"));
+    TF_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int32_t), s));
+    const size_t smem = (size_t)ntab * sizeof(LatEntry);
+    auto launch_rows = [&](auto kern, int64_t *rp, int32_t *cnt, int32_t *cl, double *vl, double *hv) -> tf_status {
+        TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+        const int64_t warps_needed = (n + 31) / 32;
+        const unsigned grid = (unsigned)std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)di.sms * std::max(1, per_sm), (warps_needed + 7) / 8));
+        kern<<<grid, 256, smem, s>>>(c, L, dtab.p, ntab, rp, cnt, cl, vl, hv, flag.p);
+        TF_LAUNCH_CHECK();
+        return TF_OK;
+    };
+    if (exact) {
+        const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 16);
+        if (dim == 3) k_lat_count_exact<3><<<g, 256, 0, s>>>(L, dtab.p, counts.p);
+        else k_lat_count_exact<2><<<g, 256, 0, s>>>(L, dtab.p, counts.p);
+        TF_LAUNCH_CHECK();
+    } else {
+        if (dim == 3) TF_TRY(launch_rows(k_lat_rows<3, false, false>, nullptr, counts.p, nullptr, nullptr, nullptr));
+        else TF_TRY(launch_rows(k_lat_rows<2, false, false>, nullptr, counts.p, nullptr, nullptr, nullptr));
+    }
+    build_trace().mark("lattice count", s);
+    TF_TRY(dalloc(&h->rowptr, n + 3, s, "rowptr (+2 padding for 16-byte bulk copies)"));
+    TF_TRY(exclusive_scan_i32_i64(counts.p, h->rowptr, n, s));
+    int64_t nnz = 0;
+    TF_CUDA_TRY(cudaMemcpyAsync(&nnz, h->rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    if (nnz < n) {
+        set_error("internal: lattice nnz %lld < n %lld", (long long)nnz, (long long)n);
+        return TF_ERR_CUDA;
+    }
+    h->nnz = nnz;
+    build_trace().mark("scan+sync", s);
+
+    // ---- fill
+    TF_TRY(dalloc(&h->cols, nnz + 4, s, "cols (nnz int32, +4 padding for 16-byte bulk copies)"));
+    TF_TRY(dalloc(&h->vals, nnz + 4, s, "vals (nnz fp64, +4 padding)"));
+    TF_TRY(dalloc(&h->hs, n, s, "Hs"));
+    build_trace().mark("alloc_csr", s);
+    if (exact) {
+        if (dim == 3) TF_TRY(launch_rows(k_lat_rows<3, true, true>, h->rowptr, nullptr, h->cols, h->vals, h->hs));
+        else TF_TRY(launch_rows(k_lat_rows<2, true, true>, h->rowptr, nullptr, h->cols, h->vals, h->hs));
+    } else {
+        if (dim == 3) TF_TRY(launch_rows(k_lat_rows<3, false, true>, h->rowptr, nullptr, h->cols, h->vals, h->hs));
+        else TF_TRY(launch_rows(k_lat_rows<2, false, true>, h->rowptr, nullptr, h->cols, h->vals, h->hs));
+    }
+    build_trace().mark("lattice fill", s);
+    int32_t hflag = 0;
+    TF_CUDA_TRY(cudaMemcpyAsync(&hflag, flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hflag != 0) {
+        set_error("internal: lattice fill disagreed with its count pass (row lengths)");
+        return TF_ERR_CUDA;
+    }
+    h->info.bin_side = 0.0;
+    for (int d = 0; d < 3; ++d) h->info.bins[d] = nd[d];
+    h->info.nbins = M.nx * M.ny * M.nz;
+    h->info.max_candidates = maxK;
+    h->info.large_rows = 0;
+    h->info.radix_passes = 0;
+    h->info.path = exact ? TF_PATH_LATTICE_EXACT : TF_PATH_LATTICE_TESTED;
+    *used = true;
+    return TF_OK;
+}
+
+}  // namespace tf

@@ -151,6 +151,31 @@ tf_status require_device(const void *p, const char *name);
 // TF_ERR_INVALID unless the current CUDA device is `device` (a handle's build device)
 tf_status require_current_device(int device, const char *who);
 
+// ------------------------------------------------------------------ the exact pair expression
+// Shared by every build path (cell list and lattice): d2 = (dx*dx + dy*dy) + dz*dz with
+// __dmul_rn/__dadd_rn (never contracted to FMA), the oracle's expression (R2-R3).
+template <int DIM>
+__device__ __forceinline__ double pair_d2(double ax, double ay, double az, double bx, double by,
+                                          double bz) {
+    const double dx = __dsub_rn(ax, bx);
+    const double dy = __dsub_rn(ay, by);
+    double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+    if (DIM == 3) {
+        const double dz = __dsub_rn(az, bz);
+        d2 = __dadd_rn(d2, __dmul_rn(dz, dz));
+    }
+    return d2;
+}
+
+// w = max(0, rmin - sqrt(d2)). d2 == 0 (every row's diagonal) sits outside the fast range of
+// the correctly rounded sqrt sequence and would send the whole warp through its slow-path
+// call once per row; sqrt(0) = 0 exactly, so feed it a safe argument and select rmin.
+__device__ __forceinline__ double weight_of(double rmin, double d2) {
+    const double r = __dsqrt_rn(d2 > 0.0 ? d2 : 1.0);
+    double w = (d2 > 0.0) ? __dsub_rn(rmin, r) : rmin;
+    return w < 0.0 ? 0.0 : w;
+}
+
 // ------------------------------------------------------------------ grid of the cell list
 struct Grid {
     int dim;
@@ -247,9 +272,12 @@ tf_status radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys_alt, u
                            int64_t n, int bits, cudaStream_t s, uint32_t **keys_out,
                            uint32_t **vals_out, int *passes);
 
-// build.cu
-tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, cudaStream_t s,
+// build.cu (flags: TF_BUILD_*; the lattice path is tried first unless TF_BUILD_CELL_LIST)
+tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, int flags, cudaStream_t s,
                               tf_filter_s *h);
+// lattice_build.cu: *used = false (and TF_OK) when the centroids are not a verified lattice
+tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cudaStream_t s, tf_filter_s *h,
+                            bool *used);
 
 // stencil.cu
 tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, double rmin, cudaStream_t s,

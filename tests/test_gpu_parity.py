@@ -98,13 +98,18 @@ def test_apply_long_rows_and_ragged(tf):
 
 # ------------------------------------------------------------------ full build parity
 
+@pytest.mark.parametrize("path", ["auto", "cell_list"])
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4])
-def test_build_and_apply_configs_full(tf, cfg):
+def test_build_and_apply_configs_full(tf, cfg, path):
     """Configs 1-4 in full: the whole CSR and Hs against the oracle's cell list (which is
-    pinned to the brute force and the closed forms), then both filters."""
+    pinned to the brute force and the closed forms), then both filters. "auto" takes the
+    lattice path on configs 1-3 (exact, tested, exact) and the cell list on config 4."""
     c, x, dc, rmin = synth.workload(cfg)
     ref = oracle.build_celllist(c, rmin)
-    f = tf.tf_build_filter(dev(c), rmin)
+    f = tf.tf_build_filter(dev(c), rmin, path=path)
+    expect = {"cell_list": "cell_list"}.get(path, {1: "lattice_exact", 2: "lattice_tested", 3: "lattice_exact",
+                                                    4: "cell_list"}[cfg])
+    assert f.stats()["path"] == expect
     assert f.nnz == ref.nnz
     compare_full(f, ref, f"c{cfg}")
     compare_applies(f, ref, x, dc, f"c{cfg}")
@@ -127,13 +132,16 @@ def _sampled(f, rows_np):
     return rp, cols[idx].cpu().numpy(), vals[idx].cpu().numpy(), hs[rows].cpu().numpy()
 
 
-def test_config5_sampled_rows(tf):
+@pytest.mark.parametrize("path", ["auto", "cell_list"])
+def test_config5_sampled_rows(tf, path):
     """Config 5 (12M Kuhn tets): nnz equals the exact lattice count; 10,000 seeded rows
     (stream S(5,5,0)) match the oracle bit-exactly; both filters at those rows; global
-    structural properties of the whole GPU CSR checked on the device."""
+    structural properties of the whole GPU CSR checked on the device. Both build paths
+    (auto = the exact lattice path)."""
     c, x, dc, rmin = synth.workload(5)
     n = c.shape[0]
-    f = tf.tf_build_filter(dev(c), rmin)
+    f = tf.tf_build_filter(dev(c), rmin, path=path)
+    assert f.stats()["path"] == ("lattice_exact" if path == "auto" else "cell_list")
     assert f.nnz == 1_030_251_952
     rows = np.sort(synth.sample_rows(5, n, 10_000))
     cl = oracle.CellList(c, rmin)
@@ -163,7 +171,8 @@ def test_config5_sampled_rows(tf):
     del rid, first, asc, diag
 
 
-def test_nnz_beyond_int32(tf):
+@pytest.mark.parametrize("path", ["auto", "cell_list"])
+def test_nnz_beyond_int32(tf, path):
     """Maximum-size case: 28.8M Kuhn tets (300x160x100 cubes) give nnz = 2,479,728,752 > 2^31
     (exact lattice count), so every element offset past 2^31 goes through the int64 paths of
     the fill, the apply plan and the TMA window addresses. Checked: nnz against the closed
@@ -171,7 +180,7 @@ def test_nnz_beyond_int32(tf):
     against the oracle; both filters at those rows; ascending columns over the whole CSR."""
     c = synth.kuhn_tets(300, 160, 100)
     n, rmin = c.shape[0], 1.5
-    f = tf.tf_build_filter(dev(c), rmin)
+    f = tf.tf_build_filter(dev(c), rmin, path=path)
     assert f.nnz == 2_479_728_752 > 2**31
     rowptr, colsd, _, _ = f.csr()
     r31 = int(torch.searchsorted(rowptr, torch.tensor([2**31], device="cuda"), right=True).item()) - 1
