@@ -33,6 +33,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <vector>
 
 #include "tf_internal.cuh"
@@ -40,7 +41,7 @@
 namespace tf {
 namespace {
 
-constexpr int kLatMaxTable = 6144;  // table entries over all types (16 B each, in shared memory)
+constexpr int kLatMaxTable = 4096;  // table entries over all types (shared memory: 16 B tested, 48 B exact)
 constexpr int kLatMaxReach = 100;   // cube offsets are stored as int8 (+128 bias)
 
 struct LatEntry {
@@ -53,9 +54,19 @@ struct LatDev {
     int64_t n;
     int T, nx, ny, nz;
     int R[3];
+    int C[3];  // boundary classes per axis (exact mode)
     int kstart[kMaxTypes + 1];
     double hs_full[kMaxTypes];  // exact mode: interior row sums (ascending-column order)
     double rmin, r2;
+};
+
+// Exact mode boundary classes: class cid = ((cz*C1 + cy)*C0 + cx)*T + t owns the list
+// [off[cid], off[cid+1]) of (delta, w) -- its type table restricted to in-grid offsets -- and hs[cid].
+struct LatClasses {
+    const int32_t *off;
+    const int32_t *delta;
+    const double *w;
+    const double *hs;
 };
 
 struct LatVerifyArgs {
@@ -119,11 +130,21 @@ __device__ __forceinline__ bool lat_in_grid(const LatDev &m, int off, int i, int
            (DIM == 2 || (unsigned)(k + dz) < (unsigned)m.nz);
 }
 
-// Exact mode row lengths: thread per row; interior rows take the table size, boundary rows
-// count their in-grid entries.
+// Boundary classes (exact mode): per axis, c = p for p < R, 2R - (n-1-p) for p > n-1-R, else R
+// (c = p when n < 2R+1): rows of one class and type keep the same table entries in the grid.
+__device__ __forceinline__ int lat_axis_class(int p, int n, int R) {
+    return (n < 2 * R + 1) ? p : (p < R ? p : (p > n - 1 - R ? 2 * R - (n - 1 - p) : R));
+}
 template <int DIM>
-__global__ void __launch_bounds__(256) k_lat_count_exact(LatDev m, const LatEntry *__restrict__ tab,
-                                                         int32_t *__restrict__ counts) {
+__device__ __forceinline__ int lat_class_id(const LatDev &m, int t, int i, int j, int k) {
+    const int cx = lat_axis_class(i, m.nx, m.R[0]), cy = lat_axis_class(j, m.ny, m.R[1]);
+    const int cz = (DIM == 3) ? lat_axis_class(k, m.nz, m.R[2]) : 0;
+    return ((cz * m.C[1] + cy) * m.C[0] + cx) * m.T + t;
+}
+
+// Exact mode row lengths: thread per row, the length of its class list.
+template <int DIM>
+__global__ void __launch_bounds__(256) k_lat_count_exact(LatDev m, LatClasses cls, int32_t *__restrict__ counts) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m.n; r += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t u = (uint32_t)r;
         const int t = (int)(u % (uint32_t)m.T);
@@ -131,19 +152,166 @@ __global__ void __launch_bounds__(256) k_lat_count_exact(LatDev m, const LatEntr
         const int i = (int)(cube % (uint32_t)m.nx);
         const uint32_t rr = cube / (uint32_t)m.nx;
         const int j = (int)(rr % (uint32_t)m.ny), k = (int)(rr / (uint32_t)m.ny);
-        const int ks = m.kstart[t], ke = m.kstart[t + 1];
-        int cnt = ke - ks;
-        if (!lat_interior<DIM>(m, i, j, k)) {
-            cnt = 0;
-            for (int e = ks; e < ke; ++e) cnt += lat_in_grid<DIM>(m, tab[e].off, i, j, k) ? 1 : 0;
-        }
-        counts[r] = cnt;
+        const int cid = lat_class_id<DIM>(m, t, i, j, k);
+        counts[r] = cls.off[cid + 1] - cls.off[cid];
     }
 }
 
-// Warp per 32 consecutive rows (decoded once, then stepped), lanes over the row's table entries.
-// FILL = false: row lengths (tested mode); FILL = true: cols / vals / Hs at rowptr.
-template <int DIM, bool EXACT, bool FILL>
+// Cycle table of the exact fill, four shifted copies so that any four consecutive entries are one
+// 16-byte-aligned vector read: copy s holds entries s, s+1, ... of the extended cycle sequence
+// (types 0..T-1 concatenated, S entries; entries S.. repeat the start one cycle later, coloff + T).
+struct LatCycle {
+    const int32_t *col;  // [4][SP] coloff = type + delta
+    const double *w;     // [4][SP]
+    int S, SP;
+};
+
+__device__ __forceinline__ void lat_decode(int64_t r, const LatDev &m, int &t, int &i, int &j, int &k) {
+    const uint32_t u = (uint32_t)r;
+    t = (int)(u % (uint32_t)m.T);
+    const uint32_t cube = u / (uint32_t)m.T;
+    i = (int)(cube % (uint32_t)m.nx);
+    const uint32_t rr = cube / (uint32_t)m.nx;
+    j = (int)(rr % (uint32_t)m.ny);
+    k = (int)(rr / (uint32_t)m.ny);
+}
+
+// Exact-mode fill: warp per 32 consecutive rows.
+//  * all rows interior (one row of cubes, no wrap): the chunk's output is a window of the periodic
+//    cycle sequence (position P = entry P mod S of cycle P div S; column = first row of that cycle
+//    + coloff), written flat over [rowptr[r0], rowptr[r0+nr]): four 16-byte-aligned entries per
+//    lane and step (one int4 of columns, two double2 of weights, read as three LDS.128 from the
+//    shifted copies); the < 4-entry head and tail are scalar;
+//  * otherwise per row: a copy of its boundary class list (interior rows: the type table).
+// Hs = the class's (type's) sum in ascending column order -- the oracle's order.
+template <int DIM>
+__global__ void __launch_bounds__(256) k_lat_fill_exact(LatDev m, LatCycle cy, LatClasses cls,
+                                                        const int64_t *__restrict__ rowptr,
+                                                        int32_t *__restrict__ cols, double *__restrict__ vals,
+                                                        double *__restrict__ hs, int32_t *__restrict__ flag) {
+    extern __shared__ __align__(16) unsigned char lat_smem[];
+    int32_t *scol = reinterpret_cast<int32_t *>(lat_smem);                // [4][SP]
+    double *sw = reinterpret_cast<double *>(scol + 4 * cy.SP);            // [4][SP]
+    __shared__ int skst[kMaxTypes + 1];
+    __shared__ double shs[kMaxTypes];
+    for (int e = threadIdx.x; e < 4 * cy.SP; e += blockDim.x) scol[e] = cy.col[e], sw[e] = cy.w[e];
+    if (threadIdx.x <= kMaxTypes) skst[threadIdx.x] = m.kstart[threadIdx.x];
+    if (threadIdx.x < kMaxTypes) shs[threadIdx.x] = m.hs_full[threadIdx.x];
+    __syncthreads();
+    const int S = cy.S, SP = cy.SP;
+    const int lane = threadIdx.x & 31;
+    const int64_t ntasks = (m.n + 31) / 32;
+    const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t task = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5;
+    // row pointers of the chunk (lane l: rowptr[r0 + l]; all: rowptr[r0 + nr]), loaded one task
+    // ahead so the stores never wait on them
+    int64_t rp_lane = 0, rp_end = 0;
+    auto load_rp = [&](int64_t tk, int64_t &pl, int64_t &pe) {
+        if (tk < ntasks) {
+            const int64_t q0 = tk * 32;
+            const int cnt = (int)(m.n - q0 < 32 ? m.n - q0 : 32);
+            if (lane < cnt) pl = rowptr[q0 + lane];
+            pe = rowptr[q0 + cnt];
+        }
+    };
+    load_rp(task, rp_lane, rp_end);
+    for (; task < ntasks; task += wstride) {
+        const int64_t r0 = task * 32;
+        const int nr = (int)(m.n - r0 < 32 ? m.n - r0 : 32);
+        const int64_t cur_lane = rp_lane, cur_end = rp_end;
+        load_rp(task + wstride, rp_lane, rp_end);
+        int t, i, j, k;
+        lat_decode(r0, m, t, i, j, k);
+        const int i_last = i + (t + nr - 1) / m.T;
+        if (i >= m.R[0] && i_last < m.nx - m.R[0] && lat_interior<DIM>(m, i, j, k)) {
+            const int64_t base = __shfl_sync(0xffffffffu, cur_lane, 0), end = cur_end;
+            const int64_t rowc = r0 - t;  // first row of the chunk's first cycle
+            const int P0 = skst[t];       // cycle position of the chunk's first entry
+            auto scalar_at = [&](int64_t g) {
+                const int64_t P = P0 + (g - base);
+                const int64_t mc = P / S, cc = P - mc * S;
+                cols[g] = (int32_t)(rowc + mc * m.T + scol[cc]);
+                vals[g] = sw[cc];
+            };
+            const int64_t g0 = (base + 3) & ~(int64_t)3, g1 = end & ~(int64_t)3;
+            if (g0 >= g1) {  // no aligned group (tiny tables only)
+                for (int64_t g = base + lane; g < end; g += 32) scalar_at(g);
+            } else {
+                if (base + lane < g0) scalar_at(base + lane);
+                if (g1 + lane < end) scalar_at(g1 + lane);
+                // per 128-entry group G: lane l writes columns G+4l..G+4l+3 (one int4) and weights
+                // G+2l, G+2l+1 and G+64+2l, G+64+2l+1 (two double2): every store instruction covers
+                // 512 contiguous bytes, whole sectors
+                const int64_t PG = P0 + (g0 - base);
+                int64_t mc = (PG + 4 * lane) / S;
+                int cc = (int)(PG + 4 * lane - mc * S);
+                int ca = (int)((PG + 2 * lane) % S), cb = (int)((PG + 64 + 2 * lane) % S);
+                for (int64_t G = g0; G < g1; G += 128) {
+                    if (G + 4 * lane < g1) {
+                        const int sh = cc & 3;
+                        const int4 co = *reinterpret_cast<const int4 *>(scol + sh * SP + (cc - sh));
+                        const int32_t rb = (int32_t)(rowc + mc * m.T);
+                        *reinterpret_cast<int4 *>(cols + G + 4 * lane) =
+                            make_int4(rb + co.x, rb + co.y, rb + co.z, rb + co.w);
+                    }
+                    if (G + 2 * lane < g1) {
+                        const int sh = ca & 1;
+                        *reinterpret_cast<double2 *>(vals + G + 2 * lane) =
+                            *reinterpret_cast<const double2 *>(sw + sh * SP + (ca - sh));
+                    }
+                    if (G + 64 + 2 * lane < g1) {
+                        const int sh = cb & 1;
+                        *reinterpret_cast<double2 *>(vals + G + 64 + 2 * lane) =
+                            *reinterpret_cast<const double2 *>(sw + sh * SP + (cb - sh));
+                    }
+                    cc += 128, ca += 128, cb += 128;
+                    while (cc >= S) cc -= S, ++mc;
+                    while (ca >= S) ca -= S;
+                    while (cb >= S) cb -= S;
+                }
+            }
+            int expect = 0;
+            if (lane < nr) {
+                const int tl = (t + lane) % m.T;
+                hs[r0 + lane] = shs[tl];
+                expect = skst[tl + 1] - skst[tl];
+            }
+            for (int o = 16; o > 0; o >>= 1) expect += __shfl_xor_sync(0xffffffffu, expect, o);
+            if (lane == 0 && expect != end - base) atomicOr(flag, 1);
+            continue;
+        }
+        for (int q = 0; q < nr; ++q) {
+            const int64_t r = r0 + q;
+            const int64_t base = __shfl_sync(0xffffffffu, cur_lane, q);
+            const int64_t nxt = __shfl_sync(0xffffffffu, cur_lane, (q + 1) & 31);
+            const int64_t end = (q + 1 < nr) ? nxt : cur_end;
+            const int cid = lat_class_id<DIM>(m, t, i, j, k);
+            const int cs = cls.off[cid], len = cls.off[cid + 1] - cs;
+            int32_t *cq = cols + base;
+            double *vq = vals + base;
+            for (int e = lane; e < len; e += 32) {
+                cq[e] = (int32_t)(r + cls.delta[cs + e]);
+                vq[e] = cls.w[cs + e];
+            }
+            if (lane == 0) {
+                hs[r] = cls.hs[cid];
+                if (base + len != end) atomicOr(flag, 1);
+            }
+            if (++t == m.T) {
+                t = 0;
+                if (++i == m.nx) {
+                    i = 0;
+                    if (++j == m.ny) j = 0, ++k;
+                }
+            }
+        }
+    }
+}
+
+// Tested mode: warp per 32 consecutive rows (decoded once, then stepped), lanes over the row's
+// table candidates, each decided by the exact fp64 pair test on the caller's coordinates.
+// FILL = false: row lengths; FILL = true: cols / vals / Hs at rowptr.
+template <int DIM, bool FILL>
 __global__ void __launch_bounds__(256) k_lat_rows(const double *__restrict__ c, LatDev m,
                                                   const LatEntry *__restrict__ gtab, int ntab,
                                                   const int64_t *__restrict__ rowptr, int32_t *__restrict__ counts,
@@ -152,10 +320,8 @@ __global__ void __launch_bounds__(256) k_lat_rows(const double *__restrict__ c, 
     extern __shared__ __align__(16) unsigned char lat_smem[];
     LatEntry *stab = reinterpret_cast<LatEntry *>(lat_smem);
     __shared__ int skst[kMaxTypes + 1];
-    __shared__ double shs[kMaxTypes];
     for (int e = threadIdx.x; e < ntab; e += blockDim.x) stab[e] = gtab[e];
     if (threadIdx.x <= kMaxTypes) skst[threadIdx.x] = m.kstart[threadIdx.x];
-    if (threadIdx.x < kMaxTypes) shs[threadIdx.x] = m.hs_full[threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
@@ -164,12 +330,8 @@ __global__ void __launch_bounds__(256) k_lat_rows(const double *__restrict__ c, 
     for (int64_t task = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; task < ntasks; task += wstride) {
         const int64_t r0 = task * 32;
         const int nr = (int)(m.n - r0 < 32 ? m.n - r0 : 32);
-        const uint32_t u = (uint32_t)r0;
-        int t = (int)(u % (uint32_t)m.T);
-        const uint32_t cube = u / (uint32_t)m.T;
-        int i = (int)(cube % (uint32_t)m.nx);
-        const uint32_t rr = cube / (uint32_t)m.nx;
-        int j = (int)(rr % (uint32_t)m.ny), k = (int)(rr / (uint32_t)m.ny);
+        int t, i, j, k;
+        lat_decode(r0, m, t, i, j, k);
         int64_t rp_lane = 0, rp_end = 0;
         if (FILL) {
             if (lane < nr) rp_lane = rowptr[r0 + lane];
@@ -177,70 +339,47 @@ __global__ void __launch_bounds__(256) k_lat_rows(const double *__restrict__ c, 
         }
         for (int q = 0; q < nr; ++q) {
             const int64_t r = r0 + q;
-            const int ks = skst[t], K = skst[t + 1] - ks;
-            const bool interior = lat_interior<DIM>(m, i, j, k);
             int64_t base = 0, end = 0;
             if (FILL) {
                 base = __shfl_sync(0xffffffffu, rp_lane, q);
                 const int64_t nxt = __shfl_sync(0xffffffffu, rp_lane, (q + 1) & 31);
                 end = (q + 1 < nr) ? nxt : rp_end;
             }
-            if (EXACT && interior) {
-                if (FILL) {
-                    int32_t *cq = cols + base;
-                    double *vq = vals + base;
-                    for (int e = lane; e < K; e += 32) {
-                        const LatEntry en = stab[ks + e];
-                        cq[e] = (int32_t)(r + en.delta);
-                        vq[e] = en.w;
-                    }
-                    if (lane == 0) {
-                        hs[r] = shs[t];
-                        if (base + K != end) atomicOr(flag, 1);
-                    }
-                } else if (lane == 0) {
-                    counts[r] = K;
+            const int ks = skst[t], K = skst[t + 1] - ks;
+            const bool interior = lat_interior<DIM>(m, i, j, k);
+            const double qx = c[r * DIM], qy = c[r * DIM + 1], qz = (DIM == 3) ? c[r * DIM + 2] : 0.0;
+            int wpos = 0;
+            double hsum = 0.0;
+            for (int e0 = 0; e0 < K; e0 += 32) {
+                const int e = e0 + lane;
+                bool ok = e < K;
+                LatEntry en{0, 0, 0.0};
+                if (ok) en = stab[ks + e];
+                if (ok && !interior) ok = lat_in_grid<DIM>(m, en.off, i, j, k);
+                double d2 = 0.0;
+                if (ok) {
+                    const int64_t p = r + en.delta;
+                    d2 = pair_d2<DIM>(qx, qy, qz, c[p * DIM], c[p * DIM + 1], (DIM == 3) ? c[p * DIM + 2] : 0.0);
+                    ok = d2 < m.r2;
                 }
-            } else {
-                double qx = 0.0, qy = 0.0, qz = 0.0;
-                if (!EXACT) {
-                    qx = c[r * DIM];
-                    qy = c[r * DIM + 1];
-                    if (DIM == 3) qz = c[r * DIM + 2];
+                const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+                if (FILL && ok) {
+                    const double w = weight_of(m.rmin, d2);
+                    const int64_t kk = base + wpos + __popc(bal & lt);
+                    cols[kk] = (int32_t)(r + en.delta);
+                    vals[kk] = w;
+                    hsum += w;
                 }
-                int wpos = 0;
-                double hsum = 0.0;
-                for (int e0 = 0; e0 < K; e0 += 32) {
-                    const int e = e0 + lane;
-                    bool ok = e < K;
-                    LatEntry en{0, 0, 0.0};
-                    if (ok) en = stab[ks + e];
-                    if (ok && !interior) ok = lat_in_grid<DIM>(m, en.off, i, j, k);
-                    double d2 = 0.0;
-                    if (!EXACT && ok) {
-                        const int64_t p = r + en.delta;
-                        d2 = pair_d2<DIM>(qx, qy, qz, c[p * DIM], c[p * DIM + 1], (DIM == 3) ? c[p * DIM + 2] : 0.0);
-                        ok = d2 < m.r2;
-                    }
-                    const uint32_t bal = __ballot_sync(0xffffffffu, ok);
-                    if (FILL && ok) {
-                        const double w = EXACT ? en.w : weight_of(m.rmin, d2);
-                        const int64_t kk = base + wpos + __popc(bal & lt);
-                        cols[kk] = (int32_t)(r + en.delta);
-                        vals[kk] = w;
-                        hsum += w;
-                    }
-                    wpos += __popc(bal);
+                wpos += __popc(bal);
+            }
+            if (FILL) {
+                for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
+                if (lane == 0) {
+                    hs[r] = hsum;
+                    if (base + wpos != end) atomicOr(flag, 1);
                 }
-                if (FILL) {
-                    for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
-                    if (lane == 0) {
-                        hs[r] = hsum;
-                        if (base + wpos != end) atomicOr(flag, 1);
-                    }
-                } else if (lane == 0) {
-                    counts[r] = wpos;
-                }
+            } else if (lane == 0) {
+                counts[r] = wpos;
             }
             if (++t == m.T) {
                 t = 0;
@@ -552,10 +691,99 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     }
     L.kstart[M.T] = (int)tab.size();
     for (int t = M.T + 1; t <= kMaxTypes; ++t) L.kstart[t] = L.kstart[M.T];
+    // the reach that matters is the largest cube offset actually in the tables (the enumeration
+    // bound above is conservative): it sets the interior test and the boundary classes
+    for (int d = 0; d < 3; ++d) R[d] = 0;
+    for (const LatEntry &e : tab) {
+        const int dd[3] = {(e.off & 255) - 128, ((e.off >> 8) & 255) - 128, ((e.off >> 16) & 255) - 128};
+        for (int d = 0; d < dim; ++d) R[d] = std::max(R[d], std::abs(dd[d]));
+    }
+    for (int d = 0; d < 3; ++d) L.R[d] = R[d];
+    const auto th0 = std::chrono::steady_clock::now();
     const int ntab = (int)tab.size();
-    DevBuf<LatEntry> dtab;
-    TF_TRY(dtab.alloc(ntab, s, "lattice table"));
-    TF_CUDA_TRY(cudaMemcpyAsync(dtab.p, tab.data(), ntab * sizeof(LatEntry), cudaMemcpyHostToDevice, s));
+    // One upload: [tested: the candidate table] or [exact: cycle table (4 shifted copies) +
+    // boundary classes]. Exact-mode boundary classes (per axis C_d = min(n_d, 2R_d + 1); see
+    // lat_axis_class): each (class, type) list is the type table restricted to the offsets in the
+    // grid at a representative position; Hs summed in ascending column order (the oracle's order).
+    std::vector<unsigned char> blob;
+    auto put = [&](const void *src, size_t bytes) -> size_t {
+        const size_t at = (blob.size() + 15) & ~(size_t)15;
+        blob.resize(at + bytes);
+        if (bytes) memcpy(blob.data() + at, src, bytes);
+        return at;
+    };
+    size_t o_tab = 0, o_ccol = 0, o_cw = 0, o_off = 0, o_delta = 0, o_w = 0, o_hs = 0;
+    const int SP = (ntab + 3 + 3) & ~3;
+    if (!exact) {
+        o_tab = put(tab.data(), (size_t)ntab * sizeof(LatEntry));
+    } else {
+        std::vector<int32_t> ccol((size_t)4 * SP);
+        std::vector<double> cw((size_t)4 * SP);
+        std::vector<int32_t> seqc(ntab);
+        std::vector<double> seqw(ntab);
+        for (int sty = 0; sty < M.T; ++sty)
+            for (int e = L.kstart[sty]; e < L.kstart[sty + 1]; ++e) seqc[e] = sty + tab[e].delta, seqw[e] = tab[e].w;
+        for (int sh = 0; sh < 4; ++sh)
+            for (int x = 0; x < SP; ++x) {
+                const int p = x + sh;  // extended cycle position
+                ccol[(size_t)sh * SP + x] = seqc[p % ntab] + M.T * (p / ntab);
+                cw[(size_t)sh * SP + x] = seqw[p % ntab];
+            }
+        o_ccol = put(ccol.data(), ccol.size() * sizeof(int32_t));
+        o_cw = put(cw.data(), cw.size() * sizeof(double));
+        int C[3] = {1, 1, 1};
+        for (int d = 0; d < dim; ++d) C[d] = (int)std::min<int64_t>(nd[d], 2 * R[d] + 1);
+        for (int d = 0; d < 3; ++d) L.C[d] = C[d];
+        const int64_t ncls = (int64_t)C[0] * C[1] * C[2] * M.T;
+        if (ncls > (1 << 20)) return TF_OK;
+        auto rep = [&](int cl, int d) -> int64_t {  // a position of class cl on axis d
+            if (nd[d] < 2 * R[d] + 1 || cl <= R[d]) return cl;
+            return nd[d] - 1 - (2 * R[d] - cl);
+        };
+        std::vector<int32_t> c_off(1, 0), c_delta;
+        std::vector<double> c_w, c_hs;
+        for (int cz = 0; cz < C[2]; ++cz)
+            for (int cy = 0; cy < C[1]; ++cy)
+                for (int cx = 0; cx < C[0]; ++cx) {
+                    const int64_t pos[3] = {rep(cx, 0), rep(cy, 1), rep(cz, 2)};
+                    for (int sty = 0; sty < M.T; ++sty) {
+                        double hsum = 0.0;
+                        for (int e = L.kstart[sty]; e < L.kstart[sty + 1]; ++e) {
+                            const int off = tab[e].off;
+                            const int dd[3] = {(off & 255) - 128, ((off >> 8) & 255) - 128, ((off >> 16) & 255) - 128};
+                            bool in = true;
+                            for (int d = 0; d < dim; ++d) in = in && pos[d] + dd[d] >= 0 && pos[d] + dd[d] < nd[d];
+                            if (!in) continue;
+                            c_delta.push_back(tab[e].delta);
+                            c_w.push_back(tab[e].w);
+                            hsum += tab[e].w;
+                        }
+                        c_off.push_back((int32_t)c_delta.size());
+                        c_hs.push_back(hsum);
+                        if (c_delta.size() > ((size_t)1 << 24)) return TF_OK;
+                    }
+                }
+        o_off = put(c_off.data(), c_off.size() * sizeof(int32_t));
+        o_delta = put(c_delta.data(), c_delta.size() * sizeof(int32_t));
+        o_w = put(c_w.data(), c_w.size() * sizeof(double));
+        o_hs = put(c_hs.data(), c_hs.size() * sizeof(double));
+    }
+    const auto th1 = std::chrono::steady_clock::now();
+    DevBuf<unsigned char> dblob;
+    TF_TRY(dblob.alloc(blob.size(), s, "lattice tables"));
+    TF_CUDA_TRY(cudaMemcpyAsync(dblob.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+    if (PhaseTrace::enabled()) {
+        const auto th2 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[topofilt trace] lattice host: tables %.3f ms, upload %zu B %.3f ms\n",
+                std::chrono::duration<double, std::milli>(th1 - th0).count(), blob.size(),
+                std::chrono::duration<double, std::milli>(th2 - th1).count());
+    }
+    auto at = [&](size_t o) { return dblob.p + o; };
+    const LatEntry *dtab = reinterpret_cast<const LatEntry *>(at(o_tab));
+    const LatCycle cyc{reinterpret_cast<const int32_t *>(at(o_ccol)), reinterpret_cast<const double *>(at(o_cw)), ntab,
+                       SP};
+    const LatClasses cls{reinterpret_cast<const int32_t *>(at(o_off)), reinterpret_cast<const int32_t *>(at(o_delta)),
+                         reinterpret_cast<const double *>(at(o_w)), reinterpret_cast<const double *>(at(o_hs))};
     build_trace().mark("lattice table", s);
 
     // ---- count -> scan -> nnz
@@ -564,26 +792,27 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     TF_TRY(counts.alloc(n, s, "row counts"));
     TF_TRY(flag.alloc(1, s, "lattice fill flag"));
     TF_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int32_t), s));
-    const size_t smem = (size_t)ntab * sizeof(LatEntry);
-    auto launch_rows = [&](auto kern, int64_t *rp, int32_t *cnt, int32_t *cl, double *vl, double *hv) -> tf_status {
+    auto grid_for = [&](auto kern, size_t smem, unsigned *grid) -> tf_status {
         TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
         TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
         const int64_t warps_needed = (n + 31) / 32;
-        const unsigned grid = (unsigned)std::max<int64_t>(
-            1, std::min<int64_t>((int64_t)di.sms * std::max(1, per_sm), (warps_needed + 7) / 8));
-        kern<<<grid, 256, smem, s>>>(c, L, dtab.p, ntab, rp, cnt, cl, vl, hv, flag.p);
-        TF_LAUNCH_CHECK();
+        *grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * std::max(1, per_sm),
+                                                                 (warps_needed + 7) / 8));
         return TF_OK;
     };
+    const size_t smem_tab = (size_t)ntab * sizeof(LatEntry), smem_cyc = (size_t)4 * SP * (sizeof(int32_t) + sizeof(double));
+    unsigned grid = 0;
     if (exact) {
         const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 16);
-        if (dim == 3) k_lat_count_exact<3><<<g, 256, 0, s>>>(L, dtab.p, counts.p);
-        else k_lat_count_exact<2><<<g, 256, 0, s>>>(L, dtab.p, counts.p);
+        if (dim == 3) k_lat_count_exact<3><<<g, 256, 0, s>>>(L, cls, counts.p);
+        else k_lat_count_exact<2><<<g, 256, 0, s>>>(L, cls, counts.p);
         TF_LAUNCH_CHECK();
     } else {
-        if (dim == 3) TF_TRY(launch_rows(k_lat_rows<3, false, false>, nullptr, counts.p, nullptr, nullptr, nullptr));
-        else TF_TRY(launch_rows(k_lat_rows<2, false, false>, nullptr, counts.p, nullptr, nullptr, nullptr));
+        auto kern = (dim == 3) ? k_lat_rows<3, false> : k_lat_rows<2, false>;
+        TF_TRY(grid_for(kern, smem_tab, &grid));
+        kern<<<grid, 256, smem_tab, s>>>(c, L, dtab, ntab, nullptr, counts.p, nullptr, nullptr, nullptr, flag.p);
+        TF_LAUNCH_CHECK();
     }
     build_trace().mark("lattice count", s);
     TF_TRY(dalloc(&h->rowptr, n + 3, s, "rowptr (+2 padding for 16-byte bulk copies)"));
@@ -604,11 +833,15 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     TF_TRY(dalloc(&h->hs, n, s, "Hs"));
     build_trace().mark("alloc_csr", s);
     if (exact) {
-        if (dim == 3) TF_TRY(launch_rows(k_lat_rows<3, true, true>, h->rowptr, nullptr, h->cols, h->vals, h->hs));
-        else TF_TRY(launch_rows(k_lat_rows<2, true, true>, h->rowptr, nullptr, h->cols, h->vals, h->hs));
+        auto kern = (dim == 3) ? k_lat_fill_exact<3> : k_lat_fill_exact<2>;
+        TF_TRY(grid_for(kern, smem_cyc, &grid));
+        kern<<<grid, 256, smem_cyc, s>>>(L, cyc, cls, h->rowptr, h->cols, h->vals, h->hs, flag.p);
+        TF_LAUNCH_CHECK();
     } else {
-        if (dim == 3) TF_TRY(launch_rows(k_lat_rows<3, false, true>, h->rowptr, nullptr, h->cols, h->vals, h->hs));
-        else TF_TRY(launch_rows(k_lat_rows<2, false, true>, h->rowptr, nullptr, h->cols, h->vals, h->hs));
+        auto kern = (dim == 3) ? k_lat_rows<3, true> : k_lat_rows<2, true>;
+        TF_TRY(grid_for(kern, smem_tab, &grid));
+        kern<<<grid, 256, smem_tab, s>>>(c, L, dtab, ntab, h->rowptr, nullptr, h->cols, h->vals, h->hs, flag.p);
+        TF_LAUNCH_CHECK();
     }
     build_trace().mark("lattice fill", s);
     int32_t hflag = 0;

@@ -24,7 +24,7 @@ def main():
         c, _, _, rmin = synth.workload(cfg)
         cd = torch.from_numpy(c).cuda()
         n, dim = c.shape
-        for path in ("lattice", "cell_list"):
+        for path in os.environ.get("BUILD_PATHS", "lattice,cell_list").split(","):
             f = tf.tf_build_filter(cd, rmin, path=path)
             nnz, got = f.nnz, f.stats()["path"]
             f.close()
