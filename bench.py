@@ -2,8 +2,12 @@
 """Benchmark of the filter hot path (BASELINE.json metric) -> ONE JSON line on rank 0.
 
 A step = one pass of the whole hot path over the workload:
-  tf_build_filter (bbox, keys, radix sort, cell start, count, scan, fill with Hs)
+  tf_build_filter (the library's path choice: lattice-ordered centroids such as config 5 take
+  the lattice build -- detect, verify, per-type tables, count, scan, fill with Hs; anything
+  else the cell list -- bbox, keys, radix sort, cell start, count, scan, fill with Hs)
   + APPLIES x (tf_sensitivity_filter + tf_density_filter)
+`build_cell_list` times the cell-list path on the same input after the timed region
+(--build-path selects the path used inside the step).
 on config 5 by default (12M Kuhn-tet centroids, rmin 1.5, 20 applies; BASELINE.json
 configs[4] -- the configuration the north-star targets are quoted on), inputs resident in
 HBM. value = algorithmic bytes of the step / step time (GB/s; bytes model SURVEY.md 8(d)).
@@ -256,7 +260,7 @@ def run_ours(args):
     def step(record):
         e0, e1 = ev(), ev()
         e0.record(stream)
-        f = tf.tf_build_filter(cd, rmin)
+        f = tf.tf_build_filter(cd, rmin, path=args.build_path)
         e1.record(stream)
         pairs = []
         for _ in range(applies):
@@ -299,6 +303,20 @@ def run_ours(args):
     launches = tf.kernel_launches() - k0
     if dist:
         dist.barrier()
+    # the general (cell-list) build on the same input, outside the timed region
+    fb = tf.tf_build_filter(cd, rmin)
+    build_path = fb.stats()["path"]
+    fb.close()
+    t_cl = []
+    for it in range(4):
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        fb = tf.tf_build_filter(cd, rmin, path="cell_list")
+        e1.record(stream)
+        torch.cuda.synchronize()
+        fb.close()
+        if it:
+            t_cl.append(e0.elapsed_time(e1) / 1e3)
     elapsed = t_start.elapsed_time(t_end) / 1e3
     for e0, e1, pairs in rec["_all"]:
         rec["build"].append(e0.elapsed_time(e1) / 1e3)
@@ -343,7 +361,13 @@ def run_ours(args):
                        "parallelism": f"replicas{ws}"},
             "build": {"ms": t_build * 1e3, "nnz_per_s": nnz / t_build,
                       "gbs": build_bytes(n, nnz, dim) / t_build / 1e9,
-                      "frac_of_8tbs": build_bytes(n, nnz, dim) / t_build / 1e9 / HBM_NOMINAL_GBS},
+                      "frac_of_8tbs": build_bytes(n, nnz, dim) / t_build / 1e9 / HBM_NOMINAL_GBS,
+                      "path": build_path if args.build_path == "auto" else args.build_path},
+            "build_cell_list": {"ms": statistics.mean(t_cl) * 1e3, "nnz_per_s": nnz / statistics.mean(t_cl),
+                                "gbs": build_bytes(n, nnz, dim) / statistics.mean(t_cl) / 1e9,
+                                "frac_of_8tbs": build_bytes(n, nnz, dim) / statistics.mean(t_cl) / 1e9
+                                / HBM_NOMINAL_GBS,
+                                "note": "the general path (any centroids), same input, timed after the step loop"},
             "apply": {"sensitivity_us": t_sens * 1e6, "sensitivity_gbs": sens_gbs,
                       "sensitivity_frac_of_8tbs": sens_gbs / HBM_NOMINAL_GBS,
                       "density_us": t_dens * 1e6, "density_gbs": dens_bytes(n, nnz) / t_dens / 1e9,
@@ -437,6 +461,7 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=200000)
+    ap.add_argument("--build-path", choices=["auto", "cell_list", "lattice"], default="auto")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: timing rules need --warmup >= 3", file=sys.stderr)

@@ -121,6 +121,17 @@ TF_API tf_status tf_build_filter(const double *centroids, int64_t n, int dim, do
  *   flags = TF_BUILD_LATTICE: the lattice path or TF_ERR_INVALID (tests, benchmarks).
  * Other arguments and errors as tf_build_filter; TF_ERR_INVALID for unknown flags.
  */
+/*
+ * tf_lattice_detect_host -- the detection step of the lattice path alone, on a HOST array (no
+ * CUDA calls; test hook and diagnostics). Reads a prefix and a few probe rows of `centroids_host`
+ * [n x dim] and proposes the lattice model: *ntypes = T (0 if the input is not lattice-ordered),
+ * cubes = (nx, ny, nz), spacing = (hx, hy, hz). It does not verify every point: tf_build_filter
+ * does that on the device before using the model.
+ * Errors: TF_ERR_INVALID (NULL argument, dim, n out of range).
+ */
+TF_API tf_status tf_lattice_detect_host(const double *centroids_host, int64_t n, int dim, int32_t *ntypes,
+                                        int64_t cubes[3], double spacing[3]);
+
 #define TF_BUILD_AUTO 0
 #define TF_BUILD_CELL_LIST 1
 #define TF_BUILD_LATTICE 2

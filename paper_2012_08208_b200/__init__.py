@@ -24,7 +24,7 @@ _STATUS = {0: "TF_OK", 1: "TF_ERR_INVALID", 2: "TF_ERR_NOMEM", 3: "TF_ERR_CUDA",
 
 # Every symbol include/topofilt.h declares (checked by tests/test_abi.py).
 EXPORTS = [
-    "tf_build_filter", "tf_build_filter_ex", "tf_filter_view", "tf_build_stats", "tf_sensitivity_filter", "tf_density_filter",
+    "tf_build_filter", "tf_build_filter_ex", "tf_lattice_detect_host", "tf_filter_view", "tf_build_stats", "tf_sensitivity_filter", "tf_density_filter",
     "tf_free", "tf_last_error", "tf_build_filter_host", "tf_sensitivity_filter_host",
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
     "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update", "tf_sensitivity_filter_energy",
@@ -79,6 +79,7 @@ def _load():
     sig = {
         "tf_build_filter": ([P, I64, I32, D, P, PP], I32),
         "tf_build_filter_ex": ([P, I64, I32, D, I32, P, PP], I32),
+        "tf_lattice_detect_host": ([P, I64, I32, P, P, P], I32),
         "tf_build_filter_host": ([P, I64, I32, D, P, PP], I32),
         "tf_filter_view": ([P, ctypes.POINTER(tf_view)], I32),
         "tf_build_stats": ([P, ctypes.POINTER(tf_build_info)], I32),
@@ -258,6 +259,22 @@ def tf_build_filter(centroids, rmin: float, stream=None, path: str = "auto") -> 
         _check(_lib.tf_build_filter_ex(ptr, n, dim, float(rmin), BUILD_FLAGS[path], _stream_ptr(stream),
                                        ctypes.byref(h)))
     return Filter(h)
+
+
+def tf_lattice_detect_host(centroids: np.ndarray):
+    """Detection step of the lattice build on a host array (no GPU needed): returns None or
+    {"T": cells per cube, "cubes": (nx, ny, nz), "spacing": (hx, hy, hz)}."""
+    c = np.ascontiguousarray(centroids, dtype=np.float64)
+    if c.ndim != 2:
+        raise ValueError("centroids must be [N, dim]")
+    T = ctypes.c_int32()
+    cubes = (ctypes.c_int64 * 3)()
+    sp = (ctypes.c_double * 3)()
+    _check(_lib.tf_lattice_detect_host(c.ctypes.data_as(ctypes.c_void_p), c.shape[0], c.shape[1], ctypes.byref(T),
+                                       cubes, sp))
+    if T.value == 0:
+        return None
+    return {"T": T.value, "cubes": tuple(cubes), "spacing": tuple(sp)}
 
 
 def tf_build_stencil(dim: int, nx: int, ny: int, nz: int, h: float, rmin: float, stream=None) -> Filter:

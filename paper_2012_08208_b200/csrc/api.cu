@@ -280,6 +280,24 @@ tf_status tf_build_filter_ex(const double *centroids, int64_t n, int dim, double
     }
 }
 
+tf_status tf_lattice_detect_host(const double *centroids_host, int64_t n, int dim, int32_t *ntypes, int64_t cubes[3],
+                                 double spacing[3]) {
+    try {
+        if (!centroids_host || !ntypes || !cubes || !spacing) {
+            set_error("tf_lattice_detect_host: NULL argument");
+            return TF_ERR_INVALID;
+        }
+        if ((dim != 2 && dim != 3) || n < 1 || n >= (int64_t)0x7fffffff) {
+            set_error("tf_lattice_detect_host: dim must be 2 or 3 and 1 <= n < 2^31-1");
+            return TF_ERR_INVALID;
+        }
+        return lattice_detect_host(centroids_host, n, dim, ntypes, cubes, spacing);
+    } catch (...) {
+        set_error("tf_lattice_detect_host: unexpected host exception");
+        return TF_ERR_NOMEM;
+    }
+}
+
 tf_status tf_build_filter_host(const double *centroids_host, int64_t n, int dim, double rmin, void *stream,
                                tf_filter *out) {
     try {

@@ -62,11 +62,18 @@ struct LatDev {
 
 // Exact mode boundary classes: class cid = ((cz*C1 + cy)*C0 + cx)*T + t owns the list
 // [off[cid], off[cid+1]) of (delta, w) -- its type table restricted to in-grid offsets -- and hs[cid].
+// Class cid = ((cz*C1 + cy)*C0 + cx)*T + t keeps the entries of its type table whose offsets stay
+// in the grid: bit e of mask[cid*W + e/32] (W = words per class); pre[cid*W + w] = set bits in
+// words < w; len[cid] = set bits; hs[cid] = their weights summed in ascending column order.
 struct LatClasses {
-    const int32_t *off;
-    const int32_t *delta;
-    const double *w;
+    const uint32_t *mask;
+    const int32_t *pre;
+    const int32_t *len;
     const double *hs;
+    int ncls, W;
+    static size_t smem_bytes(int ncls, int W) {
+        return (size_t)ncls * (sizeof(double) + sizeof(int32_t)) + (size_t)ncls * W * 2 * sizeof(uint32_t);
+    }
 };
 
 struct LatVerifyArgs {
@@ -152,8 +159,7 @@ __global__ void __launch_bounds__(256) k_lat_count_exact(LatDev m, LatClasses cl
         const int i = (int)(cube % (uint32_t)m.nx);
         const uint32_t rr = cube / (uint32_t)m.nx;
         const int j = (int)(rr % (uint32_t)m.ny), k = (int)(rr / (uint32_t)m.ny);
-        const int cid = lat_class_id<DIM>(m, t, i, j, k);
-        counts[r] = cls.off[cid + 1] - cls.off[cid];
+        counts[r] = cls.len[lat_class_id<DIM>(m, t, i, j, k)];
     }
 }
 
@@ -184,20 +190,30 @@ __device__ __forceinline__ void lat_decode(int64_t r, const LatDev &m, int &t, i
 //    shifted copies); the < 4-entry head and tail are scalar;
 //  * otherwise per row: a copy of its boundary class list (interior rows: the type table).
 // Hs = the class's (type's) sum in ascending column order -- the oracle's order.
+#ifndef TF_LAT_MINB
+#define TF_LAT_MINB 1
+#endif
 template <int DIM>
-__global__ void __launch_bounds__(256) k_lat_fill_exact(LatDev m, LatCycle cy, LatClasses cls,
+__global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, LatCycle cy, LatClasses cls,
                                                         const int64_t *__restrict__ rowptr,
                                                         int32_t *__restrict__ cols, double *__restrict__ vals,
                                                         double *__restrict__ hs, int32_t *__restrict__ flag) {
     extern __shared__ __align__(16) unsigned char lat_smem[];
     int32_t *scol = reinterpret_cast<int32_t *>(lat_smem);                // [4][SP]
     double *sw = reinterpret_cast<double *>(scol + 4 * cy.SP);            // [4][SP]
+    double *chs = sw + 4 * cy.SP;                                         // [ncls]
+    int32_t *clen = reinterpret_cast<int32_t *>(chs + cls.ncls);          // [ncls]
+    uint32_t *cmask = reinterpret_cast<uint32_t *>(clen + cls.ncls);      // [ncls*W]
+    int32_t *cpre = reinterpret_cast<int32_t *>(cmask + cls.ncls * cls.W);  // [ncls*W]
     __shared__ int skst[kMaxTypes + 1];
     __shared__ double shs[kMaxTypes];
     for (int e = threadIdx.x; e < 4 * cy.SP; e += blockDim.x) scol[e] = cy.col[e], sw[e] = cy.w[e];
+    for (int e = threadIdx.x; e < cls.ncls; e += blockDim.x) chs[e] = cls.hs[e], clen[e] = cls.len[e];
+    for (int e = threadIdx.x; e < cls.ncls * cls.W; e += blockDim.x) cmask[e] = cls.mask[e], cpre[e] = cls.pre[e];
     if (threadIdx.x <= kMaxTypes) skst[threadIdx.x] = m.kstart[threadIdx.x];
     if (threadIdx.x < kMaxTypes) shs[threadIdx.x] = m.hs_full[threadIdx.x];
     __syncthreads();
+    const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;
     const int S = cy.S, SP = cy.SP;
     const int lane = threadIdx.x & 31;
     const int64_t ntasks = (m.n + 31) / 32;
@@ -227,10 +243,10 @@ __global__ void __launch_bounds__(256) k_lat_fill_exact(LatDev m, LatCycle cy, L
             const int64_t base = __shfl_sync(0xffffffffu, cur_lane, 0), end = cur_end;
             const int64_t rowc = r0 - t;  // first row of the chunk's first cycle
             const int P0 = skst[t];       // cycle position of the chunk's first entry
-            auto scalar_at = [&](int64_t g) {
-                const int64_t P = P0 + (g - base);
-                const int64_t mc = P / S, cc = P - mc * S;
-                cols[g] = (int32_t)(rowc + mc * m.T + scol[cc]);
+            auto scalar_at = [&](int64_t g) {  // head / tail entries: chunk offsets are small ints
+                const int P = P0 + (int)(g - base);
+                const int mc = P / S, cc = P - mc * S;
+                cols[g] = (int32_t)(rowc + (int64_t)mc * m.T + scol[cc]);
                 vals[g] = sw[cc];
             };
             const int64_t g0 = (base + 3) & ~(int64_t)3, g1 = end & ~(int64_t)3;
@@ -241,33 +257,43 @@ __global__ void __launch_bounds__(256) k_lat_fill_exact(LatDev m, LatCycle cy, L
                 if (g1 + lane < end) scalar_at(g1 + lane);
                 // per 128-entry group G: lane l writes columns G+4l..G+4l+3 (one int4) and weights
                 // G+2l, G+2l+1 and G+64+2l, G+64+2l+1 (two double2): every store instruction covers
-                // 512 contiguous bytes, whole sectors
-                const int64_t PG = P0 + (g0 - base);
-                int64_t mc = (PG + 4 * lane) / S;
-                int cc = (int)(PG + 4 * lane - mc * S);
-                int ca = (int)((PG + 2 * lane) % S), cb = (int)((PG + 64 + 2 * lane) % S);
-                for (int64_t G = g0; G < g1; G += 128) {
-                    if (G + 4 * lane < g1) {
-                        const int sh = cc & 3;
-                        const int4 co = *reinterpret_cast<const int4 *>(scol + sh * SP + (cc - sh));
-                        const int32_t rb = (int32_t)(rowc + mc * m.T);
-                        *reinterpret_cast<int4 *>(cols + G + 4 * lane) =
-                            make_int4(rb + co.x, rb + co.y, rb + co.z, rb + co.w);
+                // 512 contiguous bytes, whole sectors. Cycle positions < S + 195: no division.
+                const int PG = P0 + (int)(g0 - base);
+                int mc = 0, cc = PG + 4 * lane, ca = PG + 2 * lane, cb = PG + 64 + 2 * lane;
+                while (cc >= S) cc -= S, ++mc;
+                while (ca >= S) ca -= S;
+                while (cb >= S) cb -= S;
+                // four groups per iteration: all shared-memory reads first, then all stores (ILP);
+                // table positions stay inside the padded table, so the reads need no predicate
+#ifndef TF_LAT_U
+#define TF_LAT_U 4
+#endif
+                constexpr int U = TF_LAT_U;
+                for (int64_t G = g0; G < g1; G += 128 * U) {
+                    int4 co[U];
+                    double2 wa[U], wb[U];
+                    int32_t rb[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int shc = cc & 3, sha = ca & 1, shb = cb & 1;
+                        co[u] = *reinterpret_cast<const int4 *>(scol + shc * SP + (cc - shc));
+                        wa[u] = *reinterpret_cast<const double2 *>(sw + sha * SP + (ca - sha));
+                        wb[u] = *reinterpret_cast<const double2 *>(sw + shb * SP + (cb - shb));
+                        rb[u] = (int32_t)(rowc + (int64_t)mc * m.T);
+                        cc += 128, ca += 128, cb += 128;
+                        while (cc >= S) cc -= S, ++mc;
+                        while (ca >= S) ca -= S;
+                        while (cb >= S) cb -= S;
                     }
-                    if (G + 2 * lane < g1) {
-                        const int sh = ca & 1;
-                        *reinterpret_cast<double2 *>(vals + G + 2 * lane) =
-                            *reinterpret_cast<const double2 *>(sw + sh * SP + (ca - sh));
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int64_t Gu = G + 128 * u;
+                        if (Gu + 4 * lane < g1)
+                            *reinterpret_cast<int4 *>(cols + Gu + 4 * lane) =
+                                make_int4(rb[u] + co[u].x, rb[u] + co[u].y, rb[u] + co[u].z, rb[u] + co[u].w);
+                        if (Gu + 2 * lane < g1) *reinterpret_cast<double2 *>(vals + Gu + 2 * lane) = wa[u];
+                        if (Gu + 64 + 2 * lane < g1) *reinterpret_cast<double2 *>(vals + Gu + 64 + 2 * lane) = wb[u];
                     }
-                    if (G + 64 + 2 * lane < g1) {
-                        const int sh = cb & 1;
-                        *reinterpret_cast<double2 *>(vals + G + 64 + 2 * lane) =
-                            *reinterpret_cast<const double2 *>(sw + sh * SP + (cb - sh));
-                    }
-                    cc += 128, ca += 128, cb += 128;
-                    while (cc >= S) cc -= S, ++mc;
-                    while (ca >= S) ca -= S;
-                    while (cb >= S) cb -= S;
                 }
             }
             int expect = 0;
@@ -285,17 +311,25 @@ __global__ void __launch_bounds__(256) k_lat_fill_exact(LatDev m, LatCycle cy, L
             const int64_t base = __shfl_sync(0xffffffffu, cur_lane, q);
             const int64_t nxt = __shfl_sync(0xffffffffu, cur_lane, (q + 1) & 31);
             const int64_t end = (q + 1 < nr) ? nxt : cur_end;
+            // a copy of the row's class: the type table entries flagged in its mask, scattered to
+            // their ranks (ascending order kept), all from shared memory
             const int cid = lat_class_id<DIM>(m, t, i, j, k);
-            const int cs = cls.off[cid], len = cls.off[cid + 1] - cs;
+            const int ks = skst[t], K = skst[t + 1] - ks;
             int32_t *cq = cols + base;
             double *vq = vals + base;
-            for (int e = lane; e < len; e += 32) {
-                cq[e] = (int32_t)(r + cls.delta[cs + e]);
-                vq[e] = cls.w[cs + e];
+            const int64_t rowc = r - t;
+            for (int e0 = 0; e0 < K; e0 += 32) {
+                const int wd = cid * cls.W + (e0 >> 5);
+                const uint32_t word = cmask[wd];
+                if (e0 + lane < K && ((word >> lane) & 1u)) {
+                    const int pos = cpre[wd] + __popc(word & lt);
+                    cq[pos] = (int32_t)(rowc + scol[ks + e0 + lane]);
+                    vq[pos] = sw[ks + e0 + lane];
+                }
             }
             if (lane == 0) {
-                hs[r] = cls.hs[cid];
-                if (base + len != end) atomicOr(flag, 1);
+                hs[r] = chs[cid];
+                if (base + clen[cid] != end) atomicOr(flag, 1);
             }
             if (++t == m.T) {
                 t = 0;
@@ -468,24 +502,69 @@ int detect_rows(const double *A, int64_t P, int64_t n, int dim, LatModel *M, dou
     return need_more ? -1 : 0;
 }
 
-tf_status copy_prefix(const double *c, int64_t P, int dim, cudaStream_t s, std::vector<double> &A) {
-    A.resize((size_t)P * dim);
-    TF_CUDA_TRY(cudaMemcpyAsync(A.data(), c, (size_t)P * dim * sizeof(double), cudaMemcpyDeviceToHost, s));
-    TF_CUDA_TRY(cudaStreamSynchronize(s));
-    return TF_OK;
-}
+// Where detection reads centroids from: a prefix and a few gathered points (3 doubles each).
+struct PointSource {
+    virtual tf_status prefix(int64_t P, std::vector<double> &A) = 0;
+    virtual tf_status gather(const std::vector<int64_t> &idx, std::vector<double> &pts) = 0;
+    virtual ~PointSource() = default;
+};
+
+struct DevicePoints final : PointSource {  // the caller's device array (copies on `s`)
+    const double *c;
+    int dim;
+    cudaStream_t s;
+    DevicePoints(const double *c_, int dim_, cudaStream_t s_) : c(c_), dim(dim_), s(s_) {}
+    tf_status prefix(int64_t P, std::vector<double> &A) override {
+        A.resize((size_t)P * dim);
+        TF_CUDA_TRY(cudaMemcpyAsync(A.data(), c, (size_t)P * dim * sizeof(double), cudaMemcpyDeviceToHost, s));
+        TF_CUDA_TRY(cudaStreamSynchronize(s));
+        return TF_OK;
+    }
+    tf_status gather(const std::vector<int64_t> &idx, std::vector<double> &pts) override {
+        const int m = (int)idx.size();
+        pts.assign((size_t)m * 3, 0.0);
+        if (m == 0) return TF_OK;
+        DevBuf<int64_t> didx;
+        DevBuf<double> dout;
+        TF_TRY(didx.alloc(m, s, "lattice probes"));
+        TF_TRY(dout.alloc((size_t)m * 3, s, "lattice probe points"));
+        TF_CUDA_TRY(cudaMemsetAsync(dout.p, 0, (size_t)m * 3 * sizeof(double), s));
+        TF_CUDA_TRY(cudaMemcpyAsync(didx.p, idx.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        k_lat_probe<<<(m + 127) / 128, 128, 0, s>>>(c, dim, didx.p, m, dout.p);
+        TF_LAUNCH_CHECK();
+        TF_CUDA_TRY(cudaMemcpyAsync(pts.data(), dout.p, (size_t)m * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        TF_CUDA_TRY(cudaStreamSynchronize(s));
+        return TF_OK;
+    }
+};
+
+struct HostPoints final : PointSource {  // a host array (tf_lattice_detect_host: CPU-testable)
+    const double *c;
+    int dim;
+    HostPoints(const double *c_, int dim_) : c(c_), dim(dim_) {}
+    tf_status prefix(int64_t P, std::vector<double> &A) override {
+        A.assign(c, c + (size_t)P * dim);
+        return TF_OK;
+    }
+    tf_status gather(const std::vector<int64_t> &idx, std::vector<double> &pts) override {
+        pts.assign(idx.size() * 3, 0.0);
+        for (size_t p = 0; p < idx.size(); ++p)
+            for (int d = 0; d < dim; ++d) pts[p * 3 + d] = c[idx[p] * dim + d];
+        return TF_OK;
+    }
+};
 
 // Full model (T, nx, ny, nz, spacings) or found = false.
-tf_status detect_model(const double *c, int64_t n, int dim, cudaStream_t s, LatModel *M, bool *found) {
+tf_status detect_model(PointSource &src, int64_t n, int dim, LatModel *M, bool *found) {
     *found = false;
     std::vector<double> A;
     double D[3];
     int64_t P = std::min<int64_t>(n, 4096);
-    TF_TRY(copy_prefix(c, P, dim, s, A));
+    TF_TRY(src.prefix(P, A));
     int st = detect_rows(A.data(), P, n, dim, M, D);
     if (st < 0 && P < n) {
         P = std::min<int64_t>(n, 1 << 16);
-        TF_TRY(copy_prefix(c, P, dim, s, A));
+        TF_TRY(src.prefix(P, A));
         st = detect_rows(A.data(), P, n, dim, M, D);
     }
     if (st <= 0) return TF_OK;
@@ -512,36 +591,25 @@ tf_status detect_model(const double *c, int64_t n, int dim, cudaStream_t s, LatM
         for (int64_t d = 2; d * d <= rows; ++d)
             if (rows % d == 0) {
                 divs.push_back(d);
-                if (d * d != rows && rows / d < rows) divs.push_back(rows / d);
+                if (d * d != rows) divs.push_back(rows / d);
             }
         std::sort(divs.begin(), divs.end());
         if (divs.size() > 512) return TF_OK;
         int64_t ny = rows;
         double hz = M->h[0];
-        if (!divs.empty()) {
-            const int m = (int)divs.size();
-            std::vector<int64_t> idx(m);
-            for (int p = 0; p < m; ++p) idx[p] = rowlen * divs[p];
-            DevBuf<int64_t> didx;
-            DevBuf<double> dout;
-            TF_TRY(didx.alloc(m, s, "lattice probes"));
-            TF_TRY(dout.alloc((size_t)m * 3, s, "lattice probe points"));
-            TF_CUDA_TRY(cudaMemcpyAsync(didx.p, idx.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-            k_lat_probe<<<(m + 127) / 128, 128, 0, s>>>(c, dim, didx.p, m, dout.p);
-            TF_LAUNCH_CHECK();
-            std::vector<double> pts((size_t)m * 3);
-            TF_CUDA_TRY(cudaMemcpyAsync(pts.data(), dout.p, (size_t)m * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
-            TF_CUDA_TRY(cudaStreamSynchronize(s));
-            for (int p = 0; p < m; ++p) {
-                const double *q = &pts[(size_t)p * 3];
-                const double dx = q[0] - M->c0[0][0], dy = q[1] - M->c0[0][1], dz = q[2] - M->c0[0][2];
-                const bool on_y = fabs(dx) <= tol && fabs(dy - (double)divs[p] * D[1]) <= tol && fabs(dz) <= tol;
-                if (on_y) continue;
-                if (!(fabs(dx) <= tol && fabs(dy) <= tol && dz > 0.0)) return TF_OK;  // not a lattice
-                ny = divs[p];
-                hz = dz;
-                break;
-            }
+        std::vector<int64_t> idx(divs.size());
+        for (size_t p = 0; p < divs.size(); ++p) idx[p] = rowlen * divs[p];
+        std::vector<double> pts;
+        TF_TRY(src.gather(idx, pts));
+        for (size_t p = 0; p < divs.size(); ++p) {
+            const double *q = &pts[p * 3];
+            const double dx = q[0] - M->c0[0][0], dy = q[1] - M->c0[0][1], dz = q[2] - M->c0[0][2];
+            const bool on_y = fabs(dx) <= tol && fabs(dy - (double)divs[p] * D[1]) <= tol && fabs(dz) <= tol;
+            if (on_y) continue;
+            if (!(fabs(dx) <= tol && fabs(dy) <= tol && dz > 0.0)) return TF_OK;  // not a lattice
+            ny = divs[p];
+            hz = dz;
+            break;
         }
         M->ny = ny;
         M->nz = rows / ny;
@@ -578,7 +646,8 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     NvtxRange r_det("tf_build/lattice detect + verify");
     LatModel M;
     bool found = false;
-    TF_TRY(detect_model(c, n, dim, s, &M, &found));
+    DevicePoints src(c, dim, s);
+    TF_TRY(detect_model(src, n, dim, &M, &found));
     if (!found) return TF_OK;
     build_trace().mark("lattice detect", s);
 
@@ -618,7 +687,7 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     if (dim >= 2 && M.ny > 1) hmin = std::min(hmin, M.h[1]);
     if (dim == 3 && M.nz > 1) hmin = std::min(hmin, M.h[2]);
     if (!(dev <= 0.05 * hmin)) return TF_OK;
-    const bool exact = (vres[1] & 2ull) == 0;
+    bool exact = (vres[1] & 2ull) == 0;
 
     // ---- per-type tables
     const int64_t nd[3] = {M.nx, M.ny, M.nz};
@@ -642,6 +711,7 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     for (int d = 0; d < dim; ++d) span *= 2 * R[d] + 1;
     if (span * M.T * M.T > (int64_t)4 << 20) return TF_OK;
     const double r2 = rmin * rmin;
+    const int Rb[3] = {R[0], R[1], R[2]};  // enumeration bound
     std::vector<LatEntry> tab;
     LatDev L{};
     L.n = n;
@@ -649,56 +719,80 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     L.nx = (int)M.nx;
     L.ny = (int)M.ny;
     L.nz = (int)M.nz;
-    for (int d = 0; d < 3; ++d) L.R[d] = R[d];
     L.rmin = rmin;
     L.r2 = r2;
     int maxK = 0;
-    for (int sty = 0; sty < M.T; ++sty) {
-        L.kstart[sty] = (int)tab.size();
-        std::vector<LatEntry> row;
-        for (int dz = -R[2]; dz <= R[2]; ++dz)
-            for (int dy = -R[1]; dy <= R[1]; ++dy)
-                for (int dx = -R[0]; dx <= R[0]; ++dx)
-                    for (int tt = 0; tt < M.T; ++tt) {
-                        const int dd[3] = {dx, dy, dz};
-                        double v[3] = {0, 0, 0};
-                        for (int d = 0; d < dim; ++d) v[d] = (M.c0[tt][d] - M.c0[sty][d]) + (double)dd[d] * M.h[d];
-                        // the oracle's expression, never contracted: in exact mode v is exactly the
-                        // pair difference, so this is the d2 the oracle computes (R22)
-                        volatile double p0 = v[0] * v[0], p1 = v[1] * v[1], p2 = v[2] * v[2];
-                        double d2 = p0 + p1;
-                        if (dim == 3) d2 = d2 + p2;
-                        LatEntry en;
-                        en.delta = (int32_t)((int64_t)M.T * (((int64_t)dz * M.ny + dy) * M.nx + dx) + (tt - sty));
-                        en.off = (dx + 128) | ((dy + 128) << 8) | ((dz + 128) << 16);
-                        en.w = 0.0;
-                        if (exact) {
-                            if (!(d2 < r2)) continue;
-                            double w = (d2 > 0.0) ? rmin - sqrt(d2) : rmin;
-                            en.w = w < 0.0 ? 0.0 : w;
-                        } else {
-                            if (!(sqrt(d2) < rmin + margin)) continue;
+    // per-type tables sorted by column delta; exact: accepted entries with their weights, tested:
+    // candidates. Returns false if over the table capacity.
+    auto build_tables = [&](bool ex) -> bool {
+        tab.clear();
+        maxK = 0;
+        for (int sty = 0; sty < M.T; ++sty) {
+            L.kstart[sty] = (int)tab.size();
+            std::vector<LatEntry> row;
+            for (int dz = -Rb[2]; dz <= Rb[2]; ++dz)
+                for (int dy = -Rb[1]; dy <= Rb[1]; ++dy)
+                    for (int dx = -Rb[0]; dx <= Rb[0]; ++dx)
+                        for (int tt = 0; tt < M.T; ++tt) {
+                            const int dd[3] = {dx, dy, dz};
+                            double v[3] = {0, 0, 0};
+                            for (int d = 0; d < dim; ++d) v[d] = (M.c0[tt][d] - M.c0[sty][d]) + (double)dd[d] * M.h[d];
+                            // the oracle's expression, never contracted: in exact mode v is exactly the
+                            // pair difference, so this is the d2 the oracle computes (R22)
+                            volatile double p0 = v[0] * v[0], p1 = v[1] * v[1], p2 = v[2] * v[2];
+                            double d2 = p0 + p1;
+                            if (dim == 3) d2 = d2 + p2;
+                            LatEntry en;
+                            en.delta = (int32_t)((int64_t)M.T * (((int64_t)dz * M.ny + dy) * M.nx + dx) + (tt - sty));
+                            en.off = (dx + 128) | ((dy + 128) << 8) | ((dz + 128) << 16);
+                            en.w = 0.0;
+                            if (ex) {
+                                if (!(d2 < r2)) continue;
+                                double w = (d2 > 0.0) ? rmin - sqrt(d2) : rmin;
+                                en.w = w < 0.0 ? 0.0 : w;
+                            } else {
+                                if (!(sqrt(d2) < rmin + margin)) continue;
+                            }
+                            row.push_back(en);
                         }
-                        row.push_back(en);
-                    }
-        std::sort(row.begin(), row.end(), [](const LatEntry &a, const LatEntry &b) { return a.delta < b.delta; });
-        double hsf = 0.0;
-        for (const LatEntry &e : row) hsf += e.w;
-        L.hs_full[sty] = hsf;
-        maxK = std::max(maxK, (int)row.size());
-        tab.insert(tab.end(), row.begin(), row.end());
-        if ((int64_t)tab.size() > kLatMaxTable) return TF_OK;
+            std::sort(row.begin(), row.end(), [](const LatEntry &x, const LatEntry &y) { return x.delta < y.delta; });
+            double hsf = 0.0;
+            for (const LatEntry &e : row) hsf += e.w;  // ascending column order
+            L.hs_full[sty] = hsf;
+            maxK = std::max(maxK, (int)row.size());
+            tab.insert(tab.end(), row.begin(), row.end());
+            if ((int64_t)tab.size() > kLatMaxTable) return false;
+        }
+        L.kstart[M.T] = (int)tab.size();
+        for (int t = M.T + 1; t <= kMaxTypes; ++t) L.kstart[t] = L.kstart[M.T];
+        // the reach that matters is the largest cube offset in the tables (the enumeration bound is
+        // conservative): it sets the interior test and the boundary classes
+        for (int d = 0; d < 3; ++d) R[d] = 0;
+        for (const LatEntry &e : tab) {
+            const int dd[3] = {(e.off & 255) - 128, ((e.off >> 8) & 255) - 128, ((e.off >> 16) & 255) - 128};
+            for (int d = 0; d < dim; ++d) R[d] = std::max(R[d], std::abs(dd[d]));
+        }
+        for (int d = 0; d < 3; ++d) L.R[d] = R[d];
+        return true;
+    };
+    // exact mode needs the cycle table and the boundary-class masks in shared memory; otherwise
+    // (large reach) the same input is built in tested mode
+    int64_t ncls = 0;
+    int Wc = 0;
+    if (exact) {
+        if (!build_tables(true)) return TF_OK;
+        for (int d = 0; d < 3; ++d) L.C[d] = (d < dim) ? (int)std::min<int64_t>(nd[d], 2 * R[d] + 1) : 1;
+        ncls = (int64_t)L.C[0] * L.C[1] * L.C[2] * M.T;
+        Wc = std::max(1, (maxK + 31) / 32);
+        const int SPx = ((int)tab.size() + 6) & ~3;
+        const size_t need = (size_t)4 * SPx * 12 + (ncls <= (1 << 16) ? LatClasses::smem_bytes((int)ncls, Wc) : SIZE_MAX / 2);
+        if (need > (size_t)160 * 1024) exact = false;
     }
-    L.kstart[M.T] = (int)tab.size();
-    for (int t = M.T + 1; t <= kMaxTypes; ++t) L.kstart[t] = L.kstart[M.T];
-    // the reach that matters is the largest cube offset actually in the tables (the enumeration
-    // bound above is conservative): it sets the interior test and the boundary classes
-    for (int d = 0; d < 3; ++d) R[d] = 0;
-    for (const LatEntry &e : tab) {
-        const int dd[3] = {(e.off & 255) - 128, ((e.off >> 8) & 255) - 128, ((e.off >> 16) & 255) - 128};
-        for (int d = 0; d < dim; ++d) R[d] = std::max(R[d], std::abs(dd[d]));
+    if (!exact) {
+        if (!build_tables(false)) return TF_OK;
+        ncls = 0;
+        Wc = 0;
     }
-    for (int d = 0; d < 3; ++d) L.R[d] = R[d];
     const auto th0 = std::chrono::steady_clock::now();
     const int ntab = (int)tab.size();
     // One upload: [tested: the candidate table] or [exact: cycle table (4 shifted copies) +
@@ -712,7 +806,7 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
         if (bytes) memcpy(blob.data() + at, src, bytes);
         return at;
     };
-    size_t o_tab = 0, o_ccol = 0, o_cw = 0, o_off = 0, o_delta = 0, o_w = 0, o_hs = 0;
+    size_t o_tab = 0, o_ccol = 0, o_cw = 0, o_mask = 0, o_pre = 0, o_len = 0, o_hs = 0;
     const int SP = (ntab + 3 + 3) & ~3;
     if (!exact) {
         o_tab = put(tab.data(), (size_t)ntab * sizeof(LatEntry));
@@ -731,41 +825,40 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
             }
         o_ccol = put(ccol.data(), ccol.size() * sizeof(int32_t));
         o_cw = put(cw.data(), cw.size() * sizeof(double));
-        int C[3] = {1, 1, 1};
-        for (int d = 0; d < dim; ++d) C[d] = (int)std::min<int64_t>(nd[d], 2 * R[d] + 1);
-        for (int d = 0; d < 3; ++d) L.C[d] = C[d];
-        const int64_t ncls = (int64_t)C[0] * C[1] * C[2] * M.T;
-        if (ncls > (1 << 20)) return TF_OK;
         auto rep = [&](int cl, int d) -> int64_t {  // a position of class cl on axis d
             if (nd[d] < 2 * R[d] + 1 || cl <= R[d]) return cl;
             return nd[d] - 1 - (2 * R[d] - cl);
         };
-        std::vector<int32_t> c_off(1, 0), c_delta;
-        std::vector<double> c_w, c_hs;
-        for (int cz = 0; cz < C[2]; ++cz)
-            for (int cy = 0; cy < C[1]; ++cy)
-                for (int cx = 0; cx < C[0]; ++cx) {
+        std::vector<uint32_t> c_mask((size_t)ncls * Wc, 0u);
+        std::vector<int32_t> c_pre((size_t)ncls * Wc, 0), c_len(ncls, 0);
+        std::vector<double> c_hs(ncls, 0.0);
+        int64_t cid = 0;
+        for (int cz = 0; cz < L.C[2]; ++cz)
+            for (int cy = 0; cy < L.C[1]; ++cy)
+                for (int cx = 0; cx < L.C[0]; ++cx) {
                     const int64_t pos[3] = {rep(cx, 0), rep(cy, 1), rep(cz, 2)};
-                    for (int sty = 0; sty < M.T; ++sty) {
+                    for (int sty = 0; sty < M.T; ++sty, ++cid) {
                         double hsum = 0.0;
+                        int cnt = 0;
                         for (int e = L.kstart[sty]; e < L.kstart[sty + 1]; ++e) {
+                            const int el = e - L.kstart[sty];
+                            if (el % 32 == 0) c_pre[cid * Wc + el / 32] = cnt;
                             const int off = tab[e].off;
                             const int dd[3] = {(off & 255) - 128, ((off >> 8) & 255) - 128, ((off >> 16) & 255) - 128};
                             bool in = true;
                             for (int d = 0; d < dim; ++d) in = in && pos[d] + dd[d] >= 0 && pos[d] + dd[d] < nd[d];
                             if (!in) continue;
-                            c_delta.push_back(tab[e].delta);
-                            c_w.push_back(tab[e].w);
+                            c_mask[cid * Wc + el / 32] |= 1u << (el % 32);
                             hsum += tab[e].w;
+                            ++cnt;
                         }
-                        c_off.push_back((int32_t)c_delta.size());
-                        c_hs.push_back(hsum);
-                        if (c_delta.size() > ((size_t)1 << 24)) return TF_OK;
+                        c_len[cid] = cnt;
+                        c_hs[cid] = hsum;
                     }
                 }
-        o_off = put(c_off.data(), c_off.size() * sizeof(int32_t));
-        o_delta = put(c_delta.data(), c_delta.size() * sizeof(int32_t));
-        o_w = put(c_w.data(), c_w.size() * sizeof(double));
+        o_mask = put(c_mask.data(), c_mask.size() * sizeof(uint32_t));
+        o_pre = put(c_pre.data(), c_pre.size() * sizeof(int32_t));
+        o_len = put(c_len.data(), c_len.size() * sizeof(int32_t));
         o_hs = put(c_hs.data(), c_hs.size() * sizeof(double));
     }
     const auto th1 = std::chrono::steady_clock::now();
@@ -782,8 +875,9 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     const LatEntry *dtab = reinterpret_cast<const LatEntry *>(at(o_tab));
     const LatCycle cyc{reinterpret_cast<const int32_t *>(at(o_ccol)), reinterpret_cast<const double *>(at(o_cw)), ntab,
                        SP};
-    const LatClasses cls{reinterpret_cast<const int32_t *>(at(o_off)), reinterpret_cast<const int32_t *>(at(o_delta)),
-                         reinterpret_cast<const double *>(at(o_w)), reinterpret_cast<const double *>(at(o_hs))};
+    const LatClasses cls{reinterpret_cast<const uint32_t *>(at(o_mask)), reinterpret_cast<const int32_t *>(at(o_pre)),
+                         reinterpret_cast<const int32_t *>(at(o_len)), reinterpret_cast<const double *>(at(o_hs)),
+                         (int)ncls, Wc};
     build_trace().mark("lattice table", s);
 
     // ---- count -> scan -> nnz
@@ -801,7 +895,8 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
                                                                  (warps_needed + 7) / 8));
         return TF_OK;
     };
-    const size_t smem_tab = (size_t)ntab * sizeof(LatEntry), smem_cyc = (size_t)4 * SP * (sizeof(int32_t) + sizeof(double));
+    const size_t smem_tab = (size_t)ntab * sizeof(LatEntry);
+    const size_t smem_cyc = (size_t)4 * SP * (sizeof(int32_t) + sizeof(double)) + LatClasses::smem_bytes((int)ncls, Wc);
     unsigned grid = 0;
     if (exact) {
         const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 16);
@@ -859,6 +954,21 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     h->info.radix_passes = 0;
     h->info.path = exact ? TF_PATH_LATTICE_EXACT : TF_PATH_LATTICE_TESTED;
     *used = true;
+    return TF_OK;
+}
+
+tf_status lattice_detect_host(const double *c, int64_t n, int dim, int32_t *T, int64_t cubes[3], double spacing[3]) {
+    *T = 0;
+    for (int d = 0; d < 3; ++d) cubes[d] = 0, spacing[d] = 0.0;
+    if (n < 4) return TF_OK;
+    LatModel M;
+    bool found = false;
+    HostPoints src(c, dim);
+    TF_TRY(detect_model(src, n, dim, &M, &found));
+    if (!found) return TF_OK;
+    *T = M.T;
+    cubes[0] = M.nx, cubes[1] = M.ny, cubes[2] = M.nz;
+    for (int d = 0; d < 3; ++d) spacing[d] = M.h[d];
     return TF_OK;
 }
 

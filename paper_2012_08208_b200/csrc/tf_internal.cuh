@@ -278,6 +278,8 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
 // lattice_build.cu: *used = false (and TF_OK) when the centroids are not a verified lattice
 tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cudaStream_t s, tf_filter_s *h,
                             bool *used);
+// the detection step alone on a host array (no CUDA calls): T = 0 if not lattice-ordered
+tf_status lattice_detect_host(const double *c, int64_t n, int dim, int32_t *T, int64_t cubes[3], double spacing[3]);
 
 // stencil.cu
 tf_status build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h, double rmin, cudaStream_t s,

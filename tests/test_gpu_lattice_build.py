@@ -54,7 +54,7 @@ def _lattice_cases():
     yield "hex_40x20x20_ties", synth.hex_grid(40, 20, 20), 2.0, "lattice_exact"
     yield "kuhn_spec_6x4x2", synth.kuhn_tets(6, 4, 2), 1.5, "lattice_exact"
     yield "kuhn_e02_60x20x4", synth.kuhn_tets(60, 20, 4), 1.5, "lattice_exact"
-    yield "kuhn_rmin2.7", synth.kuhn_tets(14, 11, 9), 2.7, "lattice_exact"
+    yield "kuhn_rmin2.7_downgraded", synth.kuhn_tets(14, 11, 9), 2.7, "lattice_tested"  # classes beyond smem
     yield "hex_aniso", synth.hex_grid(30, 24, 18) * np.array([1.0, 0.75, 1.25]), 1.6, "lattice_exact"
     yield "kuhn_shift_dyadic", synth.kuhn_tets(12, 10, 8) - 37.5, 1.5, "lattice_exact"
     yield "kuhn_shift_thirds", synth.kuhn_tets(12, 10, 8) + (1.0e3 + 1.0 / 3.0), 1.5, "lattice_tested"

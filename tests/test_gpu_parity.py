@@ -415,11 +415,16 @@ def test_errors(tf):
 def test_launch_counter_and_stats(tf):
     c, x, dc, rmin = synth.workload(3)
     k0 = tf.kernel_launches()
-    f = tf.tf_build_filter(dev(c), rmin)
+    f = tf.tf_build_filter(dev(c), rmin, path="cell_list")
     k1 = tf.kernel_launches()
     assert k1 - k0 >= 8
     f.sensitivity(dev(x), dev(dc))
     assert tf.kernel_launches() - k1 == 1
     st = f.stats()
+    assert st["path"] == "cell_list"
     assert st["bin_side"] >= rmin * (1 + 1e-6)
     assert st["max_candidates"] >= 27 and st["large_rows"] == 0
+    g = tf.tf_build_filter(dev(c), rmin)  # lattice path: cubes per axis, the table size
+    sg = g.stats()
+    assert sg["path"] == "lattice_exact" and sg["bin_side"] == 0.0
+    assert sg["bins"] == [160, 80, 80] and sg["max_candidates"] == 27
