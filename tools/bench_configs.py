@@ -58,6 +58,12 @@ def main():
             g.close()
 
         t_build = timed(build, reps_b)
+
+        def build_cl():
+            g = tf.tf_build_filter(cd, rmin, path="cell_list")
+            g.close()
+
+        t_build_cl = timed(build_cl, reps_b)
         f = tf.tf_build_filter(cd, rmin)
         for _ in range(3):
             f.sensitivity(xd, dcd, out=out)
@@ -66,7 +72,9 @@ def main():
         reps = 50 if cfg < 5 else 20
         row = {"config": cfg, "workload": meta["name"], "n": n, "nnz": nnz, "rmin": rmin,
                "build_ms": t_build * 1e3, "build_nnz_per_s": nnz / t_build,
-               "build_gbs": bench.build_bytes(n, nnz, dim) / t_build / 1e9}
+               "build_gbs": bench.build_bytes(n, nnz, dim) / t_build / 1e9,
+               "build_cell_list_ms": t_build_cl * 1e3,
+               "build_cell_list_frac_8tbs": bench.build_bytes(n, nnz, dim) / t_build_cl / 1e9 / HBM}
         row["build_frac_8tbs"] = row["build_gbs"] / HBM
         for mode, fl in (("hot", None), ("cold", flush)):
             ts = timed(lambda: f.sensitivity(xd, dcd, out=out), reps, fl)

@@ -52,7 +52,7 @@ def main(rnd):
     ncu(["-i", rep, "--page", "raw", "--csv"], raw)
     with open(os.path.join(dst, "ncu_full_summary.txt"), "w") as f:
         subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), raw], stdout=f, check=True)
-    for k in ("k_spmv", "k_fill", "k_count"):
+    for k in ("k_spmv", "k_fill", "k_count", "k_lat_fill_exact"):
         src = f"/tmp/src_{k}.csv"
         ncu(["-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{k}", "-c", "1"], src)
         with open(os.path.join(dst, f"{k}_source_hot.txt"), "w") as f:
@@ -63,13 +63,15 @@ def main(rnd):
 
     blocks = summary_blocks(os.path.join(dst, "ncu_full_summary.txt"))
     pick = lambda pat: next(b for b in blocks if pat in b["name"])  # noqa: E731
-    sens, dens, fill, count = pick("k_spmv<1"), pick("k_spmv<0"), pick("k_fill"), pick("k_count")
+    sens, dens, fill, count = pick("k_spmv<1"), pick("k_spmv<0"), pick("k_fill<"), pick("k_count")
+    latfill = pick("k_lat_fill_exact")
     gb = 1e9
     traffic = {
         "source": f"ncu --set full --clock-control none, config 5 (profiles/{rnd}/ncu_full_summary.txt)",
         "k_spmv_sens_bytes_per_launch": (sens["dram__bytes_read.sum"] + sens["dram__bytes_write.sum"]) * gb,
     }
-    for key, b in (("k_count", count), ("k_fill", fill), ("k_spmv_sens", sens), ("k_spmv_dens", dens)):
+    for key, b in (("k_count", count), ("k_fill", fill), ("k_lat_fill_exact", latfill), ("k_spmv_sens", sens),
+                   ("k_spmv_dens", dens)):
         traffic[key] = {"dram_read_bytes": b["dram__bytes_read.sum"] * gb,
                         "dram_write_bytes": b["dram__bytes_write.sum"] * gb,
                         "duration_ms_cold_serialised": b["gpu__time_duration.sum"]}
@@ -89,7 +91,12 @@ def main(rnd):
       f"{d['config'].get('applies_per_step', 20)} × (sensitivity + density))\n")
     w(f"* value **{d['value']:.0f} GB/s** (algorithmic bytes of the step / step time), {d['ms_per_step']:.1f} ms per step, "
       f"{d['gpu_launches']} libtopofilt launches in the timed region")
-    w(f"* build {bd['ms']:.2f} ms = {bd['nnz_per_s']:.3e} nnz/s = {100 * bd['frac_of_8tbs']:.1f}% of 8 TB/s")
+    w(f"* build ({bd.get('path', 'cell_list')} path) {bd['ms']:.2f} ms = {bd['nnz_per_s']:.3e} nnz/s = "
+      f"**{100 * bd['frac_of_8tbs']:.1f}% of 8 TB/s**")
+    if "build_cell_list" in d:
+        bc = d["build_cell_list"]
+        w(f"* the general cell-list build on the same input (`build_cell_list`, timed after the step loop): "
+          f"{bc['ms']:.2f} ms = {bc['nnz_per_s']:.3e} nnz/s = {100 * bc['frac_of_8tbs']:.1f}% of 8 TB/s")
     w(f"* sensitivity apply {ap['sensitivity_us']:.0f} µs = {ap['sensitivity_gbs']:.0f} GB/s = "
       f"**{100 * ap['sensitivity_frac_of_8tbs']:.1f}% of 8 TB/s** ({100 * ap['sensitivity_gbs'] / peak:.1f}% of the measured "
       f"{peak:.0f} GB/s copy peak)")
@@ -109,7 +116,8 @@ def main(rnd):
     w("## ncu --set full (`ncu_full_summary.txt`, `*_source_hot.txt`)\n")
     w("| kernel | duration (ncu) | DRAM read | DRAM write | issue active | DRAM % of peak |")
     w("|---|---|---|---|---|---|")
-    for nm, b in (("k_spmv sensitivity", sens), ("k_spmv density", dens), ("k_fill", fill), ("k_count", count)):
+    for nm, b in (("k_spmv sensitivity", sens), ("k_spmv density", dens), ("k_lat_fill_exact (lattice build)", latfill),
+                  ("k_fill (cell-list build)", fill), ("k_count (cell-list build)", count)):
         w(f"| {nm} | {b['gpu__time_duration.sum']:.3f} ms | {b['dram__bytes_read.sum']:.2f} GB | "
           f"{b['dram__bytes_write.sum']:.3f} GB | {b.get('smsp__issue_active.avg.pct_of_peak_sustained_active', 0):.0f}% | "
           f"{b.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 0):.0f}% |")
@@ -117,11 +125,13 @@ def main(rnd):
       "SASS evidence (`sass_evidence.txt`): `UBLKCP.S.G` (TMA bulk copies) + `SYNCS.*` (mbarriers) in the apply; "
       "`FADD2/FMUL2/FFMA2` (packed fp32x2) in count/fill.\n")
     w("## All configs (`configs.jsonl`, `tools/bench_configs.py`)\n")
-    w("| cfg | N | nnz | build ms | build nnz/s | sens cold µs (% of 8 TB/s) | dens cold µs (% of 8 TB/s) |")
-    w("|---|---|---|---|---|---|---|")
+    w("| cfg | N | nnz | build path | build ms | build nnz/s | cell-list build ms | sens cold µs (% of 8 TB/s) | "
+      "dens cold µs (% of 8 TB/s) |")
+    w("|---|---|---|---|---|---|---|---|---|")
     for r in rows:
         if "config" in r:
-            w(f"| {r['config']} | {r['n']:,} | {r['nnz']:,} | {r['build_ms']:.3f} | {r['build_nnz_per_s']:.2e} | "
+            w(f"| {r['config']} | {r['n']:,} | {r['nnz']:,} | {r['stats'].get('path', '')} | {r['build_ms']:.3f} | "
+              f"{r['build_nnz_per_s']:.2e} | {r.get('build_cell_list_ms', float('nan')):.3f} | "
               f"{r['sens_us_cold']:.1f} ({100 * r['sens_frac_8tbs_cold']:.1f}%) | "
               f"{r['dens_us_cold']:.1f} ({100 * r['dens_frac_8tbs_cold']:.1f}%) |")
     w("\nConfigs 1–2 are launch-bound (µs-scale applies).\n")
