@@ -43,6 +43,10 @@ namespace {
 
 constexpr int kLatMaxTable = 4096;  // table entries over all types (shared memory: 16 B tested, 48 B exact)
 constexpr int kLatMaxReach = 100;   // cube offsets are stored as int8 (+128 bias)
+#ifndef TF_LAT_RPL
+#define TF_LAT_RPL 2
+#endif
+constexpr int kLatRPL = TF_LAT_RPL;  // exact fill: rows per warp task = 32 * kLatRPL (1: 2.46, 2: 2.41 ms at config 5)
 
 struct LatEntry {
     int32_t delta;  // column - row (the same for every row of this type)
@@ -92,22 +96,31 @@ __global__ void k_lat_probe(const double *__restrict__ c, int dim, const int64_t
 }
 
 // out[0] = max deviation (bits of a non-negative double), out[1] = flags (1: non-finite, 2: not
-// exact: some coordinate is off the 2^-e grid, beyond 2^50 quanta, or not exactly the model value)
+// exact: some coordinate is off the 2^-e grid, beyond 2^50 quanta, or not exactly the model value).
+// Block-stride over the rows of cubes (j, k known per row); threads over the row's T*nx*DIM
+// coordinates, read coalesced.
+template <int DIM>
 __global__ void __launch_bounds__(256) k_lat_verify(const double *__restrict__ c, int64_t n, LatVerifyArgs a,
                                                     unsigned long long *__restrict__ out) {
     __shared__ double sc0[kMaxTypes][3];
+    __shared__ double shh[3];
     if (threadIdx.x < kMaxTypes * 3) sc0[threadIdx.x / 3][threadIdx.x % 3] = a.c0[threadIdx.x / 3][threadIdx.x % 3];
+    if (threadIdx.x < 3) shh[threadIdx.x] = a.h[threadIdx.x];
     __syncthreads();
     double dev = 0.0;
     unsigned flags = 0;
-    for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < n; id += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t u = (uint32_t)id;
-        const uint32_t t = u % (uint32_t)a.T, cube = u / (uint32_t)a.T;
-        const uint32_t i = cube % a.nx, rr = cube / a.nx;
-        const uint32_t idx[3] = {i, rr % a.ny, rr / a.ny};
-        for (int d = 0; d < a.dim; ++d) {
-            const double v = c[id * a.dim + d];
-            const double L = fma((double)idx[d], a.h[d], sc0[t][d]);
+    const int64_t rowlen = (int64_t)a.T * a.nx;  // points per row of cubes
+    const int64_t nrows = n / rowlen;
+    const int64_t elems = rowlen * DIM;
+    for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
+        const uint32_t jj = (uint32_t)(row % a.ny), kk = (uint32_t)(row / a.ny);
+        const double *cr = c + row * elems;
+        for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) {
+            const uint32_t p = (uint32_t)(e / DIM), d = (uint32_t)(e - (int64_t)p * DIM);
+            const uint32_t t = p % (uint32_t)a.T, i = p / (uint32_t)a.T;
+            const uint32_t idx = (d == 0) ? i : (d == 1 ? jj : kk);
+            const double v = cr[e];
+            const double L = fma((double)idx, shh[d], sc0[t][d]);
             if (!isfinite(v)) flags |= 1u;
             dev = fmax(dev, fabs(v - L));
             const double s = v * a.q;
@@ -170,6 +183,8 @@ struct LatCycle {
     const int32_t *col;  // [4][SP] coloff = type + delta
     const double *w;     // [4][SP]
     int S, SP;
+    int LW;  // > 0: the weight cycle is replicated to LW entries (two copies, shifted by 0 and 1) in
+             // shared memory and interior chunks store their weights with one TMA bulk copy
 };
 
 __device__ __forceinline__ void lat_decode(int64_t r, const LatDev &m, int &t, int &i, int &j, int &k) {
@@ -199,7 +214,8 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
                                                         int32_t *__restrict__ cols, double *__restrict__ vals,
                                                         double *__restrict__ hs, int32_t *__restrict__ flag) {
     extern __shared__ __align__(16) unsigned char lat_smem[];
-    int32_t *scol = reinterpret_cast<int32_t *>(lat_smem);                // [4][SP]
+    double *wrep = reinterpret_cast<double *>(lat_smem);                  // [2][LW] (LW even)
+    int32_t *scol = reinterpret_cast<int32_t *>(wrep + 2 * cy.LW);        // [4][SP]
     double *sw = reinterpret_cast<double *>(scol + 4 * cy.SP);            // [4][SP]
     double *chs = sw + 4 * cy.SP;                                         // [ncls]
     int32_t *clen = reinterpret_cast<int32_t *>(chs + cls.ncls);          // [ncls]
@@ -210,54 +226,89 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
     for (int e = threadIdx.x; e < 4 * cy.SP; e += blockDim.x) scol[e] = cy.col[e], sw[e] = cy.w[e];
     for (int e = threadIdx.x; e < cls.ncls; e += blockDim.x) chs[e] = cls.hs[e], clen[e] = cls.len[e];
     for (int e = threadIdx.x; e < cls.ncls * cls.W; e += blockDim.x) cmask[e] = cls.mask[e], cpre[e] = cls.pre[e];
+    for (int e = threadIdx.x; e < 2 * cy.LW; e += blockDim.x) {
+        const int x = (e < cy.LW) ? e : e - cy.LW + 1;  // copy 1 starts one entry later
+        wrep[e] = cy.w[x % cy.S];
+    }
     if (threadIdx.x <= kMaxTypes) skst[threadIdx.x] = m.kstart[threadIdx.x];
     if (threadIdx.x < kMaxTypes) shs[threadIdx.x] = m.hs_full[threadIdx.x];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // wrep -> TMA (async proxy) reads
     __syncthreads();
     const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;
     const int S = cy.S, SP = cy.SP;
+    const bool bulk = cy.LW > 0;
+    bool issued = false;
     const int lane = threadIdx.x & 31;
-    const int64_t ntasks = (m.n + 31) / 32;
+    // Tasks: CH consecutive rows (CH = 32 * RPL); the flat path needs only the chunk's first and
+    // end row pointers, the per-row path all of them (RPL per lane)
+    constexpr int RPL = kLatRPL, CH = 32 * RPL;
+    const int64_t ntasks = (m.n + CH - 1) / CH;
     const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
     int64_t task = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5;
-    // row pointers of the chunk (lane l: rowptr[r0 + l]; all: rowptr[r0 + nr]), loaded one task
-    // ahead so the stores never wait on them
-    int64_t rp_lane = 0, rp_end = 0;
-    auto load_rp = [&](int64_t tk, int64_t &pl, int64_t &pe) {
+    // row pointers of the chunk (lane l, slot u: rowptr[r0 + 32u + l]; all: rowptr[r0 + nr]),
+    // loaded one task ahead so the stores never wait on them
+    int64_t rp_lane[RPL], rp_end = 0;
+    auto load_rp = [&](int64_t tk, int64_t *pl, int64_t &pe) {
         if (tk < ntasks) {
-            const int64_t q0 = tk * 32;
-            const int cnt = (int)(m.n - q0 < 32 ? m.n - q0 : 32);
-            if (lane < cnt) pl = rowptr[q0 + lane];
+            const int64_t q0 = tk * CH;
+            const int cnt = (int)(m.n - q0 < CH ? m.n - q0 : CH);
+#pragma unroll
+            for (int u = 0; u < RPL; ++u)
+                if (32 * u + lane < cnt) pl[u] = rowptr[q0 + 32 * u + lane];
             pe = rowptr[q0 + cnt];
         }
     };
     load_rp(task, rp_lane, rp_end);
     for (; task < ntasks; task += wstride) {
-        const int64_t r0 = task * 32;
-        const int nr = (int)(m.n - r0 < 32 ? m.n - r0 : 32);
-        const int64_t cur_lane = rp_lane, cur_end = rp_end;
+        const int64_t r0 = task * CH;
+        const int nr = (int)(m.n - r0 < CH ? m.n - r0 : CH);
+        int64_t cur_lane[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) cur_lane[u] = rp_lane[u];
+        const int64_t cur_end = rp_end;
         load_rp(task + wstride, rp_lane, rp_end);
         int t, i, j, k;
         lat_decode(r0, m, t, i, j, k);
         const int i_last = i + (t + nr - 1) / m.T;
         if (i >= m.R[0] && i_last < m.nx - m.R[0] && lat_interior<DIM>(m, i, j, k)) {
-            const int64_t base = __shfl_sync(0xffffffffu, cur_lane, 0), end = cur_end;
+            const int64_t base = __shfl_sync(0xffffffffu, cur_lane[0], 0), end = cur_end;
             const int64_t rowc = r0 - t;  // first row of the chunk's first cycle
             const int P0 = skst[t];       // cycle position of the chunk's first entry
-            auto scalar_at = [&](int64_t g) {  // head / tail entries: chunk offsets are small ints
+            auto scalar_at = [&](int64_t g, bool with_w) {  // head / tail entries (small chunk offsets)
                 const int P = P0 + (int)(g - base);
                 const int mc = P / S, cc = P - mc * S;
                 cols[g] = (int32_t)(rowc + (int64_t)mc * m.T + scol[cc]);
-                vals[g] = sw[cc];
+                if (with_w) vals[g] = sw[cc];
             };
+            if (bulk) {
+                // weights: the window [P0, P0 + total) of the periodic weight sequence, one bulk
+                // store of its 16-byte-aligned middle (source copy chosen so both sides align)
+                const int64_t a0 = base + (base & 1), a1 = end & ~(int64_t)1;
+                if (lane == 0 && a1 > a0) {
+                    const int Pa = P0 + (int)(a0 - base), sh = Pa & 1;
+                    TF_DCHECK(Pa - sh + (a1 - a0) <= cy.LW);
+                    const uint32_t src = (uint32_t)__cvta_generic_to_shared(wrep + sh * cy.LW + (Pa - sh));
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(vals + a0),
+                                 "r"(src), "r"((uint32_t)((a1 - a0) * 8))
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    issued = true;
+                }
+                if (lane == 1 && (base & 1)) vals[base] = sw[P0 % S];
+                if (lane == 2 && (end & 1) && end - 1 >= a0) vals[end - 1] = sw[(P0 + (int)(end - 1 - base)) % S];
+                if (lane == 3 && a1 <= a0)
+                    for (int64_t g = base; g < end; ++g) vals[g] = sw[(P0 + (int)(g - base)) % S];
+            }
             const int64_t g0 = (base + 3) & ~(int64_t)3, g1 = end & ~(int64_t)3;
             if (g0 >= g1) {  // no aligned group (tiny tables only)
-                for (int64_t g = base + lane; g < end; g += 32) scalar_at(g);
+                for (int64_t g = base + lane; g < end; g += 32) scalar_at(g, !bulk);
             } else {
-                if (base + lane < g0) scalar_at(base + lane);
-                if (g1 + lane < end) scalar_at(g1 + lane);
-                // per 128-entry group G: lane l writes columns G+4l..G+4l+3 (one int4) and weights
-                // G+2l, G+2l+1 and G+64+2l, G+64+2l+1 (two double2): every store instruction covers
-                // 512 contiguous bytes, whole sectors. Cycle positions < S + 195: no division.
+                if (base + lane < g0) scalar_at(base + lane, !bulk);
+                if (g1 + lane < end) scalar_at(g1 + lane, !bulk);
+                // per 128-entry group G: lane l writes columns G+4l..G+4l+3 (one int4) and, without
+                // the bulk path, weights G+2l, G+2l+1 and G+64+2l, G+64+2l+1 (two double2): every
+                // store instruction covers 512 contiguous bytes, whole sectors. Cycle positions
+                // stay < S + 195: no division.
                 const int PG = P0 + (int)(g0 - base);
                 int mc = 0, cc = PG + 4 * lane, ca = PG + 2 * lane, cb = PG + 64 + 2 * lane;
                 while (cc >= S) cc -= S, ++mc;
@@ -269,38 +320,61 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
 #define TF_LAT_U 4
 #endif
                 constexpr int U = TF_LAT_U;
-                for (int64_t G = g0; G < g1; G += 128 * U) {
-                    int4 co[U];
-                    double2 wa[U], wb[U];
-                    int32_t rb[U];
+                if (bulk) {
+                    for (int64_t G = g0; G < g1; G += 128 * U) {
+                        int4 co[U];
+                        int32_t rb[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int shc = cc & 3, sha = ca & 1, shb = cb & 1;
-                        co[u] = *reinterpret_cast<const int4 *>(scol + shc * SP + (cc - shc));
-                        wa[u] = *reinterpret_cast<const double2 *>(sw + sha * SP + (ca - sha));
-                        wb[u] = *reinterpret_cast<const double2 *>(sw + shb * SP + (cb - shb));
-                        rb[u] = (int32_t)(rowc + (int64_t)mc * m.T);
-                        cc += 128, ca += 128, cb += 128;
-                        while (cc >= S) cc -= S, ++mc;
-                        while (ca >= S) ca -= S;
-                        while (cb >= S) cb -= S;
+                        for (int u = 0; u < U; ++u) {
+                            const int shc = cc & 3;
+                            co[u] = *reinterpret_cast<const int4 *>(scol + shc * SP + (cc - shc));
+                            rb[u] = (int32_t)(rowc + (int64_t)mc * m.T);
+                            cc += 128;
+                            while (cc >= S) cc -= S, ++mc;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int64_t Gu = G + 128 * u;
+                            if (Gu + 4 * lane < g1)
+                                *reinterpret_cast<int4 *>(cols + Gu + 4 * lane) =
+                                    make_int4(rb[u] + co[u].x, rb[u] + co[u].y, rb[u] + co[u].z, rb[u] + co[u].w);
+                        }
                     }
+                } else {
+                    for (int64_t G = g0; G < g1; G += 128 * U) {
+                        int4 co[U];
+                        double2 wa[U], wb[U];
+                        int32_t rb[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int64_t Gu = G + 128 * u;
-                        if (Gu + 4 * lane < g1)
-                            *reinterpret_cast<int4 *>(cols + Gu + 4 * lane) =
-                                make_int4(rb[u] + co[u].x, rb[u] + co[u].y, rb[u] + co[u].z, rb[u] + co[u].w);
-                        if (Gu + 2 * lane < g1) *reinterpret_cast<double2 *>(vals + Gu + 2 * lane) = wa[u];
-                        if (Gu + 64 + 2 * lane < g1) *reinterpret_cast<double2 *>(vals + Gu + 64 + 2 * lane) = wb[u];
+                        for (int u = 0; u < U; ++u) {
+                            const int shc = cc & 3, sha = ca & 1, shb = cb & 1;
+                            co[u] = *reinterpret_cast<const int4 *>(scol + shc * SP + (cc - shc));
+                            wa[u] = *reinterpret_cast<const double2 *>(sw + sha * SP + (ca - sha));
+                            wb[u] = *reinterpret_cast<const double2 *>(sw + shb * SP + (cb - shb));
+                            rb[u] = (int32_t)(rowc + (int64_t)mc * m.T);
+                            cc += 128, ca += 128, cb += 128;
+                            while (cc >= S) cc -= S, ++mc;
+                            while (ca >= S) ca -= S;
+                            while (cb >= S) cb -= S;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int64_t Gu = G + 128 * u;
+                            if (Gu + 4 * lane < g1)
+                                *reinterpret_cast<int4 *>(cols + Gu + 4 * lane) =
+                                    make_int4(rb[u] + co[u].x, rb[u] + co[u].y, rb[u] + co[u].z, rb[u] + co[u].w);
+                            if (Gu + 2 * lane < g1) *reinterpret_cast<double2 *>(vals + Gu + 2 * lane) = wa[u];
+                            if (Gu + 64 + 2 * lane < g1)
+                                *reinterpret_cast<double2 *>(vals + Gu + 64 + 2 * lane) = wb[u];
+                        }
                     }
                 }
             }
             int expect = 0;
-            if (lane < nr) {
-                const int tl = (t + lane) % m.T;
-                hs[r0 + lane] = shs[tl];
-                expect = skst[tl + 1] - skst[tl];
+            for (int q = lane; q < nr; q += 32) {
+                const int tl = (t + q) % m.T;
+                hs[r0 + q] = shs[tl];
+                expect += skst[tl + 1] - skst[tl];
             }
             for (int o = 16; o > 0; o >>= 1) expect += __shfl_xor_sync(0xffffffffu, expect, o);
             if (lane == 0 && expect != end - base) atomicOr(flag, 1);
@@ -308,8 +382,14 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
         }
         for (int q = 0; q < nr; ++q) {
             const int64_t r = r0 + q;
-            const int64_t base = __shfl_sync(0xffffffffu, cur_lane, q);
-            const int64_t nxt = __shfl_sync(0xffffffffu, cur_lane, (q + 1) & 31);
+            int64_t base = 0, nxt = 0;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {  // (warp-uniform slot selection)
+                const int64_t b_u = __shfl_sync(0xffffffffu, cur_lane[u], q & 31);
+                const int64_t n_u = __shfl_sync(0xffffffffu, cur_lane[u], (q + 1) & 31);
+                if ((q >> 5) == u) base = b_u;
+                if (((q + 1) >> 5) == u) nxt = n_u;
+            }
             const int64_t end = (q + 1 < nr) ? nxt : cur_end;
             // a copy of the row's class: the type table entries flagged in its mask, scattered to
             // their ranks (ascending order kept), all from shared memory
@@ -340,6 +420,8 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
             }
         }
     }
+    // bulk stores complete (and their shared-memory source stays allocated) before the CTA exits
+    if (issued) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Tested mode: warp per 32 consecutive rows (decoded once, then stepped), lanes over the row's
@@ -672,24 +754,12 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     DevBuf<unsigned long long> vout;
     TF_TRY(vout.alloc(2, s, "lattice verify"));
     TF_CUDA_TRY(cudaMemsetAsync(vout.p, 0, 2 * sizeof(unsigned long long), s));
-    const unsigned vgrid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 8);
-    k_lat_verify<<<vgrid, 256, 0, s>>>(c, n, va, vout.p);
+    const unsigned vgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(M.ny * M.nz, (int64_t)di.sms * 8));
+    if (dim == 3) k_lat_verify<3><<<vgrid, 256, 0, s>>>(c, n, va, vout.p);
+    else k_lat_verify<2><<<vgrid, 256, 0, s>>>(c, n, va, vout.p);
     TF_LAUNCH_CHECK();
-    unsigned long long vres[2];
-    TF_CUDA_TRY(cudaMemcpyAsync(vres, vout.p, sizeof(vres), cudaMemcpyDeviceToHost, s));
-    TF_CUDA_TRY(cudaStreamSynchronize(s));
-    build_trace().mark("lattice verify", s);
-    if (vres[1] & 1ull) return TF_OK;  // non-finite: the cell-list path reports it
-    double dev;
-    memcpy(&dev, &vres[0], sizeof(dev));
-    double hmin = M.h[0];
-    if (M.nx > 1) hmin = std::min(hmin, M.h[0]);
-    if (dim >= 2 && M.ny > 1) hmin = std::min(hmin, M.h[1]);
-    if (dim == 3 && M.nz > 1) hmin = std::min(hmin, M.h[2]);
-    if (!(dev <= 0.05 * hmin)) return TF_OK;
-    bool exact = (vres[1] & 2ull) == 0;
-
-    // ---- per-type tables
+    // ---- per-type tables (bounds need the deviation; the exact-mode tables do not, so they are
+    // built on the host while the verification pass runs, and discarded if it rules them out)
     const int64_t nd[3] = {M.nx, M.ny, M.nz};
     double cmax = 0.0, spread[3] = {0, 0, 0};
     for (int d = 0; d < dim; ++d) {
@@ -700,18 +770,21 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     }
     // tested mode: a true neighbour's nominal distance is < rmin + 2 sqrt(dim) (dev + rounding of L)
     const double slack = 8.0 * 2.220446049250313e-16 * cmax;
-    const double margin = 2.0 * sqrt((double)dim) * (dev + slack) + 1e-9 * rmin + slack;
-    int R[3] = {0, 0, 0};
-    for (int d = 0; d < dim; ++d) {
-        const double reach = ceil((rmin + margin + spread[d]) / M.h[d]);
-        if (!(reach <= (double)kLatMaxReach)) return TF_OK;
-        R[d] = (int)std::min<int64_t>((int64_t)reach, nd[d] - 1);
-    }
-    int64_t span = 1;
-    for (int d = 0; d < dim; ++d) span *= 2 * R[d] + 1;
-    if (span * M.T * M.T > (int64_t)4 << 20) return TF_OK;
+    double margin = 0.0;
+    int R[3] = {0, 0, 0}, Rb[3] = {0, 0, 0};  // trimmed reach, enumeration bound
+    auto set_bounds = [&](double dv) -> bool {
+        margin = 2.0 * sqrt((double)dim) * (dv + slack) + 1e-9 * rmin + slack;
+        int64_t span = 1;
+        for (int d = 0; d < 3; ++d) Rb[d] = 0;
+        for (int d = 0; d < dim; ++d) {
+            const double reach = ceil((rmin + margin + spread[d]) / M.h[d]);
+            if (!(reach <= (double)kLatMaxReach)) return false;
+            Rb[d] = (int)std::min<int64_t>((int64_t)reach, nd[d] - 1);
+            span *= 2 * Rb[d] + 1;
+        }
+        return span * M.T * M.T <= ((int64_t)4 << 20);
+    };
     const double r2 = rmin * rmin;
-    const int Rb[3] = {R[0], R[1], R[2]};  // enumeration bound
     std::vector<LatEntry> tab;
     LatDev L{};
     L.n = n;
@@ -775,91 +848,117 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
         for (int d = 0; d < 3; ++d) L.R[d] = R[d];
         return true;
     };
-    // exact mode needs the cycle table and the boundary-class masks in shared memory; otherwise
-    // (large reach) the same input is built in tested mode
-    int64_t ncls = 0;
-    int Wc = 0;
-    if (exact) {
-        if (!build_tables(true)) return TF_OK;
-        for (int d = 0; d < 3; ++d) L.C[d] = (d < dim) ? (int)std::min<int64_t>(nd[d], 2 * R[d] + 1) : 1;
-        ncls = (int64_t)L.C[0] * L.C[1] * L.C[2] * M.T;
-        Wc = std::max(1, (maxK + 31) / 32);
-        const int SPx = ((int)tab.size() + 6) & ~3;
-        const size_t need = (size_t)4 * SPx * 12 + (ncls <= (1 << 16) ? LatClasses::smem_bytes((int)ncls, Wc) : SIZE_MAX / 2);
-        if (need > (size_t)160 * 1024) exact = false;
-    }
-    if (!exact) {
-        if (!build_tables(false)) return TF_OK;
-        ncls = 0;
-        Wc = 0;
-    }
-    const auto th0 = std::chrono::steady_clock::now();
-    const int ntab = (int)tab.size();
     // One upload: [tested: the candidate table] or [exact: cycle table (4 shifted copies) +
     // boundary classes]. Exact-mode boundary classes (per axis C_d = min(n_d, 2R_d + 1); see
     // lat_axis_class): each (class, type) list is the type table restricted to the offsets in the
     // grid at a representative position; Hs summed in ascending column order (the oracle's order).
     std::vector<unsigned char> blob;
-    auto put = [&](const void *src, size_t bytes) -> size_t {
-        const size_t at = (blob.size() + 15) & ~(size_t)15;
-        blob.resize(at + bytes);
-        if (bytes) memcpy(blob.data() + at, src, bytes);
-        return at;
-    };
     size_t o_tab = 0, o_ccol = 0, o_cw = 0, o_mask = 0, o_pre = 0, o_len = 0, o_hs = 0;
-    const int SP = (ntab + 3 + 3) & ~3;
-    if (!exact) {
-        o_tab = put(tab.data(), (size_t)ntab * sizeof(LatEntry));
-    } else {
-        std::vector<int32_t> ccol((size_t)4 * SP);
-        std::vector<double> cw((size_t)4 * SP);
-        std::vector<int32_t> seqc(ntab);
-        std::vector<double> seqw(ntab);
-        for (int sty = 0; sty < M.T; ++sty)
-            for (int e = L.kstart[sty]; e < L.kstart[sty + 1]; ++e) seqc[e] = sty + tab[e].delta, seqw[e] = tab[e].w;
-        for (int sh = 0; sh < 4; ++sh)
-            for (int x = 0; x < SP; ++x) {
-                const int p = x + sh;  // extended cycle position
-                ccol[(size_t)sh * SP + x] = seqc[p % ntab] + M.T * (p / ntab);
-                cw[(size_t)sh * SP + x] = seqw[p % ntab];
-            }
-        o_ccol = put(ccol.data(), ccol.size() * sizeof(int32_t));
-        o_cw = put(cw.data(), cw.size() * sizeof(double));
-        auto rep = [&](int cl, int d) -> int64_t {  // a position of class cl on axis d
-            if (nd[d] < 2 * R[d] + 1 || cl <= R[d]) return cl;
-            return nd[d] - 1 - (2 * R[d] - cl);
+    int ntab = 0, SP = 0;
+    int64_t ncls = 0;
+    int Wc = 0;
+    auto make_blob = [&](bool ex) {
+        blob.clear();
+        ntab = (int)tab.size();
+        // One upload: [tested: the candidate table] or [exact: cycle table (4 shifted copies) +
+        // boundary classes]. Exact-mode boundary classes (per axis C_d = min(n_d, 2R_d + 1); see
+        // lat_axis_class): each (class, type) list is the type table restricted to the offsets in the
+        // grid at a representative position; Hs summed in ascending column order (the oracle's order).
+        auto put = [&](const void *src, size_t bytes) -> size_t {
+            const size_t at = (blob.size() + 15) & ~(size_t)15;
+            blob.resize(at + bytes);
+            if (bytes) memcpy(blob.data() + at, src, bytes);
+            return at;
         };
-        std::vector<uint32_t> c_mask((size_t)ncls * Wc, 0u);
-        std::vector<int32_t> c_pre((size_t)ncls * Wc, 0), c_len(ncls, 0);
-        std::vector<double> c_hs(ncls, 0.0);
-        int64_t cid = 0;
-        for (int cz = 0; cz < L.C[2]; ++cz)
-            for (int cy = 0; cy < L.C[1]; ++cy)
-                for (int cx = 0; cx < L.C[0]; ++cx) {
-                    const int64_t pos[3] = {rep(cx, 0), rep(cy, 1), rep(cz, 2)};
-                    for (int sty = 0; sty < M.T; ++sty, ++cid) {
-                        double hsum = 0.0;
-                        int cnt = 0;
-                        for (int e = L.kstart[sty]; e < L.kstart[sty + 1]; ++e) {
-                            const int el = e - L.kstart[sty];
-                            if (el % 32 == 0) c_pre[cid * Wc + el / 32] = cnt;
-                            const int off = tab[e].off;
-                            const int dd[3] = {(off & 255) - 128, ((off >> 8) & 255) - 128, ((off >> 16) & 255) - 128};
-                            bool in = true;
-                            for (int d = 0; d < dim; ++d) in = in && pos[d] + dd[d] >= 0 && pos[d] + dd[d] < nd[d];
-                            if (!in) continue;
-                            c_mask[cid * Wc + el / 32] |= 1u << (el % 32);
-                            hsum += tab[e].w;
-                            ++cnt;
-                        }
-                        c_len[cid] = cnt;
-                        c_hs[cid] = hsum;
-                    }
+        SP = (ntab + 3 + 3) & ~3;
+        if (!ex) {
+            o_tab = put(tab.data(), (size_t)ntab * sizeof(LatEntry));
+        } else {
+            std::vector<int32_t> ccol((size_t)4 * SP);
+            std::vector<double> cw((size_t)4 * SP);
+            std::vector<int32_t> seqc(ntab);
+            std::vector<double> seqw(ntab);
+            for (int sty = 0; sty < M.T; ++sty)
+                for (int e = L.kstart[sty]; e < L.kstart[sty + 1]; ++e) seqc[e] = sty + tab[e].delta, seqw[e] = tab[e].w;
+            for (int sh = 0; sh < 4; ++sh)
+                for (int x = 0; x < SP; ++x) {
+                    const int p = x + sh;  // extended cycle position
+                    ccol[(size_t)sh * SP + x] = seqc[p % ntab] + M.T * (p / ntab);
+                    cw[(size_t)sh * SP + x] = seqw[p % ntab];
                 }
-        o_mask = put(c_mask.data(), c_mask.size() * sizeof(uint32_t));
-        o_pre = put(c_pre.data(), c_pre.size() * sizeof(int32_t));
-        o_len = put(c_len.data(), c_len.size() * sizeof(int32_t));
-        o_hs = put(c_hs.data(), c_hs.size() * sizeof(double));
+            o_ccol = put(ccol.data(), ccol.size() * sizeof(int32_t));
+            o_cw = put(cw.data(), cw.size() * sizeof(double));
+            auto rep = [&](int cl, int d) -> int64_t {  // a position of class cl on axis d
+                if (nd[d] < 2 * R[d] + 1 || cl <= R[d]) return cl;
+                return nd[d] - 1 - (2 * R[d] - cl);
+            };
+            std::vector<uint32_t> c_mask((size_t)ncls * Wc, 0u);
+            std::vector<int32_t> c_pre((size_t)ncls * Wc, 0), c_len(ncls, 0);
+            std::vector<double> c_hs(ncls, 0.0);
+            int64_t cid = 0;
+            for (int cz = 0; cz < L.C[2]; ++cz)
+                for (int cy = 0; cy < L.C[1]; ++cy)
+                    for (int cx = 0; cx < L.C[0]; ++cx) {
+                        const int64_t pos[3] = {rep(cx, 0), rep(cy, 1), rep(cz, 2)};
+                        for (int sty = 0; sty < M.T; ++sty, ++cid) {
+                            double hsum = 0.0;
+                            int cnt = 0;
+                            for (int e = L.kstart[sty]; e < L.kstart[sty + 1]; ++e) {
+                                const int el = e - L.kstart[sty];
+                                if (el % 32 == 0) c_pre[cid * Wc + el / 32] = cnt;
+                                const int off = tab[e].off;
+                                const int dd[3] = {(off & 255) - 128, ((off >> 8) & 255) - 128, ((off >> 16) & 255) - 128};
+                                bool in = true;
+                                for (int d = 0; d < dim; ++d) in = in && pos[d] + dd[d] >= 0 && pos[d] + dd[d] < nd[d];
+                                if (!in) continue;
+                                c_mask[cid * Wc + el / 32] |= 1u << (el % 32);
+                                hsum += tab[e].w;
+                                ++cnt;
+                            }
+                            c_len[cid] = cnt;
+                            c_hs[cid] = hsum;
+                        }
+                    }
+            o_mask = put(c_mask.data(), c_mask.size() * sizeof(uint32_t));
+            o_pre = put(c_pre.data(), c_pre.size() * sizeof(int32_t));
+            o_len = put(c_len.data(), c_len.size() * sizeof(int32_t));
+            o_hs = put(c_hs.data(), c_hs.size() * sizeof(double));
+        }
+    };
+    // exact mode needs the cycle table and the boundary-class masks in shared memory; otherwise
+    // (large reach) the same input is built in tested mode. The exact tables do not depend on the
+    // deviation, so they are built on the host while k_lat_verify runs.
+    const auto th0 = std::chrono::steady_clock::now();
+    const bool spec_ok = set_bounds(0.0) && build_tables(true);
+    bool spec_fits = false;
+    if (spec_ok) {
+        for (int d = 0; d < 3; ++d) L.C[d] = (d < dim) ? (int)std::min<int64_t>(nd[d], 2 * R[d] + 1) : 1;
+        ncls = (int64_t)L.C[0] * L.C[1] * L.C[2] * M.T;
+        Wc = std::max(1, (maxK + 31) / 32);
+        const int SPx = ((int)tab.size() + 6) & ~3;
+        const size_t need = (size_t)4 * SPx * 12 + (ncls <= (1 << 16) ? LatClasses::smem_bytes((int)ncls, Wc) : SIZE_MAX / 2);
+        spec_fits = need <= (size_t)160 * 1024;
+        if (spec_fits) make_blob(true);
+    }
+    unsigned long long vres[2];
+    TF_CUDA_TRY(cudaMemcpyAsync(vres, vout.p, sizeof(vres), cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaStreamSynchronize(s));
+    build_trace().mark("lattice verify + tables", s);
+    if (vres[1] & 1ull) return TF_OK;  // non-finite: the cell-list path reports it
+    double dev;
+    memcpy(&dev, &vres[0], sizeof(dev));
+    double hmin = M.h[0];
+    if (dim >= 2 && M.ny > 1) hmin = std::min(hmin, M.h[1]);
+    if (dim == 3 && M.nz > 1) hmin = std::min(hmin, M.h[2]);
+    if (!(dev <= 0.05 * hmin)) return TF_OK;
+    bool exact = (vres[1] & 2ull) == 0;  // implies dev == 0
+    if (exact && !spec_ok) return TF_OK;
+    if (exact && !spec_fits) exact = false;
+    if (!exact) {
+        if (!set_bounds(dev) || !build_tables(false)) return TF_OK;
+        ncls = 0;
+        Wc = 0;
+        make_blob(false);
     }
     const auto th1 = std::chrono::steady_clock::now();
     DevBuf<unsigned char> dblob;
@@ -873,8 +972,15 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     }
     auto at = [&](size_t o) { return dblob.p + o; };
     const LatEntry *dtab = reinterpret_cast<const LatEntry *>(at(o_tab));
+    // weight-cycle replica for the bulk weight stores: enough for a chunk window starting anywhere
+    // in the cycle (two copies, 16 bytes per entry); off if it would crowd shared memory
+    int LW = ((ntab + 32 * kLatRPL * maxK + 8) + 1) & ~1;
+    if (!exact || (size_t)2 * LW * sizeof(double) > (size_t)96 * 1024) LW = 0;
+#ifdef TF_LAT_NO_BULK
+    LW = 0;
+#endif
     const LatCycle cyc{reinterpret_cast<const int32_t *>(at(o_ccol)), reinterpret_cast<const double *>(at(o_cw)), ntab,
-                       SP};
+                       SP, LW};
     const LatClasses cls{reinterpret_cast<const uint32_t *>(at(o_mask)), reinterpret_cast<const int32_t *>(at(o_pre)),
                          reinterpret_cast<const int32_t *>(at(o_len)), reinterpret_cast<const double *>(at(o_hs)),
                          (int)ncls, Wc};
@@ -896,7 +1002,8 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
         return TF_OK;
     };
     const size_t smem_tab = (size_t)ntab * sizeof(LatEntry);
-    const size_t smem_cyc = (size_t)4 * SP * (sizeof(int32_t) + sizeof(double)) + LatClasses::smem_bytes((int)ncls, Wc);
+    const size_t smem_cyc = (size_t)2 * LW * sizeof(double) + (size_t)4 * SP * (sizeof(int32_t) + sizeof(double)) +
+                            LatClasses::smem_bytes((int)ncls, Wc);
     unsigned grid = 0;
     if (exact) {
         const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 16);
