@@ -308,7 +308,7 @@ def run_ours(args):
     build_path = fb.stats()["path"]
     fb.close()
     t_cl = []
-    for it in range(4):
+    for it in range(0 if args.no_build_cell_list else 4):
         e0, e1 = ev(), ev()
         e0.record(stream)
         fb = tf.tf_build_filter(cd, rmin, path="cell_list")
@@ -363,11 +363,11 @@ def run_ours(args):
                       "gbs": build_bytes(n, nnz, dim) / t_build / 1e9,
                       "frac_of_8tbs": build_bytes(n, nnz, dim) / t_build / 1e9 / HBM_NOMINAL_GBS,
                       "path": build_path if args.build_path == "auto" else args.build_path},
-            "build_cell_list": {"ms": statistics.mean(t_cl) * 1e3, "nnz_per_s": nnz / statistics.mean(t_cl),
-                                "gbs": build_bytes(n, nnz, dim) / statistics.mean(t_cl) / 1e9,
-                                "frac_of_8tbs": build_bytes(n, nnz, dim) / statistics.mean(t_cl) / 1e9
-                                / HBM_NOMINAL_GBS,
-                                "note": "the general path (any centroids), same input, timed after the step loop"},
+            "build_cell_list": None if not t_cl else {
+                "ms": statistics.mean(t_cl) * 1e3, "nnz_per_s": nnz / statistics.mean(t_cl),
+                "gbs": build_bytes(n, nnz, dim) / statistics.mean(t_cl) / 1e9,
+                "frac_of_8tbs": build_bytes(n, nnz, dim) / statistics.mean(t_cl) / 1e9 / HBM_NOMINAL_GBS,
+                "note": "the general path (any centroids), same input, timed after the step loop"},
             "apply": {"sensitivity_us": t_sens * 1e6, "sensitivity_gbs": sens_gbs,
                       "sensitivity_frac_of_8tbs": sens_gbs / HBM_NOMINAL_GBS,
                       "density_us": t_dens * 1e6, "density_gbs": dens_bytes(n, nnz) / t_dens / 1e9,
@@ -462,6 +462,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=200000)
     ap.add_argument("--build-path", choices=["auto", "cell_list", "lattice"], default="auto")
+    ap.add_argument("--no-build-cell-list", action="store_true", help="skip the build_cell_list leg")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: timing rules need --warmup >= 3", file=sys.stderr)

@@ -172,7 +172,9 @@ __global__ void __launch_bounds__(256) k_lat_count_exact(LatDev m, LatClasses cl
         const int i = (int)(cube % (uint32_t)m.nx);
         const uint32_t rr = cube / (uint32_t)m.nx;
         const int j = (int)(rr % (uint32_t)m.ny), k = (int)(rr / (uint32_t)m.ny);
-        counts[r] = cls.len[lat_class_id<DIM>(m, t, i, j, k)];
+        const int cid = lat_class_id<DIM>(m, t, i, j, k);
+        TF_DCHECK(cid >= 0 && cid < cls.ncls);
+        counts[r] = cls.len[cid];
     }
 }
 
@@ -300,6 +302,7 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
                     for (int64_t g = base; g < end; ++g) vals[g] = sw[(P0 + (int)(g - base)) % S];
             }
             const int64_t g0 = (base + 3) & ~(int64_t)3, g1 = end & ~(int64_t)3;
+            TF_DCHECK(end >= base && end - base <= (int64_t)CH * S);
             if (g0 >= g1) {  // no aligned group (tiny tables only)
                 for (int64_t g = base + lane; g < end; g += 32) scalar_at(g, !bulk);
             } else {
@@ -327,6 +330,7 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
 #pragma unroll
                         for (int u = 0; u < U; ++u) {
                             const int shc = cc & 3;
+                            TF_DCHECK(cc >= 0 && cc < S && cc - shc + 4 <= SP);
                             co[u] = *reinterpret_cast<const int4 *>(scol + shc * SP + (cc - shc));
                             rb[u] = (int32_t)(rowc + (int64_t)mc * m.T);
                             cc += 128;
@@ -394,7 +398,9 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
             // a copy of the row's class: the type table entries flagged in its mask, scattered to
             // their ranks (ascending order kept), all from shared memory
             const int cid = lat_class_id<DIM>(m, t, i, j, k);
+            TF_DCHECK(cid >= 0 && cid < cls.ncls);
             const int ks = skst[t], K = skst[t + 1] - ks;
+            TF_DCHECK(ks >= 0 && ks + K <= S && (K + 31) / 32 <= cls.W);
             int32_t *cq = cols + base;
             double *vq = vals + base;
             const int64_t rowc = r - t;
@@ -403,6 +409,7 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
                 const uint32_t word = cmask[wd];
                 if (e0 + lane < K && ((word >> lane) & 1u)) {
                     const int pos = cpre[wd] + __popc(word & lt);
+                    TF_DCHECK(pos >= 0 && base + pos < end);
                     cq[pos] = (int32_t)(rowc + scol[ks + e0 + lane]);
                     vq[pos] = sw[ks + e0 + lane];
                 }
@@ -475,6 +482,7 @@ __global__ void __launch_bounds__(256) k_lat_rows(const double *__restrict__ c, 
                 double d2 = 0.0;
                 if (ok) {
                     const int64_t p = r + en.delta;
+                    TF_DCHECK(p >= 0 && p < m.n);
                     d2 = pair_d2<DIM>(qx, qy, qz, c[p * DIM], c[p * DIM + 1], (DIM == 3) ? c[p * DIM + 2] : 0.0);
                     ok = d2 < m.r2;
                 }
@@ -482,6 +490,7 @@ __global__ void __launch_bounds__(256) k_lat_rows(const double *__restrict__ c, 
                 if (FILL && ok) {
                     const double w = weight_of(m.rmin, d2);
                     const int64_t kk = base + wpos + __popc(bal & lt);
+                    TF_DCHECK(kk < end);
                     cols[kk] = (int32_t)(r + en.delta);
                     vals[kk] = w;
                     hsum += w;

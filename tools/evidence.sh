@@ -10,9 +10,11 @@ timeout 900 python bench.py > gpurun_out/ev_bench.json 2> gpurun_out/ev_bench.er
 kill $SMI
 timeout 900 python bench.py --impl reference > gpurun_out/ev_bench_ref.json 2> gpurun_out/ev_bench_ref.err; echo ref=$?
 timeout 600 python tools/bench_configs.py > gpurun_out/ev_configs.jsonl 2> gpurun_out/ev_configs.err; echo cfg=$?
+# launch list of one step (build + 2 applies), without the build_cell_list leg
+CMDL="python bench.py --steps 1 --warmup 0 --applies 2 --no-e2e --no-cpu-baseline --no-build-cell-list"
+timeout 300 $CMDL > gpurun_out/ev_prof_plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches.csv $CMDL > gpurun_out/ev_ncu_launch.log 2>&1; echo ncu1=$?
 CMD="python bench.py --steps 1 --warmup 0 --applies 2 --no-e2e --no-cpu-baseline"
-timeout 300 $CMD > gpurun_out/ev_prof_plain.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches.csv $CMD > gpurun_out/ev_ncu_launch.log 2>&1; echo ncu1=$?
 # the step's lattice fill and two applies, then the cell-list count and fill (bench's build_cell_list leg)
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_spmv|k_fill|k_count|k_lat_fill_exact" -c 8 -o gpurun_out/ev_prof $CMD > gpurun_out/ev_ncu_full.log 2>&1; echo ncu2=$?
 timeout 300 python tools/helm_probe.py > gpurun_out/ev_helm_probe.log 2>&1 && \

@@ -57,6 +57,8 @@ def main(rnd):
         ncu(["-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{k}", "-c", "1"], src)
         with open(os.path.join(dst, f"{k}_source_hot.txt"), "w") as f:
             subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_source_hot.py"), src], stdout=f, check=True)
+    with open(os.path.join(dst, "sass_evidence.txt"), "w") as f:
+        subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sass_evidence.py")], stdout=f, check=True)
     with open(os.path.join(dst, "launches_summary.txt"), "w") as f:
         subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_summary.py"),
                         os.path.join(dst, "launches.csv")], stdout=f, check=True)
@@ -109,7 +111,7 @@ def main(rnd):
     w(f"* cpu_baseline (oracle, {d['cpu_baseline']['cores']} core, sampled rows): {d['cpu_baseline']['value']:.2f} GB/s; "
       f"reference arm (`--impl reference`, same oracle): {ref['value']:.2f} GB/s")
     w(f"* roofline object: {json.dumps({k: d['roofline'][k] for k in ('kernel', 'bound', 'achieved', 'peak', 'frac', 'traffic')})}\n")
-    w("## Launch list (`launches.csv`, ncu gpu__time_duration, cold/serialised; one build + 2 applies each)\n")
+    w("## Launch list (`launches.csv`, ncu gpu__time_duration, cold/serialised; one step = build + 2 applies)\n")
     w("```")
     w(open(os.path.join(dst, "launches_summary.txt")).read().rstrip())
     w("```\n")
@@ -122,8 +124,9 @@ def main(rnd):
           f"{b['dram__bytes_write.sum']:.3f} GB | {b.get('smsp__issue_active.avg.pct_of_peak_sustained_active', 0):.0f}% | "
           f"{b.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 0):.0f}% |")
     w("\nAlgorithmic bytes per apply launch: sensitivity 12.843 GB, density 12.747 GB (DESIGN.md §4.5). "
-      "SASS evidence (`sass_evidence.txt`): `UBLKCP.S.G` (TMA bulk copies) + `SYNCS.*` (mbarriers) in the apply; "
-      "`FADD2/FMUL2/FFMA2` (packed fp32x2) in count/fill.\n")
+      "SASS evidence (`sass_evidence.txt`): `UBLKCP.S.G` (TMA bulk copies global->shared) + `SYNCS.*` (mbarriers) "
+      "in the apply; `UBLKCP.G.S` (TMA bulk store shared->global of the weights) + `LDS.128`/`STG.E.128` in the "
+      "lattice fill; `FADD2/FMUL2/FFMA2` (packed fp32x2) in the cell-list count/fill.\n")
     w("## All configs (`configs.jsonl`, `tools/bench_configs.py`)\n")
     w("| cfg | N | nnz | build path | build ms | build nnz/s | cell-list build ms | sens cold µs (% of 8 TB/s) | "
       "dens cold µs (% of 8 TB/s) |")
