@@ -6,14 +6,15 @@
 //                Hadamard product, the max floor and the division fused in)
 //   density      out_i = (sum_k vals[k] * x[cols[k]]) / Hs_i   (BASELINE.json north_star)
 //
-// Work split: the nnz stream is cut into windows of kWindow entries; window w owns the rows
+// Work split: the nnz stream is cut into windows of W entries (W = stage capacity minus the
+// longest row, so every window stages; kWindow for short rows); window w owns the rows
 // whose first entry falls in it (row-block table rb[] and 16-byte aligned staging ranges wlo[],
 // built once per filter by make_apply_plan). k_spmv is persistent and warp-specialised:
 //   * a producer warp streams the block's windows (w = blockIdx.x + k*gridDim.x) into a
 //     kStages-deep shared-memory ring with TMA bulk copies (cp.async.bulk, mbarrier
 //     completion, L2 evict_first) of cols/vals/rowptr -- the CSR stream never touches the
 //     LSU/L1 data pipe, which is left to the gathers;
-//   * kCW consumer warps claim 32/G rows at a time from a per-stage counter (dynamic balance),
+//   * kCW consumer warps take groups of 32/G rows, dealt round-robin per window (rotating),
 //     G lanes per row read cols/vals from shared memory, issue U gathers before accumulating,
 //     reduce with a G-lane xor-shuffle tree (deterministic) and write the fused epilogue;
 //   * sensitivity: a cooperative launch first forms t = x o dc (one gather per entry instead of
@@ -59,25 +60,32 @@ constexpr int kThreads = kCW * 32;        // consumer threads
 #define TF_APPLY_WINDOW 2048
 #endif
 #ifndef TF_APPLY_STAGE
-#define TF_APPLY_STAGE 2816
+#define TF_APPLY_STAGE 2976
+#endif
+#ifndef TF_APPLY_DYNWIN
+#define TF_APPLY_DYNWIN 1  // 1: window = stage capacity minus the longest row (all windows staged)
+#endif
+#ifndef TF_APPLY_STATIC
+#define TF_APPLY_STATIC 1  // 1: row groups of a window dealt to the warps round-robin (no atomics)
 #endif
 #ifndef TF_APPLY_ROWCAP
 #define TF_APPLY_ROWCAP 256
 #endif
 constexpr int kWindow = TF_APPLY_WINDOW;  // target nnz per window (row block)
-constexpr int kStage = TF_APPLY_STAGE;    // staged nnz capacity per stage (multiple of 4): 33 KB
+constexpr int kStage = TF_APPLY_STAGE;    // staged nnz capacity per stage (multiple of 4): 35 KB
 constexpr int kRowCap = TF_APPLY_ROWCAP;  // staged rowptr capacity per stage (int64, multiple of 2): 2 KB
 constexpr int kStages = TF_APPLY_STAGES;  // TMA ring depth per block
-constexpr int kBlocksPerSM = TF_APPLY_BPS;  // persistent grid = kBlocksPerSM x SMs (tuned on c5: 10 x 3 x 2 x 2048)
+constexpr int kBlocksPerSM = TF_APPLY_BPS;  // persistent grid = kBlocksPerSM x SMs (tuned on c5: 10 x 3 x 2 x stage 2976)
 
-__global__ void k_plan(const int64_t *__restrict__ rowptr, int64_t n, int64_t nblocks, int32_t *__restrict__ rb) {
+__global__ void k_plan(const int64_t *__restrict__ rowptr, int64_t n, int64_t nblocks, int64_t window,
+                       int32_t *__restrict__ rb) {
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nblocks;
          b += (int64_t)gridDim.x * blockDim.x) {
         if (b == nblocks) {
             rb[b] = (int32_t)n;
             continue;
         }
-        const int64_t target = b * (int64_t)kWindow;
+        const int64_t target = b * window;
         int64_t lo = 0, hi = n;  // first r in [0, n] with rowptr[r] >= target
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
@@ -147,8 +155,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // Persistent, warp-specialised SpMV. Warp kCW (the producer) streams the windows of this
 // block (w = blockIdx.x, + gridDim.x, ...) into a kStages-deep shared-memory ring with TMA
 // bulk copies; full[s] completes when a window's bytes have landed, empty[s] when all kCW
-// consumer warps have left it. Consumer warps claim groups of 32/G rows of the window from a
-// shared counter (dynamic balance, no block-wide barriers); each row is reduced by G lanes
+// consumer warps have left it. Consumer warps take groups of 32/G rows of the window dealt
+// round-robin, rotating by one warp per window (no atomics, no block-wide barriers; a shared
+// counter with TF_APPLY_STATIC=0 measured 3% slower); each row is reduced by G lanes
 // that issue U predicated (col, val) shared loads and U x/dc gathers before accumulating,
 // and the group leader writes out[r] directly.
 // MODE 0: density; 1: sensitivity; 2: both filters in one pass over H (sensitivity -> out,
@@ -273,11 +282,18 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
         const int64_t *sr = srow + st * kRowCap + (r0 - r0a);  // sr[rr] = rowptr[r0 + rr]
         mbar_wait(&full[st], (it / kStages) & 1);
         if (staged) {
+#if TF_APPLY_STATIC
+            // static claims: row group g of this window goes to warp (g + it) mod kCW (the
+            // rotation spreads the short last round over the warps); no shared atomics
+            const int g0 = (warp + kCW - (it % kCW)) % kCW;
+            for (int rbase = g0 * RPW; rbase < R; rbase += kCW * RPW) {
+#else
             for (;;) {
                 int rbase = 0;
                 if (lane == 0) rbase = atomicAdd(&next_row[st], RPW);
                 rbase = __shfl_sync(0xffffffffu, rbase, 0);
                 if (rbase >= R) break;
+#endif
                 const int rr = rbase + lane / G;
                 double acc = 0.0, acc2 = 0.0, hs_r = 1.0, x_r = 1.0;
                 if (rr < R) {
@@ -434,7 +450,7 @@ template <int MODE, int G>
 tf_status launch_spmv_g(const tf_filter_s *h, const double *x, const double *dc, double *out, double *out2,
                         cudaStream_t s, double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf,
                         int tpass) {
-    if (h->plan.unroll >= 8)
+    if ((MODE == 0 ? h->plan.unroll : h->plan.unroll_sens) >= 8)
         return launch_spmv_gu<MODE, G, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
     return launch_spmv_gu<MODE, G, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
 }
@@ -481,10 +497,38 @@ __global__ void k_plan_windows(const int64_t *__restrict__ rowptr, const int32_t
     }
 }
 
+__global__ void k_max_row(const int64_t *__restrict__ rowptr, int64_t n, unsigned long long *__restrict__ out) {
+    unsigned long long m = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, (unsigned long long)(rowptr[r + 1] - rowptr[r]));
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 }  // namespace
 
 tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
-    const int64_t nblocks = std::max<int64_t>(1, (h->nnz + kWindow - 1) / kWindow);
+    // Window (target nnz per row block). A window stages [rowptr[first row], rowptr[last row + 1])
+    // rounded out to 4 entries: at most window + (longest row - 1) + 6 entries. DYNWIN sizes the
+    // window so that every window fits the stage (more bytes per TMA round, no slack).
+    int64_t window = kWindow;
+#if TF_APPLY_DYNWIN
+    {
+        DevBuf<unsigned long long> mr;
+        TF_TRY(mr.alloc(1, s, "apply plan: longest row"));
+        TF_CUDA_TRY(cudaMemsetAsync(mr.p, 0, sizeof(unsigned long long), s));
+        k_max_row<<<(unsigned)std::min<int64_t>((h->n + 255) / 256, 148 * 8), 256, 0, s>>>(h->rowptr, h->n, mr.p);
+        TF_LAUNCH_CHECK();
+        unsigned long long maxrow = 0;
+        TF_CUDA_TRY(cudaMemcpyAsync(&maxrow, mr.p, sizeof(maxrow), cudaMemcpyDeviceToHost, s));
+        TF_CUDA_TRY(cudaStreamSynchronize(s));
+        const int64_t fit = (int64_t)kStage - (int64_t)maxrow - 8;
+        // short rows keep kWindow: the staged rowptr slice (kRowCap rows) bounds the window too
+        const double avg_row = (double)h->nnz / (double)std::max<int64_t>(1, h->n);
+        if (fit >= 256) window = (avg_row >= 16.0 ? fit : std::min<int64_t>(fit, kWindow)) & ~(int64_t)3;
+    }
+#endif
+    const int64_t nblocks = std::max<int64_t>(1, (h->nnz + window - 1) / window);
     if (nblocks >= (int64_t)1 << 31) {
         set_error("apply plan: too many row blocks");
         return TF_ERR_OVERFLOW;
@@ -495,25 +539,26 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
     TF_TRY(device_info(&di));
     h->plan.grid = di.sms * kBlocksPerSM;
     h->plan.nblocks = nblocks;
-    h->plan.block_nnz = kWindow;
+    h->plan.block_nnz = (int)window;
     h->plan.stage_cap = kStage;
-    // lanes per row in the reduction: about 3 entries per lane (wide groups keep the x/dc
-    // gathers of one warp instruction on few cache lines)
-    // lanes per row G ~ avg/6 (G lanes of a warp gather neighbouring columns of one row);
-    // unroll U so that U*G covers ~1.25x the average row in one batch of loads
+    // lanes per row G ~ avg/12 (G lanes of a warp gather neighbouring columns of one row),
+    // U = 8 gathers in flight per lane before accumulating: measured best at c5 (avg 86):
+    // G = 8, U = 8 (U = 4: +3% sensitivity, +2% density; G = 16: +25%)
     const double avg = (double)h->nnz / (double)std::max<int64_t>(1, h->n);
     int g = 1;
-    while (g < 32 && 12.0 * g < avg) g *= 2;  // measured best at c5 (avg 86): G = 8, U = 4
+    while (g < 32 && 12.0 * g < avg) g *= 2;
     h->plan.group = g;
-    h->plan.unroll = (g >= 8) ? 4 : 8;
+    h->plan.unroll = 8;
     // tuning knobs (benchmarks only): TOPOFILT_APPLY_G in {1..32, power of two}, TOPOFILT_APPLY_U in {4, 8}
     if (const char *e = getenv("TOPOFILT_APPLY_G")) {
         const int v = atoi(e);
         if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) h->plan.group = v;
     }
-    if (const char *e = getenv("TOPOFILT_APPLY_U")) h->plan.unroll = atoi(e) >= 8 ? 8 : 4;
+    h->plan.unroll_sens = h->plan.unroll;
+    if (const char *e = getenv("TOPOFILT_APPLY_U")) h->plan.unroll = h->plan.unroll_sens = atoi(e) >= 8 ? 8 : 4;
+    if (const char *e = getenv("TOPOFILT_APPLY_U_SENS")) h->plan.unroll_sens = atoi(e) >= 8 ? 8 : 4;
     const unsigned grid = (unsigned)std::min<int64_t>((nblocks + 256) / 256, 65535);
-    k_plan<<<grid, 256, 0, s>>>(h->rowptr, h->n, nblocks, h->plan.rb);
+    k_plan<<<grid, 256, 0, s>>>(h->rowptr, h->n, nblocks, window, h->plan.rb);
     TF_LAUNCH_CHECK();
     k_plan_windows<<<grid, 256, 0, s>>>(h->rowptr, h->plan.rb, nblocks, h->plan.wlo);
     TF_LAUNCH_CHECK();

@@ -199,7 +199,8 @@ struct ApplyPlan {
     int group = 1;            // lanes per row in the reduction phase (power of two <= 32)
     int64_t *wlo = nullptr;   // [2*nblocks+1] aligned staging window start / end per row block
     int grid = 0;             // persistent grid size
-    int unroll = 4;           // loads in flight per lane in the row loop (4 or 8)
+    int unroll = 4;           // loads in flight per lane in the row loop (4 or 8): density
+    int unroll_sens = 4;      // the same for the sensitivity (and both-filters) launches
     // row-range chunks of the host pipeline: windows [chunk_w[i], chunk_w[i+1]) cover rows
     // [chunk_r[i], chunk_r[i+1])
     int nchunks = -1;  // -1: not computed yet
