@@ -450,7 +450,7 @@ template <int MODE, int G>
 tf_status launch_spmv_g(const tf_filter_s *h, const double *x, const double *dc, double *out, double *out2,
                         cudaStream_t s, double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf,
                         int tpass) {
-    if ((MODE == 0 ? h->plan.unroll : h->plan.unroll_sens) >= 8)
+    if ((MODE == 0 ? h->plan.unroll : MODE == 1 ? h->plan.unroll_sens : h->plan.unroll_both) >= 8)
         return launch_spmv_gu<MODE, G, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
     return launch_spmv_gu<MODE, G, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
 }
@@ -549,6 +549,9 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
     while (g < 32 && 12.0 * g < avg) g *= 2;
     h->plan.group = g;
     h->plan.unroll = 8;
+    // both filters: (t, x) pairs double the gather registers; U = 8 spills at G >= 2, and at
+    // G = 8 U = 4 measured faster than the spilling U = 8 (2.28 vs 2.57 ms, config 5)
+    h->plan.unroll_both = (g >= 8) ? 4 : 8;
     // tuning knobs (benchmarks only): TOPOFILT_APPLY_G in {1..32, power of two}, TOPOFILT_APPLY_U in {4, 8}
     if (const char *e = getenv("TOPOFILT_APPLY_G")) {
         const int v = atoi(e);

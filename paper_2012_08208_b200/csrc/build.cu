@@ -941,13 +941,22 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     h->info.max_candidates = maxC;
     const int hard_cap = 3072;  // fill staging <= ~110 KB of shared memory
     const int cap = (std::max(1, std::min(maxC, hard_cap)) + 63) & ~63;  // multiple of 64 (packed sweeps)
-    const bool wide = (double)n / (double)g.nbins >= 12.0;
+    // warps per count / fill block follow the mean queries per bin (n / bins): a block serves one bin,
+    // so sparse bins want small blocks (config 4, 6.2 per bin: 1 warp, count -12% / fill -8%
+    // vs 2; config 3, 8 per bin: 2 warps; config 5, 20 per bin: 4 warps)
+    const double qpb = (double)n / (double)g.nbins;
+    const bool wide = qpb >= 12.0;
+    const int bw = wide ? 4 : (qpb >= 7.0 ? 2 : 1);
 
     // a5 count
     build_trace().mark("binstats+sync", s);
     NvtxRange r_count("tf_build/a5 count + a6 scan");
-    if (dim == 3) TF_TRY(wide ? (launch_count<3, 4>(P, g, cap, counts.p, s)) : (launch_count<3, 2>(P, g, cap, counts.p, s)));
-    else TF_TRY(wide ? (launch_count<2, 4>(P, g, cap, counts.p, s)) : (launch_count<2, 2>(P, g, cap, counts.p, s)));
+    int cw = bw;  // warps per count block
+    if (const char *e = getenv("TOPOFILT_COUNT_WARPS")) cw = atoi(e);  // tuning knob (benchmarks only)
+    if (dim == 3) TF_TRY(cw >= 4 ? (launch_count<3, 4>(P, g, cap, counts.p, s))
+                         : cw >= 2 ? (launch_count<3, 2>(P, g, cap, counts.p, s)) : (launch_count<3, 1>(P, g, cap, counts.p, s)));
+    else TF_TRY(cw >= 4 ? (launch_count<2, 4>(P, g, cap, counts.p, s))
+                : cw >= 2 ? (launch_count<2, 2>(P, g, cap, counts.p, s)) : (launch_count<2, 1>(P, g, cap, counts.p, s)));
 
     // a6 row pointers + nnz readback
     build_trace().mark("count", s);
@@ -971,16 +980,18 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     DevBuf<int32_t> large_rows;
     build_trace().mark("alloc_csr", s);
     if (maxC > cap) TF_TRY(large_rows.alloc(n, s, "large-neighbourhood rows"));
-    int fw = wide ? 4 : 2;  // warps per fill block (queries of one bin in parallel)
+    int fw = bw;  // warps per fill block (queries of one bin in parallel)
     if (const char *e = getenv("TOPOFILT_FILL_WARPS")) fw = atoi(e);  // tuning knob (benchmarks only)
     if (dim == 3) {
         if (fw >= 8) TF_TRY((launch_fill<3, 8>(P, g, h, cap, large_rows.p, stats.p, s)));
         else if (fw >= 4) TF_TRY((launch_fill<3, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
-        else TF_TRY((launch_fill<3, 2>(P, g, h, cap, large_rows.p, stats.p, s)));
+        else if (fw >= 2) TF_TRY((launch_fill<3, 2>(P, g, h, cap, large_rows.p, stats.p, s)));
+        else TF_TRY((launch_fill<3, 1>(P, g, h, cap, large_rows.p, stats.p, s)));
     } else {
         if (fw >= 8) TF_TRY((launch_fill<2, 8>(P, g, h, cap, large_rows.p, stats.p, s)));
         else if (fw >= 4) TF_TRY((launch_fill<2, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
-        else TF_TRY((launch_fill<2, 2>(P, g, h, cap, large_rows.p, stats.p, s)));
+        else if (fw >= 2) TF_TRY((launch_fill<2, 2>(P, g, h, cap, large_rows.p, stats.p, s)));
+        else TF_TRY((launch_fill<2, 1>(P, g, h, cap, large_rows.p, stats.p, s)));
     }
     build_trace().mark("fill", s);
     if (maxC > cap) {

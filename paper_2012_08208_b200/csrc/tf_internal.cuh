@@ -200,7 +200,8 @@ struct ApplyPlan {
     int64_t *wlo = nullptr;   // [2*nblocks+1] aligned staging window start / end per row block
     int grid = 0;             // persistent grid size
     int unroll = 4;           // loads in flight per lane in the row loop (4 or 8): density
-    int unroll_sens = 4;      // the same for the sensitivity (and both-filters) launches
+    int unroll_sens = 4;      // the same for the sensitivity launches
+    int unroll_both = 4;      // the same for the both-filters launches (16-byte gathers)
     // row-range chunks of the host pipeline: windows [chunk_w[i], chunk_w[i+1]) cover rows
     // [chunk_r[i], chunk_r[i+1])
     int nchunks = -1;  // -1: not computed yet
