@@ -523,9 +523,11 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
         TF_CUDA_TRY(cudaMemcpyAsync(&maxrow, mr.p, sizeof(maxrow), cudaMemcpyDeviceToHost, s));
         TF_CUDA_TRY(cudaStreamSynchronize(s));
         const int64_t fit = (int64_t)kStage - (int64_t)maxrow - 8;
-        // short rows keep kWindow: the staged rowptr slice (kRowCap rows) bounds the window too
+        // short rows keep kWindow (the staged rowptr slice, kRowCap rows, bounds the window
+        // too), and so does a filter whose longest row leaves less than kWindow: its long-row
+        // windows take the unstaged path instead of shrinking every window
         const double avg_row = (double)h->nnz / (double)std::max<int64_t>(1, h->n);
-        if (fit >= 256) window = (avg_row >= 16.0 ? fit : std::min<int64_t>(fit, kWindow)) & ~(int64_t)3;
+        if (fit > kWindow && avg_row >= 16.0) window = fit & ~(int64_t)3;
     }
 #endif
     const int64_t nblocks = std::max<int64_t>(1, (h->nnz + window - 1) / window);

@@ -96,6 +96,28 @@ def test_apply_long_rows_and_ragged(tf):
     compare_applies(f, ref, x, dc, "ragged")
 
 
+@pytest.mark.parametrize("lo,hi,longest", [(20, 120, None), (16, 90, 1000), (60, 100, 2900), (1, 15, 300)])
+def test_apply_window_sizing(tf, lo, hi, longest):
+    """The apply plan sizes its windows from the longest row (stage capacity minus it when rows
+    average >= 16; the fixed window otherwise): enlarged windows, a longest row that keeps the
+    fixed window, a row that barely fits a stage, and short rows -- all against the oracle."""
+    rng = np.random.default_rng(lo * 1000 + hi)
+    n = 20000
+    lens = rng.integers(lo, hi + 1, size=n)
+    if longest is not None:
+        lens[n // 3] = longest
+    rowptr = np.zeros(n + 1, np.int64)
+    rowptr[1:] = np.cumsum(lens)
+    nnz = rowptr[-1]
+    cols = np.concatenate([np.sort(rng.choice(n, size=l, replace=False)) for l in lens]).astype(np.int32)
+    vals = rng.uniform(0, 2, size=nnz)
+    hs = np.add.reduceat(vals, rowptr[:-1])
+    ref = oracle.CSR(rowptr, cols, vals, hs)
+    f = tf.tf_filter_from_csr(rowptr, cols, vals, hs)
+    x, dc = inputs_for(n, 502)
+    compare_applies(f, ref, x, dc, f"windows {lo}-{hi}/{longest}")
+
+
 # ------------------------------------------------------------------ full build parity
 
 @pytest.mark.parametrize("path", ["auto", "cell_list"])
