@@ -29,6 +29,19 @@ def main():
         torch.cuda.synchronize()
         t = (time.perf_counter() - t0) / iters
         print(f"{name}: {8 * n / t / 1e9:.1f} GB/s ({t * 1e3:.2f} ms per {8 * n / 1e6:.0f} MB)")
+    # both directions at once on two streams (the pipeline's upload and download overlap)
+    d2 = torch.empty(n, dtype=torch.float64, device="cuda")
+    su, sd = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        with torch.cuda.stream(su):
+            d.copy_(xp, non_blocking=True)
+        with torch.cuda.stream(sd):
+            od.copy_(d2, non_blocking=True)
+    torch.cuda.synchronize()
+    t = (time.perf_counter() - t0) / iters
+    print(f"h2d+d2h concurrent: {8 * n / t / 1e9:.1f} GB/s each way ({t * 1e3:.2f} ms per {8 * n / 1e6:.0f} MB each)")
     f = tf.tf_build_filter_host(pin(c).numpy(), rmin)
     for _ in range(2):
         tf.tf_filter_iteration_host(f, xp.numpy(), dcp.numpy(), os_.numpy(), od.numpy())
