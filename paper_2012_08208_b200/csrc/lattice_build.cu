@@ -186,7 +186,8 @@ struct LatCycle {
     const double *w;     // [4][SP]
     int S, SP;
     int LW;  // > 0: the weight cycle is replicated to LW entries (two copies, shifted by 0 and 1) in
-             // shared memory and interior chunks store their weights with one TMA bulk copy
+             // shared memory and interior chunks store their weights with TMA bulk copies
+    int LP;  // entries per bulk copy (even); LW >= S + LP, so a copy may start at any cycle position
 };
 
 __device__ __forceinline__ void lat_decode(int64_t r, const LatDev &m, int &t, int &i, int &j, int &k) {
@@ -283,15 +284,18 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
                 if (with_w) vals[g] = sw[cc];
             };
             if (bulk) {
-                // weights: the window [P0, P0 + total) of the periodic weight sequence, one bulk
-                // store of its 16-byte-aligned middle (source copy chosen so both sides align)
+                // weights: the window [P0, P0 + total) of the periodic weight sequence, as bulk
+                // stores of <= LP entries over its 16-byte-aligned middle, one per lane (source
+                // copy chosen per piece so both sides align); a short replica keeps shared memory
+                // small enough for two blocks per SM
                 const int64_t a0 = base + (base & 1), a1 = end & ~(int64_t)1;
-                if (lane == 0 && a1 > a0) {
-                    const int Pa = P0 + (int)(a0 - base), sh = Pa & 1;
-                    TF_DCHECK(Pa - sh + (a1 - a0) <= cy.LW);
-                    const uint32_t src = (uint32_t)__cvta_generic_to_shared(wrep + sh * cy.LW + (Pa - sh));
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(vals + a0),
-                                 "r"(src), "r"((uint32_t)((a1 - a0) * 8))
+                for (int64_t p0 = a0 + (int64_t)lane * cy.LP; p0 < a1; p0 += 32 * (int64_t)cy.LP) {
+                    const int64_t len = (a1 - p0 < cy.LP) ? a1 - p0 : cy.LP;
+                    const int Pp = (P0 + (int)(p0 - base)) % S, sh = Pp & 1;
+                    TF_DCHECK(Pp - sh + len <= cy.LW && (len & 1) == 0);
+                    const uint32_t src = (uint32_t)__cvta_generic_to_shared(wrep + sh * cy.LW + (Pp - sh));
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(vals + p0),
+                                 "r"(src), "r"((uint32_t)(len * 8))
                                  : "memory");
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     issued = true;
@@ -983,13 +987,16 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     const LatEntry *dtab = reinterpret_cast<const LatEntry *>(at(o_tab));
     // weight-cycle replica for the bulk weight stores: enough for a chunk window starting anywhere
     // in the cycle (two copies, 16 bytes per entry); off if it would crowd shared memory
-    int LW = ((ntab + 32 * kLatRPL * maxK + 8) + 1) & ~1;
+    // (pieces of LP entries: the replica needs S + LP entries, not a whole chunk's window -- config
+    // 5: 25 KB instead of 98 KB, which lets two fill blocks share an SM)
+    const int LP = (std::max(1024, (int)ntab) + 1) & ~1;
+    int LW = ((int)ntab + LP + 2 + 1) & ~1;
     if (!exact || (size_t)2 * LW * sizeof(double) > (size_t)96 * 1024) LW = 0;
 #ifdef TF_LAT_NO_BULK
     LW = 0;
 #endif
     const LatCycle cyc{reinterpret_cast<const int32_t *>(at(o_ccol)), reinterpret_cast<const double *>(at(o_cw)), ntab,
-                       SP, LW};
+                       SP, LW, LP};
     const LatClasses cls{reinterpret_cast<const uint32_t *>(at(o_mask)), reinterpret_cast<const int32_t *>(at(o_pre)),
                          reinterpret_cast<const int32_t *>(at(o_len)), reinterpret_cast<const double *>(at(o_hs)),
                          (int)ncls, Wc};
