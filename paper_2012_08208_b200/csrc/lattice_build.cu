@@ -270,12 +270,24 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
         for (int u = 0; u < RPL; ++u) cur_lane[u] = rp_lane[u];
         const int64_t cur_end = rp_end;
         load_rp(task + wstride, rp_lane, rp_end);
-        int t, i, j, k;
-        lat_decode(r0, m, t, i, j, k);
-        const int i_last = i + (t + nr - 1) / m.T;
-        if (i >= m.R[0] && i_last < m.nx - m.R[0] && lat_interior<DIM>(m, i, j, k)) {
-            const int64_t base = __shfl_sync(0xffffffffu, cur_lane[0], 0), end = cur_end;
-            const int64_t rowc = r0 - t;  // first row of the chunk's first cycle
+        // row pointer of task row q (warp-uniform q; q == nr: the task's end)
+        auto rp = [&](int q) -> int64_t {
+            if (q >= nr) return cur_end;
+            int64_t v = 0;
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {  // (warp-uniform slot selection)
+                const int64_t b_u = __shfl_sync(0xffffffffu, cur_lane[u], q & 31);
+                if ((q >> 5) == u) v = b_u;
+            }
+            return v;
+        };
+        // rows [qa, qb) of the task that lie in one x-line of interior cubes: their entries are a
+        // window of the periodic cycle sequence, written flat
+        auto flat = [&](int qa, int qb) {
+            const int64_t base = rp(qa), end = rp(qb);
+            const int64_t rs = r0 + qa;
+            const int cnt = qb - qa, t = (int)((uint32_t)rs % (uint32_t)m.T);
+            const int64_t rowc = rs - t;  // first row of the segment's first cycle
             const int P0 = skst[t];       // cycle position of the chunk's first entry
             auto scalar_at = [&](int64_t g, bool with_w) {  // head / tail entries (small chunk offsets)
                 const int P = P0 + (int)(g - base);
@@ -379,56 +391,79 @@ __global__ void __launch_bounds__(256, TF_LAT_MINB) k_lat_fill_exact(LatDev m, L
                 }
             }
             int expect = 0;
-            for (int q = lane; q < nr; q += 32) {
+            for (int q = lane; q < cnt; q += 32) {
                 const int tl = (t + q) % m.T;
-                hs[r0 + q] = shs[tl];
+                hs[rs + q] = shs[tl];
                 expect += skst[tl + 1] - skst[tl];
             }
             for (int o = 16; o > 0; o >>= 1) expect += __shfl_xor_sync(0xffffffffu, expect, o);
             if (lane == 0 && expect != end - base) atomicOr(flag, 1);
-            continue;
-        }
-        for (int q = 0; q < nr; ++q) {
+        };
+        // rows [qa, qb) one by one: a copy of each row's boundary class
+        auto rows = [&](int qa, int qb) {
+            if (qa >= qb) return;
+            int t, i, j, k;
+            lat_decode(r0 + qa, m, t, i, j, k);
+            int64_t end = rp(qa);
+            for (int q = qa; q < qb; ++q) {
+                const int64_t r = r0 + q;
+                const int64_t base = end;
+                end = rp(q + 1);
+                // a copy of the row's class: the type table entries flagged in its mask, scattered to
+                // their ranks (ascending order kept), all from shared memory
+                const int cid = lat_class_id<DIM>(m, t, i, j, k);
+                TF_DCHECK(cid >= 0 && cid < cls.ncls);
+                const int ks = skst[t], K = skst[t + 1] - ks;
+                TF_DCHECK(ks >= 0 && ks + K <= S && (K + 31) / 32 <= cls.W);
+                int32_t *cq = cols + base;
+                double *vq = vals + base;
+                const int64_t rowc = r - t;
+                for (int e0 = 0; e0 < K; e0 += 32) {
+                    const int wd = cid * cls.W + (e0 >> 5);
+                    const uint32_t word = cmask[wd];
+                    if (e0 + lane < K && ((word >> lane) & 1u)) {
+                        const int pos = cpre[wd] + __popc(word & lt);
+                        TF_DCHECK(pos >= 0 && base + pos < end);
+                        cq[pos] = (int32_t)(rowc + scol[ks + e0 + lane]);
+                        vq[pos] = sw[ks + e0 + lane];
+                    }
+                }
+                if (lane == 0) {
+                    hs[r] = chs[cid];
+                    if (base + clen[cid] != end) atomicOr(flag, 1);
+                }
+                if (++t == m.T) {
+                    t = 0;
+                    if (++i == m.nx) {
+                        i = 0;
+                        if (++j == m.ny) j = 0, ++k;
+                    }
+                }
+            }
+        };
+        // split the task at x-line ends; inside an x-line of interior (j, k), the rows of interior
+        // cubes go flat and only the rows of the R end cubes go row by row (whole tasks went row by
+        // row before whenever any of their rows was a boundary row)
+        for (int q = 0; q < nr;) {
             const int64_t r = r0 + q;
-            int64_t base = 0, nxt = 0;
-#pragma unroll
-            for (int u = 0; u < RPL; ++u) {  // (warp-uniform slot selection)
-                const int64_t b_u = __shfl_sync(0xffffffffu, cur_lane[u], q & 31);
-                const int64_t n_u = __shfl_sync(0xffffffffu, cur_lane[u], (q + 1) & 31);
-                if ((q >> 5) == u) base = b_u;
-                if (((q + 1) >> 5) == u) nxt = n_u;
-            }
-            const int64_t end = (q + 1 < nr) ? nxt : cur_end;
-            // a copy of the row's class: the type table entries flagged in its mask, scattered to
-            // their ranks (ascending order kept), all from shared memory
-            const int cid = lat_class_id<DIM>(m, t, i, j, k);
-            TF_DCHECK(cid >= 0 && cid < cls.ncls);
-            const int ks = skst[t], K = skst[t + 1] - ks;
-            TF_DCHECK(ks >= 0 && ks + K <= S && (K + 31) / 32 <= cls.W);
-            int32_t *cq = cols + base;
-            double *vq = vals + base;
-            const int64_t rowc = r - t;
-            for (int e0 = 0; e0 < K; e0 += 32) {
-                const int wd = cid * cls.W + (e0 >> 5);
-                const uint32_t word = cmask[wd];
-                if (e0 + lane < K && ((word >> lane) & 1u)) {
-                    const int pos = cpre[wd] + __popc(word & lt);
-                    TF_DCHECK(pos >= 0 && base + pos < end);
-                    cq[pos] = (int32_t)(rowc + scol[ks + e0 + lane]);
-                    vq[pos] = sw[ks + e0 + lane];
+            int t, i, j, k;
+            lat_decode(r, m, t, i, j, k);
+            const int64_t lb = r - t - (int64_t)i * m.T;  // first row of the x-line
+            const int qe = (int)((lb + (int64_t)m.nx * m.T - r0 < nr) ? lb + (int64_t)m.nx * m.T - r0 : nr);
+            if (m.nx > 2 * m.R[0] && lat_interior<DIM>(m, m.R[0], j, k)) {
+                const int64_t fa = lb + (int64_t)m.R[0] * m.T - r0, fb = lb + (int64_t)(m.nx - m.R[0]) * m.T - r0;
+                const int qa = (int)(fa > q ? fa : q), qb = (int)(fb < qe ? fb : qe);
+                if (qa < qb) {
+                    rows(q, qa);
+                    flat(qa, qb);
+                    rows(qb, qe);
+                } else {
+                    rows(q, qe);
                 }
+            } else {
+                rows(q, qe);
             }
-            if (lane == 0) {
-                hs[r] = chs[cid];
-                if (base + clen[cid] != end) atomicOr(flag, 1);
-            }
-            if (++t == m.T) {
-                t = 0;
-                if (++i == m.nx) {
-                    i = 0;
-                    if (++j == m.ny) j = 0, ++k;
-                }
-            }
+            q = qe;
         }
     }
     // bulk stores complete (and their shared-memory source stays allocated) before the CTA exits
