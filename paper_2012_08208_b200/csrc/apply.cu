@@ -514,15 +514,19 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
     int64_t window = kWindow;
 #if TF_APPLY_DYNWIN
     {
-        DevBuf<unsigned long long> mr;
-        TF_TRY(mr.alloc(1, s, "apply plan: longest row"));
-        TF_CUDA_TRY(cudaMemsetAsync(mr.p, 0, sizeof(unsigned long long), s));
-        k_max_row<<<(unsigned)std::min<int64_t>((h->n + 255) / 256, 148 * 8), 256, 0, s>>>(h->rowptr, h->n, mr.p);
-        TF_LAUNCH_CHECK();
-        unsigned long long maxrow = 0;
-        TF_CUDA_TRY(cudaMemcpyAsync(&maxrow, mr.p, sizeof(maxrow), cudaMemcpyDeviceToHost, s));
-        TF_CUDA_TRY(cudaStreamSynchronize(s));
-        const int64_t fit = (int64_t)kStage - (int64_t)maxrow - 8;
+        int64_t maxrow = h->max_row_hint;  // known exactly by the lattice build; else one reduction
+        if (maxrow < 0) {
+            DevBuf<unsigned long long> mr;
+            TF_TRY(mr.alloc(1, s, "apply plan: longest row"));
+            TF_CUDA_TRY(cudaMemsetAsync(mr.p, 0, sizeof(unsigned long long), s));
+            k_max_row<<<(unsigned)std::min<int64_t>((h->n + 255) / 256, 148 * 8), 256, 0, s>>>(h->rowptr, h->n, mr.p);
+            TF_LAUNCH_CHECK();
+            unsigned long long m = 0;
+            TF_CUDA_TRY(cudaMemcpyAsync(&m, mr.p, sizeof(m), cudaMemcpyDeviceToHost, s));
+            TF_CUDA_TRY(cudaStreamSynchronize(s));
+            maxrow = (int64_t)m;
+        }
+        const int64_t fit = (int64_t)kStage - maxrow - 8;
         // short rows keep kWindow (the staged rowptr slice, kRowCap rows, bounds the window
         // too), and so does a filter whose longest row leaves less than kWindow: its long-row
         // windows take the unstaged path instead of shrinking every window

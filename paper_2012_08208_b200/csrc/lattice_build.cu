@@ -1108,6 +1108,7 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     for (int d = 0; d < 3; ++d) h->info.bins[d] = nd[d];
     h->info.nbins = M.nx * M.ny * M.nz;
     h->info.max_candidates = maxK;
+    if (exact) h->max_row_hint = maxK;  // exact mode: the longest class list is the longest row
     h->info.large_rows = 0;
     h->info.radix_passes = 0;
     h->info.path = exact ? TF_PATH_LATTICE_EXACT : TF_PATH_LATTICE_TESTED;
