@@ -514,7 +514,7 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
     int64_t window = kWindow;
 #if TF_APPLY_DYNWIN
     {
-        int64_t maxrow = h->max_row_hint;  // known exactly by the lattice build; else one reduction
+        int64_t maxrow = h->max_row_hint;  // known from the build (count pass, lattice tables); else one reduction
         if (maxrow < 0) {
             DevBuf<unsigned long long> mr;
             TF_TRY(mr.alloc(1, s, "apply plan: longest row"));

@@ -293,6 +293,13 @@ __global__ void __launch_bounds__(256) k_binstats(const int32_t *__restrict__ cs
 }
 
 // ------------------------------------------------------------------ a5: count pass
+// Longest row for the apply plan: an atomic only when a row beats the value already seen (the
+// plain read is a cached broadcast; the maximum settles after a few rows, so atomics stay rare).
+// Each warp keeps its own maximum and reports it once per block; a stale cached read only costs
+// an extra atomic.
+__device__ __forceinline__ void note_max(int32_t *m, int v) {
+    if (v > 0 && v > *m) atomicMax(m, v);
+}
 
 // Block per query bin, WARPS warps, one warp per query. The bin's candidates (the 3^(dim-1)
 // contiguous x-triples) are staged once as bin-local fp32 SoA (padded with far sentinels to
@@ -301,7 +308,8 @@ __global__ void __launch_bounds__(256) k_binstats(const int32_t *__restrict__ cs
 // ballot/popc, band pairs are decided by the exact fp64 test. Neighbourhoods over `cap`
 // (or inputs where the fp32 band is unusable) fall back to exact fp64 tests from the SoA.
 template <int DIM, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_count(SortedPts P, Grid g, int cap, int32_t *__restrict__ counts) {
+__global__ void __launch_bounds__(WARPS * 32) k_count(SortedPts P, Grid g, int cap, int32_t *__restrict__ counts,
+                                                       int32_t *__restrict__ maxrow) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int NR = (DIM == 3) ? 9 : 3;
     __shared__ int rs[NR], rp[NR + 1];
@@ -309,6 +317,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_count(SortedPts P, Grid g, int c
     const int q0 = P.cs[b], q1 = P.cs[b + 1];
     if (q0 == q1) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int wmax = 0;  // lane 0: longest row this warp counted
     const BinView v = bin_view(b, g);
     load_ranges<DIM>(v, g, P.cs, rs, rp);
     const int C = rp[NR];
@@ -376,6 +385,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_count(SortedPts P, Grid g, int c
             if (lane == 0) {
                 counts[P.id[q]] = cnt & 0xffff;
                 if (hasb) counts[P.id[qb]] = cnt >> 16;
+                wmax = max(wmax, max(cnt & 0xffff, cnt >> 16));
             }
         }
     } else {
@@ -391,9 +401,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_count(SortedPts P, Grid g, int c
                     cnt += __popc(__ballot_sync(0xffffffffu, ok));
                 }
             }
-            if (lane == 0) counts[P.id[q]] = cnt;
+            if (lane == 0) counts[P.id[q]] = cnt, wmax = max(wmax, cnt);
         }
     }
+    if (lane == 0) note_max(maxrow, wmax);
 }
 
 // ------------------------------------------------------------------ a7: fill pass
@@ -822,12 +833,12 @@ tf_status make_grid(const double *bb, int64_t n, int dim, double rmin, Grid *g) 
 }
 
 template <int DIM, int WARPS>
-tf_status launch_count(const SortedPts &P, const Grid &g, int cap, int32_t *counts, cudaStream_t s) {
+tf_status launch_count(const SortedPts &P, const Grid &g, int cap, int32_t *counts, int32_t *maxrow, cudaStream_t s) {
     const size_t smem = (size_t)cap * (3 * sizeof(float) + sizeof(int32_t));
     auto kern = k_count<DIM, WARPS>;
     // always set: dynamic + static shared memory above 48 KB needs the opt-in attribute
     TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)g.nbins, WARPS * 32, smem, s>>>(P, g, cap, counts);
+    kern<<<(unsigned)g.nbins, WARPS * 32, smem, s>>>(P, g, cap, counts, maxrow);
     TF_LAUNCH_CHECK();
     return TF_OK;
 }
@@ -953,23 +964,26 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     NvtxRange r_count("tf_build/a5 count + a6 scan");
     int cw = bw;  // warps per count block
     if (const char *e = getenv("TOPOFILT_COUNT_WARPS")) cw = atoi(e);  // tuning knob (benchmarks only)
-    if (dim == 3) TF_TRY(cw >= 4 ? (launch_count<3, 4>(P, g, cap, counts.p, s))
-                         : cw >= 2 ? (launch_count<3, 2>(P, g, cap, counts.p, s)) : (launch_count<3, 1>(P, g, cap, counts.p, s)));
-    else TF_TRY(cw >= 4 ? (launch_count<2, 4>(P, g, cap, counts.p, s))
-                : cw >= 2 ? (launch_count<2, 2>(P, g, cap, counts.p, s)) : (launch_count<2, 1>(P, g, cap, counts.p, s)));
+    if (dim == 3) TF_TRY(cw >= 4 ? (launch_count<3, 4>(P, g, cap, counts.p, stats.p + 3, s))
+                         : cw >= 2 ? (launch_count<3, 2>(P, g, cap, counts.p, stats.p + 3, s)) : (launch_count<3, 1>(P, g, cap, counts.p, stats.p + 3, s)));
+    else TF_TRY(cw >= 4 ? (launch_count<2, 4>(P, g, cap, counts.p, stats.p + 3, s))
+                : cw >= 2 ? (launch_count<2, 2>(P, g, cap, counts.p, stats.p + 3, s)) : (launch_count<2, 1>(P, g, cap, counts.p, stats.p + 3, s)));
 
     // a6 row pointers + nnz readback
     build_trace().mark("count", s);
     TF_TRY(dalloc(&h->rowptr, n + 3, s, "rowptr (+2 padding for 16-byte bulk copies)"));
     TF_TRY(exclusive_scan_i32_i64(counts.p, h->rowptr, n, s));
     int64_t nnz = 0;
+    int32_t maxrow = 0;  // longest row (count pass), for the apply plan's window size
     TF_CUDA_TRY(cudaMemcpyAsync(&nnz, h->rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaMemcpyAsync(&maxrow, stats.p + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     TF_CUDA_TRY(cudaStreamSynchronize(s));
     if (nnz < n || nnz < 0) {
         set_error("internal: nnz %lld < n %lld", (long long)nnz, (long long)n);
         return TF_ERR_CUDA;
     }
     h->nnz = nnz;
+    h->max_row_hint = maxrow;
 
     // a7 fill
     build_trace().mark("scan+sync", s);

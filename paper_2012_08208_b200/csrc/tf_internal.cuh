@@ -247,7 +247,7 @@ struct tf_filter_s {
     double *hs = nullptr;
     tf::ApplyPlan plan;
     bool cols_ascending = false;  // set by the library's own build (tf_filter_from_csr: unknown)
-    int64_t max_row_hint = -1;    // longest row when the build knows it exactly (lattice exact mode)
+    int64_t max_row_hint = -1;    // longest row when the build knows it (count pass, lattice exact tables)
     tf_build_info info{};
     // host-API scratch (lazily allocated, owned) + a side stream / event for copy overlap
     double *hx = nullptr, *hdc = nullptr, *hout = nullptr, *hout2 = nullptr, *ht = nullptr;
