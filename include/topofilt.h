@@ -215,6 +215,17 @@ TF_API tf_status tf_sensitivity_filter_energy(tf_filter h, const double *x, cons
 /* tf_density_filter -- out_i = (sum_j W_ij x_j) / Hs_i. Same conventions. */
 TF_API tf_status tf_density_filter(tf_filter h, const double *x, double *out, void *stream);
 
+/* tf_sensitivity_filter_rows / tf_density_filter_rows -- the same filters for rows [0, nrows)
+ * only (NEXT-4: a shard's local filter lists its owned rows first and its halo
+ * rows after; only the owned rows are wanted). out[i] for i < nrows equals the full call's,
+ * bitwise; out[i] for i >= nrows is unspecified (the last row block may write it). x (and dc)
+ * are read at every column, so they must hold all n entries. out, x, dc: device fp64 [n].
+ * 0 <= nrows <= n (TF_ERR_INVALID otherwise; nrows = 0: no-op). Asynchronous on `stream`.
+ * Stencil handles compute all rows. */
+TF_API tf_status tf_sensitivity_filter_rows(tf_filter h, const double *x, const double *dc, double *out,
+                                            int64_t nrows, void *stream);
+TF_API tf_status tf_density_filter_rows(tf_filter h, const double *x, double *out, int64_t nrows, void *stream);
+
 /* tf_filter_both -- both filters of one iteration in ONE pass over H (the CSR streams from HBM
  * once; each entry gathers t_j = x_j*dc_j and x_j): sens_out as tf_sensitivity_filter,
  * dens_out as tf_density_filter, bitwise (same per-row summation order).

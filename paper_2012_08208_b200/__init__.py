@@ -29,6 +29,7 @@ EXPORTS = [
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
     "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update", "tf_sensitivity_filter_energy",
     "tf_filter_iteration_host", "tf_filter_both", "tf_build_lattice", "tf_halo_pack",
+    "tf_sensitivity_filter_rows", "tf_density_filter_rows",
     # include/topofilt_helmholtz.h (NEXT-3)
     "tf_helmholtz_build", "tf_helmholtz_filter", "tf_helmholtz_sensitivity", "tf_helmholtz_view",
     "tf_helmholtz_free",
@@ -85,6 +86,8 @@ def _load():
         "tf_build_stats": ([P, ctypes.POINTER(tf_build_info)], I32),
         "tf_sensitivity_filter": ([P, P, P, P, P], I32),
         "tf_density_filter": ([P, P, P, P], I32),
+        "tf_sensitivity_filter_rows": ([P, P, P, P, I64, P], I32),
+        "tf_density_filter_rows": ([P, P, P, I64, P], I32),
         "tf_sensitivity_filter_host": ([P, P, P, P, P], I32),
         "tf_density_filter_host": ([P, P, P, P], I32),
         "tf_filter_from_csr": ([P, P, P, P, I64, P, PP], I32),
@@ -179,20 +182,27 @@ class Filter:
             raise ValueError("filter is closed")
         return self._h
 
-    def sensitivity(self, x, dc, out=None, stream=None):
-        """dc~ = H(x∘dc) / (Hs∘max(1e-3, x)) (PAPER.md:447; Eq. filter_mat)."""
+    def sensitivity(self, x, dc, out=None, stream=None, rows=None):
+        """dc~ = H(x∘dc) / (Hs∘max(1e-3, x)) (PAPER.md:447; Eq. filter_mat).
+        rows: only rows [0, rows) are guaranteed (tf_sensitivity_filter_rows)."""
         import torch
         if out is None:
             out = torch.empty_like(x)
-        tf_sensitivity_filter(self, x, dc, out, stream)
+        if rows is None:
+            tf_sensitivity_filter(self, x, dc, out, stream)
+        else:
+            tf_sensitivity_filter_rows(self, x, dc, out, rows, stream)
         return out
 
-    def density(self, x, out=None, stream=None):
-        """x~ = Hx / Hs (BASELINE.json north_star)."""
+    def density(self, x, out=None, stream=None, rows=None):
+        """x~ = Hx / Hs (BASELINE.json north_star). rows: as in sensitivity."""
         import torch
         if out is None:
             out = torch.empty_like(x)
-        tf_density_filter(self, x, out, stream)
+        if rows is None:
+            tf_density_filter(self, x, out, stream)
+        else:
+            tf_density_filter_rows(self, x, out, rows, stream)
         return out
 
     def both(self, x, dc, sens_out=None, dens_out=None, stream=None):
@@ -339,6 +349,23 @@ def tf_filter_both(f: Filter, x, dc, sens_out=None, dens_out=None, stream=None):
                                _dptr(sens_out, "sens_out", torch.float64, f.n),
                                _dptr(dens_out, "dens_out", torch.float64, f.n), _stream_ptr(stream)))
     return sens_out, dens_out
+
+
+def tf_sensitivity_filter_rows(f: Filter, x, dc, out, nrows: int, stream=None):
+    """Rows [0, nrows) of the sensitivity filter (NEXT-4: a shard's owned rows)."""
+    import torch
+    _check(_lib.tf_sensitivity_filter_rows(f.handle, _dptr(x, "x", torch.float64, f.n),
+                                           _dptr(dc, "dc", torch.float64, f.n),
+                                           _dptr(out, "out", torch.float64, f.n), int(nrows), _stream_ptr(stream)))
+    return out
+
+
+def tf_density_filter_rows(f: Filter, x, out, nrows: int, stream=None):
+    """Rows [0, nrows) of the density filter."""
+    import torch
+    _check(_lib.tf_density_filter_rows(f.handle, _dptr(x, "x", torch.float64, f.n),
+                                       _dptr(out, "out", torch.float64, f.n), int(nrows), _stream_ptr(stream)))
+    return out
 
 
 def tf_density_filter(f: Filter, x, out, stream=None):

@@ -477,6 +477,27 @@ tf_status tf_density_filter(tf_filter h, const double *x, double *out, void *str
     return launch_density(h, x, out, (cudaStream_t)stream);
 }
 
+tf_status tf_sensitivity_filter_rows(tf_filter h, const double *x, const double *dc, double *out, int64_t nrows,
+                                     void *stream) {
+    TF_TRY(check_apply(h, x, dc, out, true));
+    if (nrows < 0 || nrows > h->n) {
+        set_error("nrows %lld outside [0, n = %lld]", (long long)nrows, (long long)h->n);
+        return TF_ERR_INVALID;
+    }
+    if (nrows == 0) return TF_OK;
+    return launch_sensitivity_rows(h, x, dc, out, nrows, (cudaStream_t)stream);
+}
+
+tf_status tf_density_filter_rows(tf_filter h, const double *x, double *out, int64_t nrows, void *stream) {
+    TF_TRY(check_apply(h, x, nullptr, out, false));
+    if (nrows < 0 || nrows > h->n) {
+        set_error("nrows %lld outside [0, n = %lld]", (long long)nrows, (long long)h->n);
+        return TF_ERR_INVALID;
+    }
+    if (nrows == 0) return TF_OK;
+    return launch_density_rows(h, x, out, nrows, (cudaStream_t)stream);
+}
+
 tf_status tf_filter_both(tf_filter h, const double *x, const double *dc, double *sens_out, double *dens_out,
                          void *stream) {
     TF_TRY(check_apply(h, x, dc, sens_out, true));

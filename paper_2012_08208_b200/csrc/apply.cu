@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                                                                       const int64_t *__restrict__ wlo,
                                                                       int64_t nwin, double *tbuf, int64_t n,
                                                                       double penal, int energy, int64_t wbeg,
-                                                                      int64_t wend, int tpass) {
+                                                                      int64_t wend, int tpass, int64_t row_limit) {
     constexpr bool SENS = MODE != 0, BOTH = MODE == 2;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *svals = reinterpret_cast<double *>(smem_raw);                           // [kStages][kStage]
@@ -227,13 +227,13 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
         };
         // prologue: the first kStages windows need no empty-wait (overlaps the t pass)
         if (lane == 0)
-            for (; w < wend && it < kStages; w += gridDim.x, ++it) issue(it);
+            for (; w < wend && rb[w] < row_limit && it < kStages; w += gridDim.x, ++it) issue(it);
         if (SENS && tpass) {
             __syncwarp();
             cooperative_groups::this_grid().sync();
         }
         if (lane == 0)
-            for (; w < wend; w += gridDim.x, ++it) {
+            for (; w < wend && rb[w] < row_limit; w += gridDim.x, ++it) {
                 const int st = it % kStages;
                 mbar_wait_sleep(&empty[st], ((it / kStages) - 1) & 1);
                 issue(st);
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
     constexpr int RPW = 32 / G;  // rows per warp claim
     const int sub = lane & (G - 1);
     int it = 0;
-    for (int64_t w = wbeg + blockIdx.x; w < wend; w += gridDim.x, ++it) {
+    for (int64_t w = wbeg + blockIdx.x; w < wend && rb[w] < row_limit; w += gridDim.x, ++it) {
         const int st = it % kStages;
         const int r0 = rb[w], R = rb[w + 1] - r0;
         const int64_t a = wlo[w], n4 = wlo[w + 1 + nwin] - a;
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
 template <int MODE, int G, int U>
 tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc, double *out, double *out2,
                          cudaStream_t s, double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf_ext,
-                         int tpass) {
+                         int tpass, int64_t row_limit) {
     constexpr bool SENS = MODE != 0;
     const size_t smem = (size_t)kStages * (kStage * (sizeof(double) + sizeof(int32_t)) + kRowCap * sizeof(int64_t));
     auto kern = k_spmv<MODE, G, U>;
@@ -430,7 +430,7 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
                         (void *)&dc,     (void *)&out,  (void *)&out2,  (void *)&rb,     (void *)&wlo,
                         (void *)&nwin,
                         (void *)&tbuf,   (void *)&n,    (void *)&penal, (void *)&energy, (void *)&wbeg,
-                        (void *)&wend,   (void *)&tpass};
+                        (void *)&wend,   (void *)&tpass, (void *)&row_limit};
         cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads + 32), args, smem, s);
         count_launch();
         if (!tbuf_ext) dev_free(tbuf, s);
@@ -441,7 +441,7 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
         return TF_OK;
     }
     kern<<<grid, kThreads + 32, smem, s>>>(rowptr, cols, vals, hs, x, dc, out, out2, rb, wlo, nwin, tbuf, n, penal,
-                                           energy, wbeg, wend, 0);
+                                           energy, wbeg, wend, 0, row_limit);
     TF_LAUNCH_CHECK();
     return TF_OK;
 }
@@ -449,24 +449,25 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
 template <int MODE, int G>
 tf_status launch_spmv_g(const tf_filter_s *h, const double *x, const double *dc, double *out, double *out2,
                         cudaStream_t s, double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf,
-                        int tpass) {
+                        int tpass, int64_t row_limit) {
     if ((MODE == 0 ? h->plan.unroll : MODE == 1 ? h->plan.unroll_sens : h->plan.unroll_both) >= 8)
-        return launch_spmv_gu<MODE, G, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
-    return launch_spmv_gu<MODE, G, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
+        return launch_spmv_gu<MODE, G, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
+    return launch_spmv_gu<MODE, G, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
 }
 
 template <int MODE>
 tf_status launch_spmv(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s,
                       double penal = 0.0, int energy = 0, int64_t wbeg = 0, int64_t wend = -1,
-                      double *tbuf = nullptr, int tpass = 1, double *out2 = nullptr) {
+                      double *tbuf = nullptr, int tpass = 1, double *out2 = nullptr,
+                      int64_t row_limit = INT64_MAX) {
     if (wend < 0) wend = h->plan.nblocks;
     switch (h->plan.group) {
-        case 1: return launch_spmv_g<MODE, 1>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
-        case 2: return launch_spmv_g<MODE, 2>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
-        case 4: return launch_spmv_g<MODE, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
-        case 8: return launch_spmv_g<MODE, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
-        case 16: return launch_spmv_g<MODE, 16>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
-        default: return launch_spmv_g<MODE, 32>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass);
+        case 1: return launch_spmv_g<MODE, 1>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
+        case 2: return launch_spmv_g<MODE, 2>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
+        case 4: return launch_spmv_g<MODE, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
+        case 8: return launch_spmv_g<MODE, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
+        case 16: return launch_spmv_g<MODE, 16>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
+        default: return launch_spmv_g<MODE, 32>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
     }
 }
 
@@ -670,6 +671,22 @@ tf_status launch_both(const tf_filter_s *h, const double *x, const double *dc, d
         return launch_stencil(h, x, nullptr, dens_out, false, s);
     }
     return launch_spmv<2>(h, x, dc, sens_out, s, 0.0, 0, 0, -1, nullptr, 1, dens_out);
+}
+
+// Rows [0, nrows) only (windows whose first row is below nrows; rows of the last such window
+// past nrows are computed too). The sensitivity t pass still covers all n entries: the kept
+// rows read columns anywhere. Stencil handles run whole.
+tf_status launch_sensitivity_rows(const tf_filter_s *h, const double *x, const double *dc, double *out,
+                                  int64_t nrows, cudaStream_t s) {
+    NvtxRange r("tf_apply/sensitivity_rows");
+    if (h->stencil.K > 0) return launch_stencil(h, x, dc, out, true, s);
+    return launch_spmv<1>(h, x, dc, out, s, 0.0, 0, 0, -1, nullptr, 1, nullptr, nrows);
+}
+
+tf_status launch_density_rows(const tf_filter_s *h, const double *x, double *out, int64_t nrows, cudaStream_t s) {
+    NvtxRange r("tf_apply/density_rows");
+    if (h->stencil.K > 0) return launch_stencil(h, x, nullptr, out, false, s);
+    return launch_spmv<0>(h, x, nullptr, out, s, 0.0, 0, 0, -1, nullptr, 1, nullptr, nrows);
 }
 
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s) {

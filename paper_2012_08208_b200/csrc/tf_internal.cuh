@@ -301,6 +301,9 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s);
 tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double *dc, double *out,
                              cudaStream_t s);
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s);
+tf_status launch_sensitivity_rows(const tf_filter_s *h, const double *x, const double *dc, double *out,
+                                  int64_t nrows, cudaStream_t s);
+tf_status launch_density_rows(const tf_filter_s *h, const double *x, double *out, int64_t nrows, cudaStream_t s);
 // both filters in one pass over H (sensitivity -> sens_out, density -> dens_out)
 tf_status launch_both(const tf_filter_s *h, const double *x, const double *dc, double *sens_out, double *dens_out,
                       cudaStream_t s);

@@ -12,7 +12,8 @@ ranks.
 Per apply: pack the owned values each other rank needs (tf_halo_pack, a library kernel),
 exchange them point-to-point (torch.distributed batch_isend_irecv: NCCL over NVLink/NVSwitch
 on GPUs; x and dc land directly in the halo tail of the local vectors, no unpack), run the
-library filter on the local vectors, and return the owned rows. The exchange is the path's one
+library filter's owned rows (tf_*_filter_rows: the local order puts them first) on the local
+vectors, and return them. The exchange is the path's one
 real collective step; everything else is the single-GPU library.
 """
 from __future__ import annotations
@@ -177,12 +178,12 @@ class ShardedFilter:
     def sensitivity(self, x_owned, dc_owned):
         """Owned rows of the sensitivity filter (Eq. filter)."""
         self._exchange(x_owned, dc_owned)
-        self.filter.sensitivity(self.x_loc, self.dc_loc, out=self.out_loc)
+        self.filter.sensitivity(self.x_loc, self.dc_loc, out=self.out_loc, rows=self.plan.n_owned)
         return self.out_loc[:self.plan.n_owned]
 
     def density(self, x_owned):
         self._exchange(x_owned, None)
-        self.filter.density(self.x_loc, out=self.out_loc)
+        self.filter.density(self.x_loc, out=self.out_loc, rows=self.plan.n_owned)
         return self.out_loc[:self.plan.n_owned]
 
     def apply_with_halo(self, x_owned, dc_owned, received: dict, density: bool = False):
@@ -191,10 +192,11 @@ class ShardedFilter:
         for j, bufs in received.items():
             for dstv, b in zip(self.recv_views(dc_owned is not None)[j], bufs):
                 dstv.copy_(b)
+        n = self.plan.n_owned  # the owned rows come first in the local order; halo rows are not needed
         if density:
-            self.filter.density(self.x_loc, out=self.out_loc)
+            self.filter.density(self.x_loc, out=self.out_loc, rows=n)
         else:
-            self.filter.sensitivity(self.x_loc, self.dc_loc, out=self.out_loc)
+            self.filter.sensitivity(self.x_loc, self.dc_loc, out=self.out_loc, rows=n)
         return self.out_loc[:self.plan.n_owned]
 
     def close(self):

@@ -386,6 +386,47 @@ def test_filter_both_bitwise(tf, case):
         f.both(xd, dcd, sens_out=o, dens_out=o)
 
 
+@pytest.mark.parametrize("case", ["c4", "ragged_long_rows", "stencil_c3"])
+def test_filter_rows_prefix(tf, case):
+    """tf_*_filter_rows: rows [0, nrows) bitwise equal to the full call for nrows at 0, 1, a window
+    boundary neighbourhood, mid and n (incl. the unstaged long-row windows); out-of-range nrows
+    is TF_ERR_INVALID."""
+    if case == "ragged_long_rows":
+        rng = np.random.default_rng(19)
+        n = 6000
+        lens = rng.integers(1, 40, size=n)
+        lens[[10, 3000]] = [12000, 7000]
+        rowptr = np.zeros(n + 1, np.int64)
+        rowptr[1:] = np.cumsum(lens)
+        cols = np.concatenate([np.sort(rng.choice(n, size=l, replace=l > n)) for l in lens]).astype(np.int32)
+        vals = rng.uniform(0, 2, size=rowptr[-1])
+        hs = np.add.reduceat(vals, rowptr[:-1])
+        f = tf.tf_filter_from_csr(rowptr, cols, vals, hs)
+        x, dc = inputs_for(n, 616)
+    elif case == "stencil_c3":
+        c, x, dc, rmin = synth.workload(3)
+        f = tf.tf_build_stencil(3, 160, 80, 80, 1.0, rmin)
+    else:
+        c, x, dc, rmin = synth.workload(4)
+        f = tf.tf_build_filter(dev(c), rmin)
+    n = f.n
+    xd, dcd = dev(x), dev(dc)
+    full_s, full_d = f.sensitivity(xd, dcd), f.density(xd)
+    for nrows in sorted({0, 1, 2047, 2048, 2049, 3001, n // 2 + 7, n - 1, n}):
+        s = torch.full_like(xd, float("nan"))
+        d = torch.full_like(xd, float("nan"))
+        f.sensitivity(xd, dcd, out=s, rows=nrows)
+        f.density(xd, out=d, rows=nrows)
+        assert torch.equal(s[:nrows], full_s[:nrows]), (case, nrows)
+        assert torch.equal(d[:nrows], full_d[:nrows]), (case, nrows)
+    o = torch.empty_like(xd)
+    for bad in (-1, n + 1):
+        with pytest.raises(tf.TopofiltError):
+            f.sensitivity(xd, dcd, out=o, rows=bad)
+        with pytest.raises(tf.TopofiltError):
+            f.density(xd, out=o, rows=bad)
+
+
 def test_streams_concurrent_applies(tf):
     c, x, dc, rmin = synth.workload(3)
     f = tf.tf_build_filter(dev(c), rmin)

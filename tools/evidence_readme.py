@@ -193,6 +193,18 @@ def main(rnd):
             f"{b['name'].split('(')[0].split('::')[-1]}: {b['gpu__time_duration.sum']:.1f} "
             f"{b['gpu__time_duration.sum_unit']}, DRAM {b['dram__bytes_read.sum']:.1f} "
             f"{b['dram__bytes_read.sum_unit']} read" for b in mb) + " (vs the stored-CSR k_spmv sensitivity above).\n")
+    sp = os.path.join(EV, "ev_shard_probe.jsonl")
+    if os.path.exists(sp):
+        shutil.copy(sp, os.path.join(dst, "shard_probe.jsonl"))
+        rows = [json.loads(l) for l in open(sp) if l.strip()]
+        one = next(r for r in rows if r["world"] == 1)
+        w("NEXT-4 slab sharding, projected (`shard_probe.jsonl`, `tools/shard_probe.py`; config 5, the middle "
+          "rank's owned-row applies measured on one B200, the halo exchange projected at 770 GB/s, not "
+          f"overlapped): 1 GPU {one['sens_us'] + one['dens_us']:.0f} µs per iteration; " + "; ".join(
+              f"{r['world']} ranks: {r['iteration_us_projected']:.0f} µs ({r['speedup_projected_vs_1gpu']:.2f}×; "
+              f"halo {100 * r['halo_frac']:.0f}% of owned, {r['halo_mb_per_sens_apply']:.1f} MB per apply; "
+              f"all local rows {r['sens_us_all_local_rows'] + r['dens_us_all_local_rows']:.0f} vs owned rows "
+              f"{r['sens_us'] + r['dens_us']:.0f} µs)" for r in rows if r["world"] > 1) + ".\n")
     probe = os.path.join(EV, "ev_helm_probe.log")
     if os.path.exists(probe):
         shutil.copy(probe, os.path.join(dst, "helm_probe.log"))
