@@ -97,8 +97,7 @@ __global__ void k_lat_probe(const double *__restrict__ c, int dim, const int64_t
 
 // out[0] = max deviation (bits of a non-negative double), out[1] = flags (1: non-finite, 2: not
 // exact: some coordinate is off the 2^-e grid, beyond 2^50 quanta, or not exactly the model value).
-// Block-stride over the rows of cubes (j, k known per row); threads over the row's T*nx*DIM
-// coordinates, read coalesced.
+// Block-stride over the rows of cubes (j, k known per row); threads over the row's T*nx points.
 template <int DIM>
 __global__ void __launch_bounds__(256) k_lat_verify(const double *__restrict__ c, int64_t n, LatVerifyArgs a,
                                                     unsigned long long *__restrict__ out) {
@@ -115,16 +114,21 @@ __global__ void __launch_bounds__(256) k_lat_verify(const double *__restrict__ c
     for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
         const uint32_t jj = (uint32_t)(row % a.ny), kk = (uint32_t)(row / a.ny);
         const double *cr = c + row * elems;
-        for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) {
-            const uint32_t p = (uint32_t)(e / DIM), d = (uint32_t)(e - (int64_t)p * DIM);
-            const uint32_t t = p % (uint32_t)a.T, i = p / (uint32_t)a.T;
-            const uint32_t idx = (d == 0) ? i : (d == 1 ? jj : kk);
-            const double v = cr[e];
-            const double L = fma((double)idx, shh[d], sc0[t][d]);
-            if (!isfinite(v)) flags |= 1u;
-            dev = fmax(dev, fabs(v - L));
-            const double s = v * a.q;
-            if (!(a.q > 0.0 && s == rint(s) && fabs(s) <= 1125899906842624.0 && v == L)) flags |= 2u;
+        // thread per point (one 32-bit division per point, the DIM coordinates from one 8*DIM-byte
+        // span: a warp's loads cover the row's bytes contiguously)
+        for (uint32_t p = threadIdx.x; p < (uint32_t)rowlen; p += blockDim.x) {
+            const uint32_t i = p / (uint32_t)a.T, t = p - i * (uint32_t)a.T;
+            const double *cp = cr + (int64_t)p * DIM;
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) {
+                const uint32_t idx = (d == 0) ? i : (d == 1 ? jj : kk);
+                const double v = cp[d];
+                const double L = fma((double)idx, shh[d], sc0[t][d]);
+                if (!isfinite(v)) flags |= 1u;
+                dev = fmax(dev, fabs(v - L));
+                const double s = v * a.q;
+                if (!(a.q > 0.0 && s == rint(s) && fabs(s) <= 1125899906842624.0 && v == L)) flags |= 2u;
+            }
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
