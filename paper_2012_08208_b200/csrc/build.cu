@@ -32,6 +32,7 @@
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -709,6 +710,126 @@ __global__ void TF_FILL_BOUNDS k_fill(SortedPts P, Grid g, const int64_t *__rest
     }
 }
 
+// ------------------------------------------------------------------ a7 fill for short rows
+// Warp per query (sorted order, so the warps of a block share their bins through L1), used
+// when the longest row (count pass) is <= 32*KS. No staging and no block sort: every candidate
+// of the 3^(dim-1) x-triples takes the exact fp64 test (pair_d2, the count pass's exact
+// expression on the same bytes, so the accepted set equals the counted one), the accepted
+// (id, d2) pairs are compacted into a per-warp list, and each entry's place in the ascending
+// row is its rank among the row's (distinct) ids: rank = #{ids < id}, counted against the list
+// four ids per shared load. Rows are a few dozen entries, so the O(K^2/32) rank costs less
+// than staging + sorting the bin's candidates -- estimated; measured 1.4x slower than k_fill at
+// configs 3 and 4 (issue-bound: the rank loop is 31% of the instructions, the query's bin
+// decode 7%), so it is opt-in (TOPOFILT_FILL=warp) and kept parity-tested.
+constexpr int kFillWarpWarps = 8;
+
+template <int DIM, int KS>
+__global__ void __launch_bounds__(kFillWarpWarps * 32)
+    k_fill_warp(SortedPts P, const uint32_t *__restrict__ keys, Grid g, int64_t n,
+                const int64_t *__restrict__ rowptr, int32_t *__restrict__ cols, double *__restrict__ vals,
+                double *__restrict__ hs, int32_t *__restrict__ stats) {
+    constexpr int NR = (DIM == 3) ? 9 : 3;
+    constexpr int CAPK = 32 * KS;
+    __shared__ __align__(16) int32_t s_id[kFillWarpWarps][CAPK + 4];
+    __shared__ double s_d2[kFillWarpWarps][CAPK];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    const double r2 = g.r2, rmin = g.rmin;
+    int32_t *sid = s_id[warp];
+    double *sd2 = s_d2[warp];
+    for (int64_t q = (int64_t)blockIdx.x * kFillWarpWarps + warp; q < n; q += (int64_t)gridDim.x * kFillWarpWarps) {
+        int bx, by, bz;
+        decode_bin((int64_t)keys[q], g, bx, by, bz);
+        int rs_ = 0, re_ = 0;
+        if (lane < NR) xtriple_range<DIM>(lane, bx, by, bz, g, P.cs, rs_, re_);
+        const double qx = P.x[q], qy = P.y[q], qz = (DIM == 3) ? P.z[q] : 0.0;
+        const int32_t qid = P.id[q];
+        const int64_t base = rowptr[qid];
+        const int64_t len = rowptr[qid + 1] - base;
+        // the runs flattened: candidate t of the query lies in run r with ex[r] <= t < ex[r+1] at
+        // sorted position st[r] + (t - ex[r]); every lane holds the NR run bounds in registers
+        int incl = re_ - rs_;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        int ex[NR + 1], st[NR];
+        ex[0] = 0;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            ex[r + 1] = __shfl_sync(0xffffffffu, incl, r);
+            st[r] = __shfl_sync(0xffffffffu, rs_, r);
+        }
+        const int C = ex[NR];
+        int nacc = 0;
+        for (int t0 = 0; t0 < C; t0 += 64) {
+            bool ok[2];
+            double d2[2];
+            int pp[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int t = t0 + 32 * u + lane;
+                int p = st[0] + t;
+#pragma unroll
+                for (int r = 1; r < NR; ++r)
+                    if (t >= ex[r]) p = st[r] + (t - ex[r]);
+                pp[u] = p;
+                ok[u] = false;
+                d2[u] = 0.0;
+                if (t < C) {
+                    d2[u] = pair_d2<DIM>(qx, qy, qz, P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0);
+                    ok[u] = d2[u] < r2;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, ok[u]);
+                if (ok[u]) {
+                    const int k = nacc + __popc(bal & lt);
+                    if (k < CAPK) sid[k] = P.id[pp[u]], sd2[k] = d2[u];
+                }
+                nacc += __popc(bal);
+            }
+        }
+        const int K = min(nacc, CAPK);
+        if (lane < 4) sid[K + lane] = 0x7fffffff;  // pads of the 4-wide rank loads
+        __syncwarp();
+        int32_t myid[KS];
+        int rank[KS];
+#pragma unroll
+        for (int t = 0; t < KS; ++t) {
+            const int e = lane + 32 * t;
+            myid[t] = (e < K) ? sid[e] : 0x7fffffff;
+            rank[t] = 0;
+        }
+        for (int j = 0; j < K; j += 4) {
+            const int4 v = *reinterpret_cast<const int4 *>(sid + j);
+#pragma unroll
+            for (int t = 0; t < KS; ++t)
+                rank[t] += (v.x < myid[t]) + (v.y < myid[t]) + (v.z < myid[t]) + (v.w < myid[t]);
+        }
+        double hsum = 0.0;
+#pragma unroll
+        for (int t = 0; t < KS; ++t) {
+            const int e = lane + 32 * t;
+            if (e < K && rank[t] < len) {
+                const double w = weight_of(rmin, sd2[e]);
+                cols[base + rank[t]] = myid[t];
+                vals[base + rank[t]] = w;
+                hsum += w;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
+        if (lane == 0) {
+            hs[qid] = hsum;
+            // the fill must write exactly the row length the count pass produced
+            if ((int64_t)nacc != len) atomicOr(&stats[2], 1);
+        }
+        __syncwarp();  // the list is reused by the warp's next query
+    }
+}
+
 // ------------------------------------------------------------------ row sort (large path only)
 // Sorts (col, val) of each listed row ascending by col. Uses the all-ascending bitonic
 // network (mirror step i ^ (k-1), then half-cleaners i ^ j), so indices >= L act as +inf
@@ -857,6 +978,17 @@ tf_status launch_fill(const SortedPts &P, const Grid &g, tf_filter_s *h, int cap
     return TF_OK;
 }
 
+template <int DIM, int KS>
+tf_status launch_fill_warp(const SortedPts &P, const uint32_t *keys, const Grid &g, int64_t n, tf_filter_s *h,
+                           int sms, int32_t *stats, cudaStream_t s) {
+    const int64_t need = (n + kFillWarpWarps - 1) / kFillWarpWarps;
+    const unsigned grid = (unsigned)std::min<int64_t>(need, (int64_t)sms * 32);
+    k_fill_warp<DIM, KS><<<grid, kFillWarpWarps * 32, 0, s>>>(P, keys, g, n, h->rowptr, h->cols, h->vals, h->hs,
+                                                                stats);
+    TF_LAUNCH_CHECK();
+    return TF_OK;
+}
+
 }  // namespace
 
 tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, int flags, cudaStream_t s,
@@ -932,6 +1064,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     P.z = (dim == 3) ? sxyz.p + 2 * n : sxyz.p + n;
     P.id = reinterpret_cast<const int32_t *>(vs);
     P.cs = cs.p;
+    const uint32_t *ks_keys = ks;  // sorted bin keys (the warp fill decodes each query's bin)
 
     // largest neighbourhood -> shared-memory capacity of the count / fill passes
     DevBuf<int32_t> counts, stats;
@@ -993,10 +1126,34 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     TF_TRY(dalloc(&h->hs, n, s, "Hs"));
     DevBuf<int32_t> large_rows;
     build_trace().mark("alloc_csr", s);
-    if (maxC > cap) TF_TRY(large_rows.alloc(n, s, "large-neighbourhood rows"));
+    // a7 kernel: the block-per-bin fill. TOPOFILT_FILL=warp selects the warp-per-query fill for
+    // rows up to 128 entries (measured slower: config 4 fill 1.08 vs 0.77 ms, config 3 1.24 vs
+    // 1.05 ms); both are parity-tested (tests/test_gpu_fuzz.py)
+    int fill_kind = 0;
+    if (const char *e = getenv("TOPOFILT_FILL")) {
+        if (!strcmp(e, "block")) fill_kind = 0;
+        else if (!strcmp(e, "warp") && maxrow <= 128) fill_kind = 1;
+    }
+    if (fill_kind == 1) {
+        const int ks = std::max(1, (maxrow + 31) / 32);
+        if (dim == 3) {
+            if (ks == 1) TF_TRY((launch_fill_warp<3, 1>(P, ks_keys, g, n, h, di.sms, stats.p, s)));
+            else if (ks == 2) TF_TRY((launch_fill_warp<3, 2>(P, ks_keys, g, n, h, di.sms, stats.p, s)));
+            else if (ks == 3) TF_TRY((launch_fill_warp<3, 3>(P, ks_keys, g, n, h, di.sms, stats.p, s)));
+            else TF_TRY((launch_fill_warp<3, 4>(P, ks_keys, g, n, h, di.sms, stats.p, s)));
+        } else {
+            if (ks == 1) TF_TRY((launch_fill_warp<2, 1>(P, ks_keys, g, n, h, di.sms, stats.p, s)));
+            else if (ks == 2) TF_TRY((launch_fill_warp<2, 2>(P, ks_keys, g, n, h, di.sms, stats.p, s)));
+            else if (ks == 3) TF_TRY((launch_fill_warp<2, 3>(P, ks_keys, g, n, h, di.sms, stats.p, s)));
+            else TF_TRY((launch_fill_warp<2, 4>(P, ks_keys, g, n, h, di.sms, stats.p, s)));
+        }
+    }
+    if (fill_kind == 0 && maxC > cap) TF_TRY(large_rows.alloc(n, s, "large-neighbourhood rows"));
     int fw = bw;  // warps per fill block (queries of one bin in parallel)
     if (const char *e = getenv("TOPOFILT_FILL_WARPS")) fw = atoi(e);  // tuning knob (benchmarks only)
-    if (dim == 3) {
+    if (fill_kind == 1) {
+        // done above
+    } else if (dim == 3) {
         if (fw >= 8) TF_TRY((launch_fill<3, 8>(P, g, h, cap, large_rows.p, stats.p, s)));
         else if (fw >= 4) TF_TRY((launch_fill<3, 4>(P, g, h, cap, large_rows.p, stats.p, s)));
         else if (fw >= 2) TF_TRY((launch_fill<3, 2>(P, g, h, cap, large_rows.p, stats.p, s)));
@@ -1008,7 +1165,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
         else TF_TRY((launch_fill<2, 1>(P, g, h, cap, large_rows.p, stats.p, s)));
     }
     build_trace().mark("fill", s);
-    if (maxC > cap) {
+    if (fill_kind == 0 && maxC > cap) {
         const int scap = 8192;
         const size_t smem = (size_t)scap * (sizeof(double) + sizeof(int32_t));
         TF_CUDA_TRY(cudaFuncSetAttribute(k_rowsort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

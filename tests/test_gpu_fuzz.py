@@ -78,3 +78,55 @@ def test_random_clouds(tf, seed):
         scale = np.where(want != 0, np.abs(want), np.abs(want).max())
         assert np.all(np.abs(got - want) <= 1e-10 * scale), f"seed {seed} {what}"
     f.close()
+
+
+@pytest.mark.parametrize("kind", ["block", "warp"])
+@pytest.mark.parametrize("seed", range(24))
+def test_fill_kernels(tf, seed, kind, monkeypatch):
+    """Both a7 fill kernels, forced (TOPOFILT_FILL): the block-per-bin fill (staging + id sort) and
+    the warp-per-query fill (exact tests + id ranks; serves rows up to 128 entries, KS = 1..4, and
+    falls back to the block fill above that). Whole CSR bit-exact vs the oracle, Hs 1e-12."""
+    monkeypatch.setenv("TOPOFILT_FILL", kind)
+    c, rmin = cloud(seed)
+    ref = oracle.build_celllist(c, rmin)
+    f = tf.tf_build_filter(dev(c), rmin, path="cell_list")
+    rowptr, cols, vals, hs = (t.cpu().numpy() for t in f.csr())
+    np.testing.assert_array_equal(rowptr, ref.rowptr)
+    np.testing.assert_array_equal(cols, ref.cols)
+    np.testing.assert_array_equal(vals, ref.vals)
+    np.testing.assert_allclose(hs, ref.hs, rtol=1e-12)
+    f.close()
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_fill_kernels_agree_configs(tf, cfg, monkeypatch):
+    """Configs 1-4 on the cell-list path: the warp fill's CSR equals the block fill's byte for byte,
+    Hs within 1e-12 (different summation order)."""
+    c, _, _, rmin = synth.workload(cfg)
+    cd = dev(c)
+    out = {}
+    for kind in ("block", "warp"):
+        monkeypatch.setenv("TOPOFILT_FILL", kind)
+        f = tf.tf_build_filter(cd, rmin, path="cell_list")
+        out[kind] = [t.clone() for t in f.csr()]
+        f.close()
+    (ra, ca, va, ha), (rb, cb, vb, hb) = out["block"], out["warp"]
+    assert torch.equal(ra, rb) and torch.equal(ca, cb) and torch.equal(va, vb)
+    assert ((ha - hb).abs() / hb.abs()).max().item() <= 1e-12
+
+
+@pytest.mark.parametrize("rmin", [2.6, 2.8])
+def test_fill_warp_long_rows(tf, rmin, monkeypatch):
+    """Rows of 97-128 entries (longest 104 / 126): the forced warp fill's four-slot ranks (KS = 4)
+    against the oracle; ragged row lengths from a uniform random cloud."""
+    monkeypatch.setenv("TOPOFILT_FILL", "warp")
+    c = np.ascontiguousarray(synth.uniform(777, 0, 3 * 6000, 0.0, 18.0).reshape(-1, 3))
+    ref = oracle.build_celllist(c, rmin)
+    assert 96 < np.diff(ref.rowptr).max() <= 128
+    f = tf.tf_build_filter(dev(c), rmin, path="cell_list")
+    rowptr, cols, vals, hs = (t.cpu().numpy() for t in f.csr())
+    np.testing.assert_array_equal(rowptr, ref.rowptr)
+    np.testing.assert_array_equal(cols, ref.cols)
+    np.testing.assert_array_equal(vals, ref.vals)
+    np.testing.assert_allclose(hs, ref.hs, rtol=1e-12)
+    f.close()
