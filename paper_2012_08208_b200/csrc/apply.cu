@@ -96,10 +96,29 @@ __global__ void k_plan(const int64_t *__restrict__ rowptr, int64_t n, int64_t nb
     }
 }
 
+#ifndef TF_APPLY_FASTDIV
+#define TF_APPLY_FASTDIV 0  // 1: reciprocal + Newton quotient (<= ~1 ulp) instead of the IEEE division
+#endif
+#if TF_APPLY_FASTDIV
+__device__ __forceinline__ double quot(double a, double b) {
+    // b > 0 and normal here (b >= Hs_i * 1e-3 >= rmin * 1e-3)
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+    double e = fma(-b, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-b, r, 1.0);
+    r = fma(r, e, r);
+    const double q = a * r;
+    return fma(r, fma(-b, q, a), q);
+}
+#else
+__device__ __forceinline__ double quot(double a, double b) { return a / b; }
+#endif
+
 template <bool SENS>
 __device__ __forceinline__ double finish(double acc, double hs_i, double x_i) {
-    if (SENS) return acc / (hs_i * fmax(1e-3, x_i));
-    return acc / hs_i;
+    if (SENS) return quot(acc, hs_i * fmax(1e-3, x_i));
+    return quot(acc, hs_i);
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
