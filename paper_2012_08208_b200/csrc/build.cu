@@ -918,6 +918,10 @@ tf_status make_grid(const double *bb, int64_t n, int dim, double rmin, Grid *g) 
     for (int d = 0; d < dim; ++d) lo[d] = bb[d], span[d] = bb[3 + d] - bb[d];
     // Bin side s >= rmin*(1+1e-6): a pair within rmin lies in adjacent bins (R5).
     double s = rmin * (1.0 + 1e-6);
+    if (const char *e = getenv("TOPOFILT_BIN_SCALE")) {  // tuning knob (benchmarks only): f in [1, 4]
+        const double f = atof(e);
+        if (f >= 1.0 && f <= 4.0) s *= f;
+    }
     const double cap_total = std::max(4.0 * (double)n, 64.0);
     for (int it = 0; it < 4096; ++it) {
         double total = 1.0;
