@@ -130,3 +130,20 @@ def test_fill_warp_long_rows(tf, rmin, monkeypatch):
     np.testing.assert_array_equal(vals, ref.vals)
     np.testing.assert_allclose(hs, ref.hs, rtol=1e-12)
     f.close()
+
+
+@pytest.mark.parametrize("scale", [1.5, 3.0])
+@pytest.mark.parametrize("seed", [0, 2, 3, 6, 9, 14, 20])
+def test_bin_scale_invariance(tf, seed, scale, monkeypatch):
+    """The GPU cell list with bins of scale*rmin (TOPOFILT_BIN_SCALE) gives the same CSR as the
+    oracle: the 3^dim rule holds for any bin side >= rmin*(1+1e-6) (SURVEY 8(c) O2 invariance)."""
+    monkeypatch.setenv("TOPOFILT_BIN_SCALE", str(scale))
+    c, rmin = cloud(seed)
+    ref = oracle.build_celllist(c, rmin)
+    f = tf.tf_build_filter(dev(c), rmin, path="cell_list")
+    rowptr, cols, vals, hs = (t.cpu().numpy() for t in f.csr())
+    np.testing.assert_array_equal(rowptr, ref.rowptr)
+    np.testing.assert_array_equal(cols, ref.cols)
+    np.testing.assert_array_equal(vals, ref.vals)
+    np.testing.assert_allclose(hs, ref.hs, rtol=1e-12)
+    f.close()
