@@ -38,6 +38,28 @@ def summary_blocks(path):
     return blocks
 
 
+SURVEY_KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+               "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+               "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+               "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+               "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+               "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]
+
+
+def write_survey_metrics(raw, out):
+    """SURVEY 8(d)'s ncu metric list (DRAM bytes and throughput, L2 hit rate, fp64 pipe) per kernel."""
+    import csv
+    rows = list(csv.reader(open(raw)))
+    h, units = rows[0], rows[1]
+    keys = [k for k in SURVEY_KEYS if k in h]
+    with open(out, "w") as f:
+        f.write("# SURVEY 8(d) ncu metrics per kernel (ncu --set full --clock-control none; config 5 bench step: "
+                "lattice build + 2 applies, then the cell-list build leg); source: tools/evidence.sh capture\n")
+        f.write("kernel | " + " | ".join(f"{k} [{units[h.index(k)]}]" for k in keys) + "\n")
+        for r in rows[2:]:
+            f.write(r[h.index("Kernel Name")][:40] + " | " + " | ".join(r[h.index(k)] for k in keys) + "\n")
+
+
 def main(rnd):
     dst = os.path.join(ROOT, "profiles", rnd)
     os.makedirs(dst, exist_ok=True)
@@ -52,6 +74,7 @@ def main(rnd):
     ncu(["-i", rep, "--page", "raw", "--csv"], raw)
     with open(os.path.join(dst, "ncu_full_summary.txt"), "w") as f:
         subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), raw], stdout=f, check=True)
+    write_survey_metrics(raw, os.path.join(dst, "survey_metrics.txt"))
     for k in ("k_spmv", "k_fill", "k_count", "k_lat_fill_exact"):
         src = f"/tmp/src_{k}.csv"
         ncu(["-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{k}", "-c", "1"], src)
