@@ -44,6 +44,10 @@ __device__ __forceinline__ double oc_value(double d, double dc, double lmid, dou
 constexpr unsigned long long kNanBit = 1ull << 63;
 
 constexpr int kOcThreads = 256;
+#ifndef TF_OC_UNROLL
+#define TF_OC_UNROLL 8
+#endif
+constexpr int kOcUnroll = TF_OC_UNROLL;
 
 __global__ void __launch_bounds__(kOcThreads) k_oc(const double *__restrict__ x, const double *__restrict__ dc,
                                                    int64_t n, double move, double l1, double l2, double tol,
@@ -64,15 +68,34 @@ __global__ void __launch_bounds__(kOcThreads) k_oc(const double *__restrict__ x,
         lmid = 0.5 * (l2 + l1);
         u128 acc = 0;
         int nan = 0;
-        auto body = [&](int64_t i) {
-            const double v = oc_value(__ldcg(x + i), __ldcg(dc + i), lmid, move);
+        auto add = [&](double xi, double dci) {
+            const double v = oc_value(xi, dci, lmid, move);
             if (v != v) nan = 1;
             else acc += (u128)__double2ull_rz(v * 0x1p62);  // exact: v is a multiple of 2^-62, v <= 1
         };
+        // kOcUnroll elements per thread in flight (loads first): with one element per thread per
+        // step the pass was latency-bound (ncu: 24% DRAM, 50% issue). Config 5, 30 passes:
+        // U = 1 1776 us, 4 1486 us, 8 1402 us, 16 1662 us (117 registers). Integer sums: order-free.
         if (it & 1) {
-            for (int64_t i = last; i >= 0; i -= stride) body(i);
+            int64_t i = last;
+            for (; i - (kOcUnroll - 1) * stride >= 0; i -= kOcUnroll * stride) {
+                double xv[kOcUnroll], dv[kOcUnroll];
+#pragma unroll
+                for (int u = 0; u < kOcUnroll; ++u) xv[u] = __ldcg(x + i - u * stride), dv[u] = __ldcg(dc + i - u * stride);
+#pragma unroll
+                for (int u = 0; u < kOcUnroll; ++u) add(xv[u], dv[u]);
+            }
+            for (; i >= 0; i -= stride) add(__ldcg(x + i), __ldcg(dc + i));
         } else {
-            for (int64_t i = gid; i < n; i += stride) body(i);
+            int64_t i = gid;
+            for (; i + (kOcUnroll - 1) * stride < n; i += kOcUnroll * stride) {
+                double xv[kOcUnroll], dv[kOcUnroll];
+#pragma unroll
+                for (int u = 0; u < kOcUnroll; ++u) xv[u] = __ldcg(x + i + u * stride), dv[u] = __ldcg(dc + i + u * stride);
+#pragma unroll
+                for (int u = 0; u < kOcUnroll; ++u) add(xv[u], dv[u]);
+            }
+            for (; i < n; i += stride) add(__ldcg(x + i), __ldcg(dc + i));
         }
         // block reduction of the 128-bit sums (integer: order does not matter)
         unsigned long long lo = (unsigned long long)acc, hi = (unsigned long long)(acc >> 64);
