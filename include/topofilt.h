@@ -89,6 +89,8 @@ typedef struct {
                              (built unsorted, then sorted by the row-sort kernel) */
     int32_t radix_passes;
     int32_t path;         /* TF_PATH_* */
+    int64_t groups;       /* cell-list path: query groups of the group kernels;
+                             0 = the per-bin kernels ran */
 } tf_build_info;
 
 /*
@@ -119,6 +121,7 @@ TF_API tf_status tf_build_filter(const double *centroids, int64_t n, int dim, do
  *     Detection costs a few small device-to-host copies (synchronising `stream`).
  *   flags = TF_BUILD_CELL_LIST: always the cell list.
  *   flags = TF_BUILD_LATTICE: the lattice path or TF_ERR_INVALID (tests, benchmarks).
+ *   flags = TF_BUILD_CELL_LIST_BINS: the cell list with its per-bin kernels (tests, benchmarks).
  * Other arguments and errors as tf_build_filter; TF_ERR_INVALID for unknown flags.
  */
 /*
@@ -135,6 +138,9 @@ TF_API tf_status tf_lattice_detect_host(const double *centroids_host, int64_t n,
 #define TF_BUILD_AUTO 0
 #define TF_BUILD_CELL_LIST 1
 #define TF_BUILD_LATTICE 2
+#define TF_BUILD_CELL_LIST_BINS 3 /* the cell list with the per-bin count/fill kernels (the
+                                     round-1 kernels; also the fallback for neighbourhoods beyond
+                                     the group kernels' shared memory) */
 TF_API tf_status tf_build_filter_ex(const double *centroids, int64_t n, int dim, double rmin, int flags,
                                     void *stream, tf_filter *out);
 

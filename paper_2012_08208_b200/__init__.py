@@ -37,7 +37,7 @@ EXPORTS = [
 
 
 # tf_build_filter_ex flags (TF_BUILD_*) and tf_build_info.path values (TF_PATH_*)
-BUILD_FLAGS = {"auto": 0, "cell_list": 1, "lattice": 2}
+BUILD_FLAGS = {"auto": 0, "cell_list": 1, "lattice": 2, "cell_list_bins": 3}
 BUILD_PATHS = {0: "cell_list", 1: "lattice_tested", 2: "lattice_exact"}
 
 
@@ -56,7 +56,7 @@ class tf_view(ctypes.Structure):
 class tf_build_info(ctypes.Structure):
     _fields_ = [("bin_side", ctypes.c_double), ("bins", ctypes.c_int64 * 3), ("nbins", ctypes.c_int64),
                 ("max_candidates", ctypes.c_int64), ("large_rows", ctypes.c_int64),
-                ("radix_passes", ctypes.c_int32), ("path", ctypes.c_int32)]
+                ("radix_passes", ctypes.c_int32), ("path", ctypes.c_int32), ("groups", ctypes.c_int64)]
 
 
 class tf_helmholtz_info(ctypes.Structure):
@@ -225,7 +225,7 @@ class Filter:
         _check(_lib.tf_build_stats(self.handle, ctypes.byref(info)))
         return {"bin_side": info.bin_side, "bins": list(info.bins), "nbins": info.nbins,
                 "max_candidates": info.max_candidates, "large_rows": info.large_rows,
-                "radix_passes": info.radix_passes, "path": BUILD_PATHS[info.path]}
+                "radix_passes": info.radix_passes, "path": BUILD_PATHS[info.path], "groups": info.groups}
 
     def sensitivity_host(self, x: np.ndarray, dc: np.ndarray, out: np.ndarray | None = None, stream=None):
         return tf_sensitivity_filter_host(self, x, dc, out, stream)

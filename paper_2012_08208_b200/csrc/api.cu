@@ -268,7 +268,8 @@ tf_status tf_build_filter_ex(const double *centroids, int64_t n, int dim, double
                              tf_filter *out) {
     try {
         TF_TRY(check_build_args(n, dim, rmin, out));
-        if (flags != TF_BUILD_AUTO && flags != TF_BUILD_CELL_LIST && flags != TF_BUILD_LATTICE) {
+        if (flags != TF_BUILD_AUTO && flags != TF_BUILD_CELL_LIST && flags != TF_BUILD_LATTICE &&
+            flags != TF_BUILD_CELL_LIST_BINS) {
             set_error("tf_build_filter_ex: unknown flags %d", flags);
             return TF_ERR_INVALID;
         }

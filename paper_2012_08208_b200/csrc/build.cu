@@ -37,6 +37,7 @@
 #include <algorithm>
 
 #include "tf_internal.cuh"
+#include "smem_sort.cuh"
 
 namespace tf {
 namespace {
@@ -151,11 +152,7 @@ __global__ void __launch_bounds__(256) k_gather_sorted(const double *__restrict_
 }
 
 // ------------------------------------------------------------------ neighbourhood helpers
-struct SortedPts {
-    const double *x, *y, *z;  // SoA, sorted by (bin key, id)
-    const int32_t *id;
-    const int32_t *cs;        // cell start [nbins+1]
-};
+using SortedPts = SortedPtsView;
 
 __device__ __forceinline__ void decode_bin(int64_t b, const Grid &g, int &bx, int &by, int &bz) {
     bx = (int)(b % g.nb[0]);
@@ -409,88 +406,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_count(SortedPts P, Grid g, int c
 }
 
 // ------------------------------------------------------------------ a7: fill pass
-// Block-wide stable LSD radix sort of C (key, val) pairs in shared memory, 8-bit digits.
-// Warp w owns the contiguous strip [w*Q, (w+1)*Q): per-warp digit histograms, a block scan
-// over (digit, warp) in digit-major order, then a stable scatter where the rank inside a
-// 32-element round comes from __match_any_sync peer groups. Returns 0 if the result is in
-// (ka, va), 1 if in (kb, vb).
-template <int WARPS>
-__device__ int block_radix_sort_smem(uint32_t *ka, uint32_t *va, uint32_t *kb, uint32_t *vb, int C, int bits,
-                                     int32_t (*wc)[256], int32_t *wsum) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t lt = (1u << lane) - 1u;
-    const int Q = (((C + WARPS - 1) / WARPS) + 31) & ~31;
-    const int s0 = min(C, warp * Q), s1 = min(C, s0 + Q);
-    int which = 0;
-    for (int shift = 0; shift < bits; shift += 8) {
-        uint32_t *ki = which ? kb : ka, *vi = which ? vb : va, *ko = which ? ka : kb, *vo = which ? va : vb;
-        for (int i = lane; i < 256; i += 32) wc[warp][i] = 0;
-        __syncwarp();
-        for (int base = s0; base < s1; base += 32) {
-            const int i = base + lane;
-            const int d = (i < s1) ? (int)((ki[i] >> shift) & 255u) : 256;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            if (d < 256 && lane == __ffs(peers) - 1) wc[warp][d] += __popc(peers);
-            __syncwarp();
-        }
-        __syncthreads();
-        // exclusive scan over (digit, warp), digit-major: each thread owns DPT consecutive digits
-        constexpr int DPT = 256 / (32 * WARPS);
-        int tot[DPT], run = 0;
-#pragma unroll
-        for (int k = 0; k < DPT; ++k) {
-            const int d = tid * DPT + k;
-            int t = 0;
-#pragma unroll
-            for (int w = 0; w < WARPS; ++w) t += wc[w][d];
-            tot[k] = t;
-            run += t;
-        }
-        int inc = run;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int u = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += u;
-        }
-        if (lane == 31) wsum[warp] = inc;
-        __syncthreads();
-        int ex = inc - run;
-        for (int w = 0; w < warp; ++w) ex += wsum[w];
-#pragma unroll
-        for (int k = 0; k < DPT; ++k) {
-            const int d = tid * DPT + k;
-            int off = ex;
-#pragma unroll
-            for (int w = 0; w < WARPS; ++w) {
-                const int c = wc[w][d];
-                wc[w][d] = off;
-                off += c;
-            }
-            ex += tot[k];
-        }
-        __syncthreads();
-        for (int base = s0; base < s1; base += 32) {
-            const int i = base + lane;
-            const bool valid = i < s1;
-            const uint32_t key = valid ? ki[i] : 0u, val = valid ? vi[i] : 0u;
-            const int d = valid ? (int)((key >> shift) & 255u) : 256;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            const int before = valid ? wc[warp][d] : 0;
-            __syncwarp();
-            if (valid && lane == __ffs(peers) - 1) wc[warp][d] = before + __popc(peers);
-            __syncwarp();
-            if (valid) {
-                const int dst = before + __popc(peers & lt);
-                TF_DCHECK(dst >= 0 && dst < C);
-                ko[dst] = key;
-                vo[dst] = val;
-            }
-        }
-        __syncthreads();
-        which ^= 1;
-    }
-    return which;
-}
+// (block_radix_sort_smem: smem_sort.cuh)
 
 // Shared-memory layout of the fill staging: five 4-byte arrays of `cap` entries (20 B per
 // candidate), reused across the phases of k_fill:
@@ -997,7 +913,7 @@ tf_status launch_fill_warp(const SortedPts &P, const uint32_t *keys, const Grid 
 
 tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, int flags, cudaStream_t s,
                               tf_filter_s *h) {
-    if (flags != TF_BUILD_CELL_LIST) {
+    if (flags != TF_BUILD_CELL_LIST && flags != TF_BUILD_CELL_LIST_BINS) {
         bool used = false;
         TF_TRY(build_lattice_csr(c, n, dim, rmin, s, h, &used));
         if (used) return TF_OK;
@@ -1069,6 +985,16 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     P.id = reinterpret_cast<const int32_t *>(vs);
     P.cs = cs.p;
     const uint32_t *ks_keys = ks;  // sorted bin keys (the warp fill decodes each query's bin)
+
+    // a5-a7 by query groups (cl_build.cu) unless the per-bin kernels are asked for or a group's
+    // neighbourhood union exceeds the group kernels' shared-memory capacity
+    bool legacy = (flags == TF_BUILD_CELL_LIST_BINS);
+    if (const char *e = getenv("TOPOFILT_CL")) legacy = legacy || !strcmp(e, "bins");  // benchmarks
+    if (!legacy) {
+        bool done = false;
+        TF_TRY(build_cell_list_groups(P, ks_keys, g, n, s, h, &done));
+        if (done) return TF_OK;
+    }
 
     // largest neighbourhood -> shared-memory capacity of the count / fill passes
     DevBuf<int32_t> counts, stats;

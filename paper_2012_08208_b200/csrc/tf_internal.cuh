@@ -190,6 +190,14 @@ struct Grid {
     float t_in, t_out;
 };
 
+// ------------------------------------------------------------------ cell-list sorted points
+// Centroids in cell-list order (build.cu a4): exact fp64 SoA copies, original ids, cell starts.
+struct SortedPtsView {
+    const double *x, *y, *z;  // SoA, sorted by (bin key, id)
+    const int32_t *id;
+    const int32_t *cs;        // cell start [nbins+1]
+};
+
 // ------------------------------------------------------------------ apply plan
 struct ApplyPlan {
     int64_t nblocks = 0;      // row blocks
@@ -278,6 +286,10 @@ tf_status radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys_alt, u
 // build.cu (flags: TF_BUILD_*; the lattice path is tried first unless TF_BUILD_CELL_LIST)
 tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, int flags, cudaStream_t s,
                               tf_filter_s *h);
+// cl_build.cu: the group kernels of the cell-list build (count -> scan -> fill) on the sorted
+// points; *done = false (TF_OK, nothing allocated in h) when a union exceeds their capacity
+tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_keys, const Grid &g, int64_t n,
+                                 cudaStream_t s, tf_filter_s *h, bool *done);
 // lattice_build.cu: *used = false (and TF_OK) when the centroids are not a verified lattice
 tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cudaStream_t s, tf_filter_s *h,
                             bool *used);
