@@ -6,27 +6,27 @@
 // sorted SoA); this file does a5 (count), a7 (fill) on top of that, and hands the row lengths to
 // the a6 scan in between.
 //
-// Design. A GROUP is <= 32 consecutive points of the cell-sorted order inside
-// one "unit" (a bin row cut into blocks of kUnitBins bins), i.e. a compact run along x. One warp
-// serves one group, lane = query:
-//   k_cl_count  (1) gathers the group's UNION neighbourhood -- the 3^(dim-1) contiguous x-runs
-//               [bx0-1, bx1+1] of the bin rows around it --, (2) sorts it by point id with a
-//               warp-level LSD radix sort (so the union is in ascending COLUMN order),
-//               (3) writes that sorted list (sorted-SoA positions) for the fill, (4) sweeps it:
-//               every lane tests its query against every union candidate with packed fp32x2
-//               math (EDM form, R4c), one sign bit per test shifted into a per-query 32-bit mask
-//               word (SHF.L.W funnel), band candidates caught by a running unsigned minimum and
-//               decided by the exact fp64 test, (5) stores the words (coalesced: word k of lane q
-//               at [k][q]) and the row length = popcount.
-//   k_cl_fill   stages the union's exact fp64 coordinates and ids in shared memory, expands each
-//               lane's mask words into its query's candidate list (lane-serial, all lanes at
-//               once), then per query writes the row with all 32 lanes: exact fp64 d^2 and weight
-//               (the oracle's expression), int32 column, fp64 value, coalesced, Hs by a fixed-
-//               order lane reduction. No test is repeated: the set bits ARE the accepted pairs.
-// Compared with the per-bin kernels of build.cu (k_count / k_fill, kept as the fallback for
-// neighbourhoods beyond shared memory): the id sort is shared by 32 queries instead of one bin's
-// ~20, the fill re-tests nothing, and a test costs ~4.5 lane-instructions instead of a ballot,
-// compaction and list traffic per 64 candidates.
+// Design. A GROUP is <= kGroupQ (32) consecutive points of the cell-sorted order
+// inside one "unit" (a bin row cut into blocks of kUnitBins bins), i.e. a compact run along x:
+//   k_cl_groups  group records and the size of each group's UNION neighbourhood -- the 3^(dim-1)
+//                contiguous x-runs [bx0-1, bx1+1] of the bin rows around it;
+//   k_cl_count   block per group: (1) stages the union, (2) sorts it by point id with the block
+//                radix sort (smem_sort.cuh), so the union is in ascending COLUMN order, (3) writes
+//                that sorted list (sorted-SoA positions) for the fill, (4) sweeps it: lane = query,
+//                every union candidate tested with packed fp32x2 math in EDM form (R4c), one sign
+//                bit per test funnel-shifted (SHF.L.W) into a per-query 32-bit mask word, band
+//                candidates caught by a running unsigned minimum (VIMNMX3) and decided by the
+//                exact fp64 test; (5) stores the words (coalesced, word k of query q at [k][q]) and
+//                the row length = popcount;
+//   k_cl_fill    warp per group: lane = query walks its mask words (branch-free, two bits per
+//                step) into a list of candidate indices, then lane = entry writes each row: exact
+//                fp64 coordinates, the oracle's d^2 and weight, coalesced int32 / fp64 stores, Hs by
+//                a fixed-order lane reduction. No pair is tested twice: the set bits ARE the
+//                accepted pairs.
+// The per-bin kernels of build.cu (k_count / k_fill) stay as TF_BUILD_CELL_LIST_BINS and as the
+// fallback for unions beyond kMaxUnion. Measured: both group kernels are bound
+// by L1 wavefronts -- the sweep's broadcast candidate loads and the sort in the count, the
+// per-entry coordinate gathers in the fill.
 //
 // Exactness (R2-R4, R4c): a bit is set only if the fp32 value proves d^2 < r^2 with
 // the derived error bound, or the exact fp64 test (pair_d2, uncontracted) says so; the fill's
@@ -46,11 +46,16 @@ namespace tf {
 namespace {
 
 constexpr int kUnitBins = 32;     // bins per unit along x: a group spans at most this many bins
+#ifndef TF_CL_GROUPQ
+#define TF_CL_GROUPQ 32
+#endif
+constexpr int kGroupQ = TF_CL_GROUPQ;  // queries per group (they share one sorted union); 32 per fill warp
+constexpr int kHalves = kGroupQ / 32;
 constexpr int kMaxUnion = 6144;   // largest union (candidates) the group kernels take
 constexpr float kFarCC = 1e30f;   // |c|^2 of padding candidates / q of idle lanes: never "in"
 
 struct GroupRec {
-    int32_t q0, q1;    // sorted positions [q0, q1), q1 - q0 <= 32
+    int32_t q0, q1;    // sorted positions [q0, q1), q1 - q0 <= kGroupQ
     int32_t bx0, bx1;  // bin x-range of the group's queries
     int32_t row;       // bin row index by + bz * nb[1]
     int32_t L;         // union size (candidates)
@@ -86,7 +91,7 @@ __device__ __forceinline__ void unit_range(int64_t u, const Grid &g, int nxb, co
     e = cs[b1];
 }
 
-// ng[u] = groups of unit u (ceil(points / 32)); ng[U] = 0 (the scan's total slot)
+// ng[u] = groups of unit u (ceil(points / kGroupQ)); ng[U] = 0 (the scan's total slot)
 __global__ void __launch_bounds__(256) k_cl_units(const int32_t *__restrict__ cs, Grid g, int nxb, int64_t U,
                                                   int32_t *__restrict__ ng) {
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= U; u += (int64_t)gridDim.x * blockDim.x) {
@@ -96,7 +101,7 @@ __global__ void __launch_bounds__(256) k_cl_units(const int32_t *__restrict__ cs
         }
         int32_t s, e;
         unit_range(u, g, nxb, cs, s, e);
-        ng[u] = (e - s + 31) >> 5;
+        ng[u] = (e - s + kGroupQ - 1) / kGroupQ;
     }
 }
 
@@ -131,10 +136,10 @@ __global__ void __launch_bounds__(256) k_cl_groups(const int32_t *__restrict__ c
         unit_range(u, g, nxb, cs, s, e);
         const int32_t row = (int32_t)(u / nxb);
         int32_t gi = goff[u];
-        for (int32_t q0 = s; q0 < e; q0 += 32, ++gi) {
+        for (int32_t q0 = s; q0 < e; q0 += kGroupQ, ++gi) {
             GroupRec G;
             G.q0 = q0;
-            G.q1 = min(q0 + 32, e);
+            G.q1 = min(q0 + kGroupQ, e);
             G.bx0 = (int32_t)(keys[G.q0] % (uint32_t)g.nb[0]);
             G.bx1 = (int32_t)(keys[G.q1 - 1] % (uint32_t)g.nb[0]);
             G.row = row;
@@ -331,8 +336,10 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_cl_count(SortedPtsView P, 
         }
     }
     __syncthreads();
-    // (5) sweep: lane = query, words split over the warps
-    const int q = R.q0 + lane;
+    // (5) sweep: lane = query of this warp's half of the group, words split over the half's warps
+    constexpr int WPH = kCountWarps / kHalves;  // warps per half
+    const int half = warp / WPH, wsub = warp % WPH;
+    const int q = R.q0 + 32 * half + lane;
     const bool have = q < R.q1;
     double qxd = 0, qyd = 0, qzd = 0;
     f2u QX = 0, QY = 0, QZ = 0, QQ;
@@ -357,7 +364,7 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_cl_count(SortedPtsView P, 
     const f2u *B22 = reinterpret_cast<const f2u *>(B2);
     const double r2 = g.r2;
     int cnt = 0;
-    for (int k = warp; k < LP / 32; k += kCountWarps) {
+    for (int k = wsub; k < LP / 32; k += WPH) {
         // four independent 8-candidate accumulators (shorter dependency chains), then combined
         uint32_t wq[4] = {0, 0, 0, 0}, bm[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
 #pragma unroll
@@ -411,31 +418,34 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_cl_count(SortedPtsView P, 
             }
         }
         if (!have) w = 0;
-        mask[base + 32 * k + lane] = w;
+        mask[kHalves * base + kGroupQ * k + 32 * half + lane] = w;
         cnt += __popc(w);
     }
     wcnt[warp][lane] = cnt;
     __syncthreads();
-    if (warp == 0 && have) {
+    if (wsub == 0 && have) {
         int c = 0;
 #pragma unroll
-        for (int w = 0; w < kCountWarps; ++w) c += wcnt[w][lane];
+        for (int w = 0; w < WPH; ++w) c += wcnt[half * WPH + w][lane];
         counts[P.id[q]] = c;
         if (c > stats[3]) atomicMax(&stats[3], c);  // longest row (apply plan)
     }
 }
 
 // ------------------------------------------------------------------ a7: fill (group kernel)
-// Warp per group, two phases.
-//  expansion (lane = query): the group's mask words are staged in shared memory transposed to
-//    [lane][word] (odd stride); each lane walks its own words -- two set bits or one word step per
-//    iteration, independently of the other lanes -- and appends the candidate indices (ascending =
-//    ascending column) to its list ent[lane][0..len);
+// Warp per half group (32 queries), two phases.
+//  expansion (lane = query): the half's mask words are staged in shared memory transposed to
+//    [lane][word] (odd stride); each lane walks its own words -- up to two set bits or one word step
+//    per iteration, independently of the other lanes -- and appends the candidate indices
+//    (ascending = ascending column) to its list ent[lane][0..len);
 //  emission (lane = entry): two rows per pass, their first kFillRounds 32-entry rounds in flight
 //    together: sorted-SoA position from the group's union list, exact fp64 coordinates and id,
 //    the oracle's d^2 and weight, coalesced int32 / fp64 stores, Hs by a fixed-order lane reduction.
-// Shared memory per warp: masks [32][nw_max | 1] uint32 + lists [32][S] uint16.
-constexpr int kFillRounds = 3;
+// Shared memory per warp: masks [32][MS] uint32 (MS odd, > words) + lists [32][S] uint16.
+#ifndef TF_CL_FILL_ROUNDS
+#define TF_CL_FILL_ROUNDS 3
+#endif
+constexpr int kFillRounds = TF_CL_FILL_ROUNDS;
 constexpr int kListCap = 256;  // per-lane list capacity; longer rows take the word-parallel path
 
 template <int DIM, int WARPS>
@@ -448,18 +458,23 @@ __global__ void __launch_bounds__(WARPS * 32) k_cl_fill(SortedPtsView P, Grid g,
                                                         double *__restrict__ hs, int32_t *__restrict__ stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int32_t gi = (int32_t)blockIdx.x * WARPS + warp;
+    const int32_t wi = (int32_t)blockIdx.x * WARPS + warp;
+    const int32_t gi = wi / kHalves, half = wi % kHalves;
     if (gi >= G) return;
     const size_t per_warp = (size_t)32 * MS * 4 + (size_t)32 * S * 2;
     uint32_t *sm = reinterpret_cast<uint32_t *>(smem_raw + (size_t)warp * per_warp);  // [32][MS]
     uint16_t *ent = reinterpret_cast<uint16_t *>(sm + 32 * MS);                       // [32][S]
-    const GroupRec R = rec[gi];
+    GroupRec R = rec[gi];
+    R.q0 += 32 * half;  // this warp's queries
+    R.q1 = min(R.q1, R.q0 + 32);
+    if (R.q0 >= R.q1) return;
     const int L = R.L, LP = (L + 31) & ~31, nw = LP >> 5;
     const int64_t base = loff[gi];
+    const uint32_t *mk = mask + kHalves * base + 32 * half;
     for (int k0 = 0; k0 < MS; k0 += 4) {
         uint32_t m[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) m[u] = (k0 + u < nw) ? mask[base + 32 * (k0 + u) + lane] : 0u;
+        for (int u = 0; u < 4; ++u) m[u] = (k0 + u < nw) ? mk[kGroupQ * (k0 + u) + lane] : 0u;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (k0 + u < MS) sm[lane * MS + k0 + u] = m[u];
@@ -503,7 +518,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_cl_fill(SortedPtsView P, Grid g,
         if (have && n != len) atomicOr(&stats[2], 1);  // count/fill agreement (always-on invariant)
     }
     __syncwarp();
-    const double r2 = g.r2, rmin = g.rmin;
+    const double rmin = g.rmin;
+#ifdef TF_DEBUG_CHECKS
+    const double r2 = g.r2;
+#endif
     const int nq = R.q1 - R.q0;
     for (int i0 = 0; i0 < nq; i0 += 2) {
         int li[2];
@@ -625,7 +643,7 @@ tf_status launch_cl_fill(const SortedPtsView &P, const Grid &g, const GroupRec *
     const size_t smem = (size_t)WARPS * ((size_t)32 * MS * 4 + (size_t)32 * S * 2);
     auto kern = k_cl_fill<DIM, WARPS>;
     TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)((G + WARPS - 1) / WARPS), WARPS * 32, smem, s>>>(P, g, rec, loff, G, MS, S, list, mask,
+    kern<<<(unsigned)(((int64_t)G * kHalves + WARPS - 1) / WARPS), WARPS * 32, smem, s>>>(P, g, rec, loff, G, MS, S, list, mask,
                                                                      h->rowptr, h->cols, h->vals, h->hs, stats);
     TF_LAUNCH_CHECK();
     return TF_OK;
@@ -687,7 +705,7 @@ tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_
     DevBuf<int32_t> list, counts;
     DevBuf<uint32_t> mask;
     TF_TRY(list.alloc(hTot, s, "group unions"));
-    TF_TRY(mask.alloc(hTot, s, "group masks"));
+    TF_TRY(mask.alloc((size_t)kHalves * hTot, s, "group masks"));
     TF_TRY(counts.alloc(n, s, "row counts"));
     if (dim == 3) TF_TRY((launch_cl_count<3>(P, g, rec.p, loff.p, hG, LPmax, list.p, mask.p, counts.p, stats.p, s)));
     else TF_TRY((launch_cl_count<2>(P, g, rec.p, loff.p, hG, LPmax, list.p, mask.p, counts.p, stats.p, s)));
