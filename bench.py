@@ -334,7 +334,10 @@ def run_ours(args):
     sens_gbs = sens_bytes(n, nnz) / t_sens / 1e9
     traffic, traffic_src = ncu_traffic()
 
-    # correctness guard on the timed path (one row sample, cheap)
+    # self-check of what was timed (after the timed region): 1,000 seeded rows of a handle built
+    # through the timed path and of the general cell-list handle, CSR bitwise and both filters
+    # within 1e-10 of the oracle's row functions; a mismatch fails the run
+    check = verify_rows(tf, c, x, dc, rmin, cd, xd, dcd, args, device) if rank == 0 else None
     res = {}
     if not args.no_e2e:  # every rank (its own GPU and host buffers); max time over ranks
         res["e2e"] = run_e2e(tf, c, x, dc, rmin, applies, n, nnz, dim, args, dist, ws, device)
@@ -380,11 +383,51 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "gpu_launches": launches,
             "clocks": clk.summary(),
+            "check": check,
         }
         line.update(res)
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def verify_rows(tf, c, x, dc, rmin, cd, xd, dcd, args, device, count=1000):
+    """Compare `count` seeded rows (stream S(cfg,5,0), synth.sample_rows) of the timed path's CSR
+    and both filters -- and of the cell-list path's CSR -- with the oracle's cell-list row functions
+    (test infrastructure, run here outside every timed region). Raises on any mismatch."""
+    import torch
+
+    import oracle
+    n = c.shape[0]
+    rows = np.sort(synth.sample_rows(args.config, n, count))
+    ref = oracle.CellList(c, rmin).rows(rows)
+    want_s = oracle.apply_sensitivity(ref, x, dc)
+    want_d = oracle.apply_density(ref, x)
+    rt = torch.from_numpy(rows).to(device)
+    out = {"rows": int(rows.size), "stream": "synth.sample_rows(config, n, 1000)", "csr": "bitwise"}
+    for label, path in (("timed", args.build_path), ("cell_list", "cell_list")):
+        f = tf.tf_build_filter(cd, rmin, path=path)
+        rowptr, cols, vals, hs = f.csr()
+        starts = rowptr[rt]
+        lens = rowptr[rt + 1] - starts
+        total = int(lens.sum())
+        seg0 = torch.repeat_interleave(torch.cumsum(lens, 0) - lens, lens)
+        idx = torch.repeat_interleave(starts, lens) + (torch.arange(total, device=device) - seg0)
+        rp = np.zeros(rows.size + 1, np.int64)
+        rp[1:] = np.cumsum(lens.cpu().numpy())
+        ok = (np.array_equal(rp, ref.rowptr) and np.array_equal(cols[idx].cpu().numpy(), ref.cols)
+              and np.array_equal(vals[idx].cpu().numpy(), ref.vals))
+        hs_rel = float(np.max(np.abs(hs[rt].cpu().numpy() - ref.hs) / np.abs(ref.hs)))
+        s = f.sensitivity(xd, dcd)[rt].cpu().numpy()
+        d = f.density(xd)[rt].cpu().numpy()
+        rel = max(float(np.max(np.abs(s - want_s) / np.abs(want_s))), float(np.max(np.abs(d - want_d) / np.abs(want_d))))
+        path_name = f.stats()["path"]
+        f.close()
+        if not ok or hs_rel > 1e-12 or rel > 1e-10:
+            raise SystemExit(f"bench self-check FAILED ({label} path {path_name}): csr_equal={ok} "
+                             f"hs_rel={hs_rel:.3e} out_rel={rel:.3e}")
+        out[label] = {"path": path_name, "hs_max_rel": hs_rel, "outputs_max_rel": rel}
+    return out
 
 
 def run_e2e(tf, c, x, dc, rmin, applies, n, nnz, dim, args, dist=None, ws=1, device=None):

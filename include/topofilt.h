@@ -23,7 +23,7 @@
  *     Work is stream-ordered; apply calls are asynchronous (no host sync).
  *   - A handle is bound to the CUDA device that was current when it was built; calls on it
  *     must be made with that device current (TF_ERR_INVALID otherwise); tf_free works from any
- *     device.
+ *     device. Device pointers must belong to the current device (TF_ERR_INVALID otherwise).
  *   - Every call returns tf_status; nothing throws or aborts across the ABI.
  *     On a non-OK status tf_last_error() returns a thread-local message.
  *   - Sizes: 1 <= n < 2^31 - 1 (int32 column indices); nnz < 2^63.
@@ -186,9 +186,15 @@ TF_API int64_t tf_filter_nnz(tf_filter h);
  *   The paper's call is move = 0.2, l1 = 0, l2 = 1e5, tol = 1e-4. Branch decisions use the EXACT
  *   sum (128-bit fixed point; R15), so results are bitwise reproducible.
  *   x, dc: device fp64 [n] (x in [0, 1], dc <= 0); x_new: device fp64 [n] (may alias x);
- *   lmid_out: device fp64 [1] (the last l_mid); iters_out: device int32 [1] or NULL.
- *   One cooperative kernel launch on `stream`, no host sync.
+ *   lmid_out: device fp64 [1] (the last l_mid); iters_out: device int32 [2] or NULL:
+ *   iters_out[0] = bisection steps, iters_out[1] = flags: bit 0 (TF_OC_BRACKET_EXHAUSTED) every step
+ *   moved l1 up -- sum(x_new) still exceeded volfrac*n at l2, so the volume constraint is violated
+ *   (raise l2); bit 1 (TF_OC_NO_PROGRESS) the bisection stopped before l2 - l1 <= tol because l_mid
+ *   rounded to l1 or l2 (tol below the fp64 spacing) or after 4096 steps (reading R23).
+ *   One cooperative kernel launch on `stream`, no host sync (read the flags after the stream).
  */
+#define TF_OC_BRACKET_EXHAUSTED 1
+#define TF_OC_NO_PROGRESS 2
 TF_API tf_status tf_oc_update(const double *x, const double *dc, int64_t n, double volfrac, double move,
                               double l1, double l2, double tol, double *x_new, double *lmid_out,
                               int32_t *iters_out, void *stream);
@@ -240,7 +246,10 @@ TF_API tf_status tf_density_filter_rows(tf_filter h, const double *x, double *ou
 TF_API tf_status tf_filter_both(tf_filter h, const double *x, const double *dc, double *sens_out, double *dens_out,
                                 void *stream);
 
-/* tf_free -- release everything the handle owns (synchronises the device). NULL: no-op. */
+/* tf_free -- release everything the handle owns, stream-ordered on the stream the handle was built
+ * on (cudaFreeAsync; no device-wide synchronisation). Work on that stream and on the handle's own
+ * host-pipeline streams is ordered before the release; work the caller issued with h on OTHER
+ * streams must be complete, or ordered before that stream, when tf_free is called. NULL: no-op. */
 TF_API void tf_free(tf_filter h);
 
 /* tf_last_error -- thread-local message for the last non-OK status of this thread. */

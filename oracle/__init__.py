@@ -66,7 +66,7 @@ def lib():
         L.or_apply_density.argtypes = [I64, P, P, P, P, P, P, P]
         L.or_apply_density.restype = None
         L.or_oc_update.argtypes = [I64, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                   ctypes.c_double, P, P]
+                                   ctypes.c_double, P, P, P]
         L.or_oc_update.restype = ctypes.c_int
         L.or_compliance_sensitivity.argtypes = [I64, P, P, ctypes.c_double, P]
         L.or_compliance_sensitivity.restype = None
@@ -212,15 +212,20 @@ def apply_density(H: CSR, x: np.ndarray) -> np.ndarray:
 
 
 def oc_update(d: np.ndarray, dc: np.ndarray, volfrac: float, move: float = 0.2, l1: float = 0.0,
-              l2: float = 100000.0, tol: float = 1e-4):
+              l2: float = 100000.0, tol: float = 1e-4, flags: bool = False):
     """NEXT-1: OC update with bisection (Eq. update; listing PAPER.md:380-385),
-    exact-sum branch decisions (R15). Returns (density_new, last l_mid, iterations)."""
+    exact-sum branch decisions (R15), termination rule R23. Returns (density_new,
+    last l_mid, iterations), plus the flags word (bit 0 bracket exhausted, bit 1 no progress)
+    when flags=True."""
     d = _c64(d)
     dc = _c64(dc)
     out = np.empty_like(d)
     lm = np.zeros(1)
+    fl = np.zeros(1, dtype=np.int32)
     it = lib().or_oc_update(d.shape[0], _p(d), _p(dc), float(volfrac), float(move), float(l1), float(l2),
-                            float(tol), _p(out), _p(lm))
+                            float(tol), _p(out), _p(lm), fl.ctypes.data)
+    if flags:
+        return out, float(lm[0]), int(it), int(fl[0])
     return out, float(lm[0]), int(it)
 
 

@@ -354,15 +354,20 @@ static double oc_value(double d, double dc, double lmid, double move)
 /* exact value*2^62 as an integer (value in [0.001, 1], a multiple of 2^-62) */
 static unsigned __int128 oc_units(double v) { return (unsigned __int128)ldexp(v, 62); }
 
+/* Reading R23: the listing's loop runs while l2 - l1 > tol; when tol is below the fp64
+ * spacing near l_mid, l_mid rounds to l1 or l2 and the bracket stops shrinking, so the loop also
+ * stops there (and after 4096 steps). *flags_out: bit 0 = every step moved l1 up (the volume still
+ * exceeds the target at l2: bracket exhausted), bit 1 = stopped without reaching tol. */
 int or_oc_update(int64_t n, const double *d, const double *dc, double volfrac, double move,
-                 double l1, double l2, double tol, double *xnew, double *lmid_out)
+                 double l1, double l2, double tol, double *xnew, double *lmid_out, int *flags_out)
 {
     const double target = volfrac * (double)n;
     const unsigned __int128 T = oc_units(target);  /* target*2^62 is an integer for target >= 2^-10 */
-    int iters = 0;
+    int iters = 0, all_up = 1, stalled = 0;
     double lmid = 0.5 * (l2 + l1);
     while (l2 - l1 > tol) {
         lmid = 0.5 * (l2 + l1);
+        if (lmid == l1 || lmid == l2 || iters >= 4096) { stalled = 1; break; }
         unsigned __int128 S = 0;
         int nan = 0;
         for (int64_t i = 0; i < n; ++i) {
@@ -371,11 +376,12 @@ int or_oc_update(int64_t n, const double *d, const double *dc, double volfrac, d
             else S += oc_units(v);
         }
         if (!nan && S > T) l1 = lmid;
-        else l2 = lmid;
+        else { l2 = lmid; all_up = 0; }
         ++iters;
     }
     for (int64_t i = 0; i < n; ++i) xnew[i] = oc_value(d[i], dc[i], lmid, move);
     *lmid_out = lmid;
+    if (flags_out) *flags_out = ((iters > 0 && all_up) ? 1 : 0) | (stalled ? 2 : 0);
     return iters;
 }
 

@@ -129,12 +129,13 @@ def _check(status: int):
         raise TopofiltError(status, _lib.tf_last_error().decode(errors="replace"))
 
 
-def _stream_ptr(stream=None):
-    """None -> torch's current CUDA stream; 0 -> the legacy default stream; else a torch.cuda.Stream."""
+def _stream_ptr(stream=None, device=None):
+    """None -> torch's current CUDA stream (of `device` if given); 0 -> the legacy default stream;
+    else a torch.cuda.Stream."""
     if isinstance(stream, int):
         return ctypes.c_void_p(stream)
     import torch
-    s = torch.cuda.current_stream() if stream is None else stream
+    s = torch.cuda.current_stream(device) if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
 
 
@@ -446,18 +447,24 @@ def version() -> int:
 
 
 def tf_oc_update(x, dc, volfrac: float, move: float = 0.2, l1: float = 0.0, l2: float = 100000.0,
-                 tol: float = 1e-4, x_new=None, stream=None):
-    """NEXT-1: OC update with bisection. Returns (x_new, lmid tensor[1], iters tensor[1])."""
+                 tol: float = 1e-4, x_new=None, stream=None, flags: bool = False):
+    """NEXT-1: OC update with bisection. Returns (x_new, lmid tensor[1], iters
+    tensor[1]), plus the flags tensor[1] (TF_OC_* bits: 1 bracket exhausted, 2 no progress) when
+    flags=True. Runs on x's device."""
     import torch
     n = x.numel()
-    if x_new is None:
-        x_new = torch.empty_like(x)
-    lm = torch.empty(1, dtype=torch.float64, device=x.device)
-    it = torch.empty(1, dtype=torch.int32, device=x.device)
-    _check(_lib.tf_oc_update(_dptr(x, "x", torch.float64), _dptr(dc, "dc", torch.float64, n), n, float(volfrac),
-                             float(move), float(l1), float(l2), float(tol), _dptr(x_new, "x_new", torch.float64, n),
-                             _dptr(lm, "lmid"), ctypes.c_void_p(it.data_ptr()), _stream_ptr(stream)))
-    return x_new, lm, it
+    with torch.cuda.device(x.device):
+        if x_new is None:
+            x_new = torch.empty_like(x)
+        lm = torch.empty(1, dtype=torch.float64, device=x.device)
+        it = torch.empty(2, dtype=torch.int32, device=x.device)
+        _check(_lib.tf_oc_update(_dptr(x, "x", torch.float64), _dptr(dc, "dc", torch.float64, n), n,
+                                 float(volfrac), float(move), float(l1), float(l2), float(tol),
+                                 _dptr(x_new, "x_new", torch.float64, n), _dptr(lm, "lmid"),
+                                 ctypes.c_void_p(it.data_ptr()), _stream_ptr(stream, x.device)))
+    if flags:
+        return x_new, lm, it[:1], it[1:]
+    return x_new, lm, it[:1]
 
 
 # ------------------------------------------------------------------ NEXT-3: Helmholtz PDE filter

@@ -129,6 +129,11 @@ tf_status require_device(const void *p, const char *name) {
         set_error("%s is not a device pointer (use the *_host variant for host buffers)", name);
         return TF_ERR_INVALID;
     }
+    int cur = -1;
+    if (a.type == cudaMemoryTypeDevice && cudaGetDevice(&cur) == cudaSuccess && a.device != cur) {
+        set_error("%s lives on device %d but device %d is current", name, a.device, cur);
+        return TF_ERR_INVALID;
+    }
     return TF_OK;
 }
 
@@ -140,23 +145,27 @@ static bool overlaps(const void *a, const void *b, size_t bytes) {
 static void destroy(tf_filter_s *h) {
     if (!h) return;
     DeviceScope on(h->device);  // free on the handle's device, whichever is current
-    cudaDeviceSynchronize();
-    // stream-ordered allocations go back to the pool; the device is idle after the sync
-    if (h->rowptr) cudaFreeAsync(h->rowptr, 0);
-    if (h->cols) cudaFreeAsync(h->cols, 0);
-    if (h->vals) cudaFreeAsync(h->vals, 0);
-    if (h->hs) cudaFreeAsync(h->hs, 0);
-    if (h->plan.rb) cudaFreeAsync(h->plan.rb, 0);
-    if (h->plan.wlo) cudaFreeAsync(h->plan.wlo, 0);
-    if (h->stencil_off) cudaFreeAsync(h->stencil_off, 0);
-    if (h->stencil_w) cudaFreeAsync(h->stencil_w, 0);
-    if (h->lattice_table) cudaFreeAsync(h->lattice_table, 0);
-    if (h->hx) cudaFreeAsync(h->hx, 0);
-    if (h->hdc) cudaFreeAsync(h->hdc, 0);
-    if (h->hout) cudaFreeAsync(h->hout, 0);
-    if (h->hout2) cudaFreeAsync(h->hout2, 0);
-    if (h->ht) cudaFreeAsync(h->ht, 0);
-    if (h->side) cudaStreamDestroy(h->side);
+    // Stream-ordered release on the handle's build stream (no device-wide synchronisation): work
+    // the handle's own host-pipeline streams may still run is ordered before the frees by events;
+    // work the caller issued on other streams must be complete or ordered before tf_free (the
+    // cudaFreeAsync contract, include/topofilt.h).
+    cudaStream_t fs = h->stream;
+    for (cudaStream_t side : {h->side, h->side2}) {
+        if (!side) continue;
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+            cudaEventRecord(e, side);
+            cudaStreamWaitEvent(fs, e, 0);
+            cudaEventDestroy(e);
+        } else {
+            cudaStreamSynchronize(side);
+        }
+    }
+    for (void *p : {(void *)h->rowptr, (void *)h->cols, (void *)h->vals, (void *)h->hs, (void *)h->plan.rb,
+                    (void *)h->plan.wlo, (void *)h->stencil_off, (void *)h->stencil_w, h->lattice_table,
+                    (void *)h->hx, (void *)h->hdc, (void *)h->hout, (void *)h->hout2, (void *)h->ht})
+        if (p) cudaFreeAsync(p, fs);
+    if (h->side) cudaStreamDestroy(h->side);  // returns at once; pending work still completes
     if (h->side2) cudaStreamDestroy(h->side2);
     for (cudaEvent_t e : h->evc)
         if (e) cudaEventDestroy(e);
@@ -166,6 +175,7 @@ static void destroy(tf_filter_s *h) {
     }
     if (h->ev) cudaEventDestroy(h->ev);
     if (h->ev2) cudaEventDestroy(h->ev2);
+    cudaGetLastError();  // nothing to report from a void call
     delete h;
 }
 
@@ -202,6 +212,7 @@ static tf_status build_common(const double *c, int64_t n, int dim, double rmin, 
         set_error("cudaGetDevice failed");
         return TF_ERR_CUDA;
     }
+    h->stream = s;
     h->n = n;
     h->dim = dim;
     h->rmin = rmin;
@@ -343,6 +354,7 @@ tf_status tf_build_stencil(int dim, int64_t nx, int64_t ny, int64_t nz, double h
         tf_filter_s *f = new (std::nothrow) tf_filter_s();
         if (!f) return TF_ERR_NOMEM;
         cudaGetDevice(&f->device);
+        f->stream = (cudaStream_t)stream;
         f->n = nx * ny * nzz;
         f->dim = dim;
         f->rmin = rmin;
@@ -392,6 +404,7 @@ tf_status tf_build_lattice(int dim, int64_t nx, int64_t ny, int64_t nz, double h
         tf_filter_s *f = new (std::nothrow) tf_filter_s();
         if (!f) return TF_ERR_NOMEM;
         cudaGetDevice(&f->device);
+        f->stream = (cudaStream_t)stream;
         f->n = nx * ny * nzz * ntypes;
         f->dim = dim;
         f->rmin = rmin;
@@ -686,6 +699,7 @@ tf_status tf_filter_from_csr(const int64_t *rowptr_host, const int32_t *cols_hos
     tf_filter_s *h = new (std::nothrow) tf_filter_s();
     if (!h) return TF_ERR_NOMEM;
     cudaGetDevice(&h->device);
+    h->stream = s;
     h->n = n;
     h->nnz = nnz;
     tf_status st = TF_OK;

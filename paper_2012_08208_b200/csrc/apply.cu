@@ -591,6 +591,10 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
     TF_LAUNCH_CHECK();
     k_plan_windows<<<grid, 256, 0, s>>>(h->rowptr, h->plan.rb, nblocks, h->plan.wlo);
     TF_LAUNCH_CHECK();
+    // host copy of the row-block table; valid after the build's final stream synchronisation
+    h->plan.rb_host.resize(nblocks + 1);
+    TF_CUDA_TRY(cudaMemcpyAsync(h->plan.rb_host.data(), h->plan.rb, (nblocks + 1) * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, s));
     h->plan.nchunks = -1;  // host-pipeline chunks: computed on first use (ensure_chunk_plan)
     return TF_OK;
 }
@@ -706,6 +710,31 @@ tf_status launch_density_rows(const tf_filter_s *h, const double *x, double *out
     NvtxRange r("tf_apply/density_rows");
     if (h->stencil.K > 0) return launch_stencil(h, x, nullptr, out, false, s);
     return launch_spmv<0>(h, x, nullptr, out, s, 0.0, 0, 0, -1, nullptr, 1, nullptr, nrows);
+}
+
+// Rows [r0, r1): windows from the one holding r0 (its rows before r0 are recomputed -- the same
+// values) to the first whose first row is >= r1. The sensitivity t pass covers all n entries.
+static int64_t window_of_row(const tf_filter_s *h, int64_t r0) {
+    const std::vector<int32_t> &rb = h->plan.rb_host;
+    if (rb.empty()) return 0;
+    const auto it = std::upper_bound(rb.begin(), rb.end(), (int32_t)r0);
+    return std::max<int64_t>(0, (int64_t)(it - rb.begin()) - 1);
+}
+
+tf_status launch_sensitivity_rowrange(const tf_filter_s *h, const double *x, const double *dc, double *out,
+                                      int64_t r0, int64_t r1, cudaStream_t s) {
+    NvtxRange r("tf_apply/sensitivity_range");
+    if (r1 <= r0) return TF_OK;
+    if (h->stencil.K > 0) return launch_stencil(h, x, dc, out, true, s);
+    return launch_spmv<1>(h, x, dc, out, s, 0.0, 0, window_of_row(h, r0), -1, nullptr, 1, nullptr, r1);
+}
+
+tf_status launch_density_rowrange(const tf_filter_s *h, const double *x, double *out, int64_t r0, int64_t r1,
+                                  cudaStream_t s) {
+    NvtxRange r("tf_apply/density_range");
+    if (r1 <= r0) return TF_OK;
+    if (h->stencil.K > 0) return launch_stencil(h, x, nullptr, out, false, s);
+    return launch_spmv<0>(h, x, nullptr, out, s, 0.0, 0, window_of_row(h, r0), -1, nullptr, 1, nullptr, r1);
 }
 
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s) {

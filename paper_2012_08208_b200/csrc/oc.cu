@@ -49,10 +49,22 @@ constexpr int kOcThreads = 256;
 #endif
 constexpr int kOcUnroll = TF_OC_UNROLL;
 
-__global__ void __launch_bounds__(kOcThreads) k_oc(const double *__restrict__ x, const double *__restrict__ dc,
+constexpr int kOcMaxIter = 4096;  // safety cap (reading R23); fp64 halvings end in < 2100 steps
+
+// v * 2^62 as an exact 128-bit integer, for finite v >= 2^-10 (every x_new >= 0.001 qualifies; the
+// bound v <= 1 holds for x in [0, 1] but is not relied on)
+__device__ __forceinline__ u128 units62(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const int e = (int)((b >> 52) & 0x7ff) - 1023;
+    const unsigned long long m = (b & ((1ull << 52) - 1)) | (1ull << 52);
+    return (u128)m << (e + 10);  // v * 2^62 = m * 2^(e - 52 + 62), e >= -10
+}
+
+// x and xnew may alias (the header allows x_new == x): no __restrict__ on them
+__global__ void __launch_bounds__(kOcThreads) k_oc(const double *x, const double *__restrict__ dc,
                                                    int64_t n, double move, double l1, double l2, double tol,
                                                    unsigned long long t_lo, unsigned long long t_hi,
-                                                   ulonglong2 *__restrict__ parts, double *__restrict__ xnew,
+                                                   ulonglong2 *__restrict__ parts, double *xnew,
                                                    double *__restrict__ lmid_out, int *__restrict__ iters_out) {
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     const u128 T = ((u128)t_hi << 64) | (u128)t_lo;
@@ -63,15 +75,19 @@ __global__ void __launch_bounds__(kOcThreads) k_oc(const double *__restrict__ x,
     __shared__ int s_nan[kOcThreads / 32];
     __shared__ int s_up;
     double lmid = 0.5 * (l2 + l1);
-    int it = 0;
+    int it = 0, all_up = 1, stalled = 0;
     while (l2 - l1 > tol) {  // identical fp values in every thread: uniform trip count
         lmid = 0.5 * (l2 + l1);
+        if (lmid == l1 || lmid == l2 || it >= kOcMaxIter) {  // no progress possible (reading R23)
+            stalled = 1;
+            break;
+        }
         u128 acc = 0;
         int nan = 0;
         auto add = [&](double xi, double dci) {
             const double v = oc_value(xi, dci, lmid, move);
             if (v != v) nan = 1;
-            else acc += (u128)__double2ull_rz(v * 0x1p62);  // exact: v is a multiple of 2^-62, v <= 1
+            else acc += units62(v);  // exact: v >= 0.001 is a multiple of 2^-62
         };
         // kOcUnroll elements per thread in flight (loads first): with one element per thread per
         // step the pass was latency-bound (ncu: 24% DRAM, 50% issue). Config 5, 30 passes:
@@ -149,14 +165,17 @@ __global__ void __launch_bounds__(kOcThreads) k_oc(const double *__restrict__ x,
         }
         __syncthreads();
         if (s_up) l1 = lmid;
-        else l2 = lmid;
+        else l2 = lmid, all_up = 0;
         ++it;
         __syncthreads();  // s_up / s_lo reuse
     }
     for (int64_t i = gid; i < n; i += stride) xnew[i] = oc_value(__ldcg(x + i), __ldcg(dc + i), lmid, move);
     if (gid == 0) {
         *lmid_out = lmid;
-        if (iters_out) *iters_out = it;
+        if (iters_out) {
+            iters_out[0] = it;
+            iters_out[1] = ((it > 0 && all_up) ? TF_OC_BRACKET_EXHAUSTED : 0) | (stalled ? TF_OC_NO_PROGRESS : 0);
+        }
     }
 }
 

@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <string>
+#include <vector>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -202,6 +203,7 @@ struct SortedPtsView {
 struct ApplyPlan {
     int64_t nblocks = 0;      // row blocks
     int32_t *rb = nullptr;    // [nblocks+1] first row of each block
+    std::vector<int32_t> rb_host;  // host copy (row-range applies pick their first window from it)
     int block_nnz = 0;        // target nnz per block (window)
     int stage_cap = 0;        // staged-path capacity (nnz)
     int group = 1;            // lanes per row in the reduction phase (power of two <= 32)
@@ -246,6 +248,7 @@ struct StencilGeom {
 // ------------------------------------------------------------------ the handle
 struct tf_filter_s {
     int device = -1;  // the CUDA device current at build time; every call must use it
+    cudaStream_t stream = nullptr;  // the build stream: tf_free releases the memory stream-ordered on it
     int64_t n = 0, nnz = 0;
     int dim = 0;
     double rmin = 0;
@@ -271,7 +274,24 @@ struct tf_filter_s {
     void *lattice_table = nullptr;
 };
 
+// ------------------------------------------------------------------ shard plan (NEXT-4)
+struct tf_shard_s {
+    int device = -1;
+    int nranks = 0, rank = 0, axis = 0;
+    double cut_lo = 0, cut_hi = 0;   // this rank's slab along `axis` (-inf / +inf at the ends)
+    int64_t n_interior = 0, n_owned = 0, n_halo = 0;
+    std::vector<int64_t> recv, send;  // per rank: halo points received from / sent to it
+    int32_t *local_ids = nullptr;     // [n_owned + n_halo] global ids in local order
+    int32_t *send_idx = nullptr;      // sum(send): local indices, grouped by destination rank
+    cudaStream_t stream = nullptr;
+};
+
 namespace tf {
+
+// shard.cu (NEXT-4): the device slab partition of rank `me` of W; gather of centroid rows
+tf_status shard_plan(const double *c, int64_t n, int dim, double rmin, int W, int me, cudaStream_t s,
+                     tf_shard_s *p);
+tf_status launch_gather_rows(const double *src, int dim, const int32_t *idx, int64_t m, double *dst, cudaStream_t s);
 
 // scan.cu
 tf_status exclusive_scan_i32_i64(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s);
@@ -316,6 +336,11 @@ tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cud
 tf_status launch_sensitivity_rows(const tf_filter_s *h, const double *x, const double *dc, double *out,
                                   int64_t nrows, cudaStream_t s);
 tf_status launch_density_rows(const tf_filter_s *h, const double *x, double *out, int64_t nrows, cudaStream_t s);
+// rows [r0, r1) (NEXT-4 interior/boundary split); rows of the first window before r0 are recomputed
+tf_status launch_sensitivity_rowrange(const tf_filter_s *h, const double *x, const double *dc, double *out,
+                                      int64_t r0, int64_t r1, cudaStream_t s);
+tf_status launch_density_rowrange(const tf_filter_s *h, const double *x, double *out, int64_t r0, int64_t r1,
+                                  cudaStream_t s);
 // both filters in one pass over H (sensitivity -> sens_out, density -> dens_out)
 tf_status launch_both(const tf_filter_s *h, const double *x, const double *dc, double *sens_out, double *dens_out,
                       cudaStream_t s);

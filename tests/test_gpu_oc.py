@@ -80,3 +80,27 @@ def test_sensitivity_from_energy(tf, cfg, penal):
     got = tf.tf_sensitivity_filter_energy(f, dev(x), dev(U), penal).cpu().numpy()
     scale = np.where(ref != 0, np.abs(ref), np.abs(ref).max())
     assert np.all(np.abs(got - ref) <= 1e-10 * scale)
+
+
+@pytest.mark.parametrize("case", ["no_progress", "exhausted", "x_above_4"])
+def test_oc_termination_and_flags(tf, case):
+    """Reading R23 and the bracket-exhausted flag, bitwise with the oracle; x outside [0, 1]
+    (x > 4, where a 64-bit fixed-point sum would saturate) still matches the exact oracle."""
+    n = 5000
+    rng = np.random.default_rng(3)
+    if case == "no_progress":
+        d, dc, kw = np.full(n, 0.5), np.full(n, -1.0e4), dict(tol=1e-13)
+        vf = 0.5
+    elif case == "exhausted":
+        d, dc, kw = rng.uniform(0.5, 1.0, n), -rng.uniform(0.5, 1.5, n), dict(l2=1e-6, tol=1e-12)
+        vf = 0.1
+    else:
+        d, dc, kw = rng.uniform(4.5, 6.0, n), -rng.uniform(0.5, 1.5, n), dict(move=0.2)
+        vf = 2.0
+    ref, lref, itref, flref = oracle.oc_update(d, dc, vf, flags=True, **kw)
+    xn, lm, it, fl = tf.tf_oc_update(dev(d), dev(dc), vf, flags=True, **kw)
+    assert int(it.item()) == itref and int(fl.item()) == flref
+    assert float(lm.item()) == lref
+    np.testing.assert_array_equal(xn.cpu().numpy(), ref)
+    if case != "x_above_4":
+        assert flref != 0

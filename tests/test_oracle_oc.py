@@ -67,3 +67,28 @@ def test_compliance_sensitivity_matches_listing():
         np.testing.assert_allclose(oracle.compliance_sensitivity(x, U, penal), ref, rtol=4e-16, atol=0)
     # p = 1: dc = -U exactly
     np.testing.assert_array_equal(oracle.compliance_sensitivity(x, U, 1.0), -U)
+
+
+def test_termination_rule_no_progress():
+    """Reading R23: with tol below the fp64 spacing near lambda* the listing's loop never ends;
+    the oracle stops when l_mid rounds to l1 or l2 and flags it (bit 1)."""
+    n = 64
+    d = np.full(n, 0.5)
+    dc = np.full(n, -1.0e4)  # lambda* = -dc d^2 / vf^2 = 1e4 at vf = 0.5: spacing there ~1.8e-12
+    x, lm, it, fl = oracle.oc_update(d, dc, 0.5, tol=1e-13, flags=True)
+    assert fl & 2
+    assert it < 4096
+    assert np.nextafter(lm, np.inf) - lm > 1e-13 or np.nextafter(lm, -np.inf) - lm < -1e-13
+
+
+def test_bracket_exhausted_flag():
+    """Every step moving l1 up (the volume constraint still violated at l2) sets bit 0; a normal
+    run sets no flag."""
+    n = 100
+    d = np.full(n, 0.9)
+    dc = np.full(n, -1.0)
+    x, lm, it, fl = oracle.oc_update(d, dc, 0.1, l2=1e-6, tol=1e-12, flags=True)
+    assert fl == 1
+    assert x.sum() > 0.1 * n
+    _, _, _, fl2 = oracle.oc_update(d, dc, 0.8, flags=True)  # reachable within the move limit
+    assert fl2 == 0
