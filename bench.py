@@ -12,9 +12,12 @@ on config 5 by default (12M Kuhn-tet centroids, rmin 1.5, 20 applies; BASELINE.j
 configs[4] -- the configuration the north-star targets are quoted on), inputs resident in
 HBM. value = algorithmic bytes of the step / step time (GB/s; bytes model SURVEY.md 8(d)).
 
-Multi-GPU (`torchrun --nproc-per-node N bench.py --gpus N`): the filter does not shard in
-the 1-GPU scope, so every rank runs an independent
-replica (weak scaling); time = max over ranks; value = all ranks' bytes / that time.
+Multi-GPU (`torchrun --nproc-per-node N bench.py --gpus N`): ONE problem (the same config)
+sharded over the N ranks (NEXT-4, paper_2012_08208_b200/sharded.py): device slab plan, local build,
+and every apply with an NCCL point-to-point halo exchange overlapped with the interior rows
+(strong scaling); time = max over ranks; value = the whole problem's algorithmic bytes / that time.
+`--dry-run --gpus N` runs the same sharded step with N shards as threads on one GPU (a loopback
+transport instead of NCCL): a functional check of the multi-GPU path, not a measurement.
 
 `--impl reference` times the CPU oracle (test infrastructure, oracle/) on a bounded
 sample of the same workload instead (the reference arm of this tier).
@@ -430,6 +433,122 @@ def verify_rows(tf, c, x, dc, rmin, cd, xd, dcd, args, device, count=1000):
     return out
 
 
+def run_sharded(args):
+    """One problem over N shards (NEXT-4). A step = the device slab plan + local centroid gather +
+    local build + APPLIES x (sensitivity + density), each apply with its halo exchange. Real run:
+    one process per GPU under torchrun, NCCL transport. Dry run: N threads on one GPU, loopback."""
+    import threading
+
+    import torch
+    import paper_2012_08208_b200 as tf
+    from paper_2012_08208_b200 import sharded
+
+    c, x, dc, rmin, meta = load_workload(args.config)
+    n, dim = c.shape
+    applies = args.applies if args.applies is not None else meta["applies"]
+    if args.dry_run:
+        world, dist = args.gpus, None
+        hub = sharded.LoopbackTransport(world)
+        ranks = list(range(world))
+        device = torch.device("cuda", 0)
+        torch.cuda.set_device(device)
+    else:
+        world, rank, local = dist_env()
+        torch.cuda.set_device(local)
+        dist = init_dist("nccl")
+        ranks = [rank]
+        device = torch.device("cuda", local)
+    cd = torch.from_numpy(c).to(device)
+    xg, dcg = torch.from_numpy(x).to(device), torch.from_numpy(dc).to(device)
+    res = {}
+
+    def body(k):
+        stream = torch.cuda.Stream(device) if args.dry_run else torch.cuda.current_stream(device)
+        transport = hub.endpoint(k) if args.dry_run else sharded.DistTransport()
+        ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        with torch.cuda.stream(stream):
+            def step(record):
+                e0, e1, e2 = ev(), ev(), ev()
+                e0.record(stream)
+                sf = sharded.ShardedFilter(cd, rmin, k, world, transport)
+                e1.record(stream)
+                ids = sf.plan.owned_ids.long()
+                xo, dco = xg[ids], dcg[ids]
+                for _ in range(applies):
+                    sf.sensitivity(xo, dco)
+                    sf.density(xo)
+                e2.record(stream)
+                info = (sf.plan.n_owned, sf.plan.n_interior, sf.plan.n_halo,
+                        int(sf.filter.csr()[0][sf.plan.n_owned].item()) if sf.filter else 0)
+                sf.close()
+                return (e0, e1, e2), info
+            for _ in range(args.warmup):
+                step(False)
+            torch.cuda.synchronize(device)
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize(device)
+            t0, t1 = ev(), ev()
+            l0 = tf.kernel_launches()
+            with ClockSampler(device.index if device.index is not None else 0) as clk:
+                t0.record(stream)
+                evs = []
+                for _ in range(args.steps):
+                    e, info = step(True)
+                    evs.append(e)
+                t1.record(stream)
+                torch.cuda.synchronize(device)
+            launches = tf.kernel_launches() - l0
+        res[k] = dict(launches=launches, clocks=clk.summary(), elapsed=t0.elapsed_time(t1) / 1e3, build=[a.elapsed_time(b) / 1e3 for a, b, _ in evs],
+                      apply=[b.elapsed_time(c_) / 1e3 / applies for _, b, c_ in evs], info=info)
+
+    if args.dry_run:
+        th = [threading.Thread(target=body, args=(k,)) for k in ranks]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    else:
+        body(ranks[0])
+    mine = [res[k] for k in ranks]
+    t_max = max(r["elapsed"] for r in mine)
+    t_max = reduce_max(t_max, dist, device)
+    owned_nnz = sum(r["info"][3] for r in mine)
+    halo = [r["info"][2] for r in mine]
+    if dist:
+        t = torch.tensor([float(owned_nnz)], dtype=torch.float64, device=device)
+        dist.all_reduce(t)
+        owned_nnz = int(t.item())
+    nnz = owned_nnz  # the owned rows of all shards are the global rows
+    b_build = max(statistics.mean(r["build"]) for r in mine)
+    b_apply = max(statistics.mean(r["apply"]) for r in mine)
+    value = step_bytes(n, nnz, dim, applies) * args.steps / t_max / 1e9
+    rank0 = (args.dry_run or dist_env()[1] == 0)
+    if rank0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1 if args.dry_run else world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": meta["name"], "config_index": args.config, "n": n, "dim": dim, "rmin": rmin,
+                       "nnz": nnz, "applies_per_step": applies, "shards": world,
+                       "step": "shard plan + local build + applies x (sensitivity + density), halo exchange per apply",
+                       "l2": "inputs larger than L2 (CSR %.1f GB over all shards); no flush" % (12 * nnz / 1e9),
+                       "parallelism": f"slabs{world}" + (" (dry run: threads on one GPU, loopback transport)"
+                                                         if args.dry_run else " (NCCL point-to-point halo)")},
+            "shard": {"plan_build_ms_max": b_build * 1e3, "iteration_ms_max": b_apply * 1e3,
+                      "halo_points": halo if args.dry_run else None},
+            "dry_run": bool(args.dry_run),
+            "gpu_launches": mine[0]["launches"],
+            "clocks": mine[0]["clocks"],
+            "e2e": None,
+            "e2e_note": "the host-buffer path (tf_build_filter_host / tf_filter_iteration_host) is single-GPU; "
+                        "the sharded run keeps its inputs resident on every rank",
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def run_e2e(tf, c, x, dc, rmin, applies, n, nnz, dim, args, dist=None, ws=1, device=None):
     """Same step through the C ABI's host-buffer variants: H2D of centroids / x / dc from
     pinned memory and D2H of every filtered field inside the timed region. Under torchrun every
@@ -506,11 +625,15 @@ def main(argv=None):
     ap.add_argument("--cpu-rows", type=int, default=200000)
     ap.add_argument("--build-path", choices=["auto", "cell_list", "lattice"], default="auto")
     ap.add_argument("--no-build-cell-list", action="store_true", help="skip the build_cell_list leg")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="with --gpus N > 1: the sharded path with N shards as threads on one GPU")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: timing rules need --warmup >= 3", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and (args.dry_run or dist_env()[0] > 1):
+        run_sharded(args)
     else:
         run_ours(args)
 

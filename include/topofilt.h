@@ -246,6 +246,55 @@ TF_API tf_status tf_density_filter_rows(tf_filter h, const double *x, double *ou
 TF_API tf_status tf_filter_both(tf_filter h, const double *x, const double *dc, double *sens_out, double *dens_out,
                                 void *stream);
 
+/*
+ * tf_sensitivity_filter_range / tf_density_filter_range -- the filters for rows [r0, r1) only
+ * (NEXT-4: a shard applies its interior rows while the halo exchange is in flight, then its
+ * boundary rows). out[i] for r0 <= i < r1 equals the full call's, bitwise; rows of the row block
+ * holding r0 that precede it are rewritten with their full-call values; other rows unspecified.
+ * The sensitivity filter reads x and dc of every local index (its fused x*dc pass covers all n).
+ * 0 <= r0 <= r1 <= n (TF_ERR_INVALID otherwise). Asynchronous on `stream`.
+ */
+TF_API tf_status tf_sensitivity_filter_range(tf_filter h, const double *x, const double *dc, double *out,
+                                             int64_t r0, int64_t r1, void *stream);
+TF_API tf_status tf_density_filter_range(tf_filter h, const double *x, double *out, int64_t r0, int64_t r1,
+                                         void *stream);
+
+/*
+ * NEXT-4: slab partition of one filter problem over `nranks`
+ * GPUs, computed on the device from the global centroids (the same on every rank):
+ *   longest bounding-box axis; slabs cut at count quantiles of a 65,536-bucket histogram of that
+ *   coordinate (points with equal coordinates stay together); rank k's window = its slab widened by
+ *   rmin(1 + 1e-9) plus a rounding slack on both sides (open at the domain ends); halo of rank k =
+ *   the other ranks' points in its window; INTERIOR owned points lie at least that far inside
+ *   both faces (no neighbour outside the slab), the other owned points are BOUNDARY.
+ *   Local order: [interior | boundary | halo grouped by source rank], each ascending global id.
+ *   Send list to rank j: my owned points in j's window, ascending global id, as LOCAL indices --
+ *   the order in which rank j stores them in its halo.
+ * tf_shard_plan: centroids device fp64 [n x dim] (finite); 1 <= nranks <= 64; 0 <= rank < nranks.
+ *   Synchronises `stream` a few times (histogram, counts). Errors as tf_build_filter.
+ * tf_shard_view_get: sizes and borrowed device views (valid until tf_shard_free):
+ *   local_ids [n_owned + n_halo] int32 global ids; send_idx [sum of send counts] int32 local
+ *   indices grouped by destination rank ascending.
+ * tf_shard_counts: recv_host[k] / send_host[k] = halo points received from / sent to rank k.
+ * tf_gather_rows: dst[t*dim + d] = src[idx[t]*dim + d] for t < m (device arrays; builds the local
+ *   centroids of a shard). Asynchronous on `stream`.
+ */
+typedef struct tf_shard_s *tf_shard;
+typedef struct {
+    int32_t nranks, rank, axis;
+    double cut_lo, cut_hi;        /* this rank's slab along `axis` (-inf / +inf at the ends) */
+    int64_t n_interior, n_owned, n_halo;
+    const int32_t *local_ids;
+    const int32_t *send_idx;
+} tf_shard_view;
+TF_API tf_status tf_shard_plan(const double *centroids, int64_t n, int dim, double rmin, int32_t nranks,
+                               int32_t rank, void *stream, tf_shard *out);
+TF_API tf_status tf_shard_view_get(tf_shard s, tf_shard_view *v);
+TF_API tf_status tf_shard_counts(tf_shard s, int64_t *recv_host, int64_t *send_host);
+TF_API void tf_shard_free(tf_shard s);
+TF_API tf_status tf_gather_rows(const double *src, int32_t dim, const int32_t *idx, int64_t m, double *dst,
+                                void *stream);
+
 /* tf_free -- release everything the handle owns, stream-ordered on the stream the handle was built
  * on (cudaFreeAsync; no device-wide synchronisation). Work on that stream and on the handle's own
  * host-pipeline streams is ordered before the release; work the caller issued with h on OTHER

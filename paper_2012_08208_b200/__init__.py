@@ -29,6 +29,8 @@ EXPORTS = [
     "tf_density_filter_host", "tf_filter_from_csr", "tf_kernel_launches", "tf_debug_set_alloc_limit",
     "tf_version", "tf_build_stencil", "tf_filter_nnz", "tf_oc_update", "tf_sensitivity_filter_energy",
     "tf_filter_iteration_host", "tf_filter_both", "tf_build_lattice", "tf_halo_pack",
+    "tf_sensitivity_filter_range", "tf_density_filter_range", "tf_gather_rows",
+    "tf_shard_plan", "tf_shard_view_get", "tf_shard_counts", "tf_shard_free",
     "tf_sensitivity_filter_rows", "tf_density_filter_rows",
     # include/topofilt_helmholtz.h (NEXT-3)
     "tf_helmholtz_build", "tf_helmholtz_filter", "tf_helmholtz_sensitivity", "tf_helmholtz_view",
@@ -57,6 +59,13 @@ class tf_build_info(ctypes.Structure):
     _fields_ = [("bin_side", ctypes.c_double), ("bins", ctypes.c_int64 * 3), ("nbins", ctypes.c_int64),
                 ("max_candidates", ctypes.c_int64), ("large_rows", ctypes.c_int64),
                 ("radix_passes", ctypes.c_int32), ("path", ctypes.c_int32), ("groups", ctypes.c_int64)]
+
+
+class tf_shard_view(ctypes.Structure):
+    _fields_ = [("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("axis", ctypes.c_int32),
+                ("cut_lo", ctypes.c_double), ("cut_hi", ctypes.c_double), ("n_interior", ctypes.c_int64),
+                ("n_owned", ctypes.c_int64), ("n_halo", ctypes.c_int64), ("local_ids", ctypes.c_void_p),
+                ("send_idx", ctypes.c_void_p)]
 
 
 class tf_helmholtz_info(ctypes.Structure):
@@ -104,6 +113,13 @@ def _load():
         "tf_filter_both": ([P, P, P, P, P, P], I32),
         "tf_build_lattice": ([I32, I64, I64, I64, D, I32, P, D, P, PP], I32),
         "tf_halo_pack": ([P, P, I64, P, P], I32),
+        "tf_sensitivity_filter_range": ([P, P, P, P, I64, I64, P], I32),
+        "tf_density_filter_range": ([P, P, P, I64, I64, P], I32),
+        "tf_shard_plan": ([P, I64, I32, D, I32, I32, P, PP], I32),
+        "tf_shard_view_get": ([P, ctypes.POINTER(tf_shard_view)], I32),
+        "tf_shard_counts": ([P, P, P], I32),
+        "tf_shard_free": ([P], None),
+        "tf_gather_rows": ([P, I32, P, I64, P, P], I32),
         "tf_helmholtz_build": ([P, I64, P, I64, I32, D, P, PP], I32),
         "tf_helmholtz_filter": ([P, P, P, D, I32, P, P], I32),
         "tf_helmholtz_sensitivity": ([P, P, P, P, D, I32, P, P], I32),
@@ -366,6 +382,36 @@ def tf_density_filter_rows(f: Filter, x, out, nrows: int, stream=None):
     import torch
     _check(_lib.tf_density_filter_rows(f.handle, _dptr(x, "x", torch.float64, f.n),
                                        _dptr(out, "out", torch.float64, f.n), int(nrows), _stream_ptr(stream)))
+    return out
+
+
+def tf_sensitivity_filter_range(f: Filter, x, dc, out, r0: int, r1: int, stream=None):
+    """Rows [r0, r1) of the sensitivity filter (NEXT-4: interior rows during the halo exchange,
+    then the boundary rows)."""
+    import torch
+    _check(_lib.tf_sensitivity_filter_range(f.handle, _dptr(x, "x", torch.float64, f.n),
+                                            _dptr(dc, "dc", torch.float64, f.n),
+                                            _dptr(out, "out", torch.float64, f.n), int(r0), int(r1),
+                                            _stream_ptr(stream)))
+    return out
+
+
+def tf_density_filter_range(f: Filter, x, out, r0: int, r1: int, stream=None):
+    """Rows [r0, r1) of the density filter."""
+    import torch
+    _check(_lib.tf_density_filter_range(f.handle, _dptr(x, "x", torch.float64, f.n),
+                                        _dptr(out, "out", torch.float64, f.n), int(r0), int(r1),
+                                        _stream_ptr(stream)))
+    return out
+
+
+def tf_gather_rows(src, idx, out, stream=None):
+    """out[t] = src[idx[t]] for rows of a [*, dim] fp64 array (library kernel)."""
+    import torch
+    dim = 1 if src.dim() == 1 else src.shape[1]
+    m = idx.numel()
+    _check(_lib.tf_gather_rows(_dptr(src, "src", torch.float64), int(dim), _dptr(idx, "idx", torch.int32, m),
+                               m, _dptr(out, "out", torch.float64, m * dim), _stream_ptr(stream, src.device)))
     return out
 
 

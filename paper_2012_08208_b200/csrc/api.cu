@@ -512,6 +512,106 @@ tf_status tf_density_filter_rows(tf_filter h, const double *x, double *out, int6
     return launch_density_rows(h, x, out, nrows, (cudaStream_t)stream);
 }
 
+static tf_status check_range(const tf_filter_s *h, int64_t r0, int64_t r1) {
+    if (r0 < 0 || r1 < r0 || r1 > h->n) {
+        set_error("row range [%lld, %lld) outside [0, n = %lld]", (long long)r0, (long long)r1, (long long)h->n);
+        return TF_ERR_INVALID;
+    }
+    return TF_OK;
+}
+
+tf_status tf_sensitivity_filter_range(tf_filter h, const double *x, const double *dc, double *out, int64_t r0,
+                                      int64_t r1, void *stream) {
+    TF_TRY(check_apply(h, x, dc, out, true));
+    TF_TRY(check_range(h, r0, r1));
+    return launch_sensitivity_rowrange(h, x, dc, out, r0, r1, (cudaStream_t)stream);
+}
+
+tf_status tf_density_filter_range(tf_filter h, const double *x, double *out, int64_t r0, int64_t r1, void *stream) {
+    TF_TRY(check_apply(h, x, nullptr, out, false));
+    TF_TRY(check_range(h, r0, r1));
+    return launch_density_rowrange(h, x, out, r0, r1, (cudaStream_t)stream);
+}
+
+tf_status tf_shard_plan(const double *centroids, int64_t n, int dim, double rmin, int32_t nranks, int32_t rank,
+                        void *stream, tf_shard *out) {
+    try {
+        TF_TRY(check_build_args(n, dim, rmin, reinterpret_cast<tf_filter *>(out)));
+        if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks) {
+            set_error("tf_shard_plan: need 1 <= nranks <= 64 and 0 <= rank < nranks (got %d, %d)", nranks, rank);
+            return TF_ERR_INVALID;
+        }
+        TF_TRY(require_device(centroids, "tf_shard_plan: centroids"));
+        tf_shard_s *p = new (std::nothrow) tf_shard_s();
+        if (!p) {
+            set_error("host allocation failed");
+            return TF_ERR_NOMEM;
+        }
+        cudaGetDevice(&p->device);
+        p->nranks = nranks;
+        p->rank = rank;
+        p->stream = (cudaStream_t)stream;
+        tf_status st = shard_plan(centroids, n, dim, rmin, nranks, rank, (cudaStream_t)stream, p);
+        if (st != TF_OK) {
+            tf_shard_free(p);
+            return st;
+        }
+        *out = p;
+        return TF_OK;
+    } catch (const std::exception &e) {
+        set_error("tf_shard_plan: %s", e.what());
+        return TF_ERR_NOMEM;
+    }
+}
+
+tf_status tf_shard_view_get(tf_shard s, tf_shard_view *v) {
+    if (!s || !v) {
+        set_error("tf_shard_view_get: NULL argument");
+        return TF_ERR_INVALID;
+    }
+    v->nranks = s->nranks;
+    v->rank = s->rank;
+    v->axis = s->axis;
+    v->cut_lo = s->cut_lo;
+    v->cut_hi = s->cut_hi;
+    v->n_interior = s->n_interior;
+    v->n_owned = s->n_owned;
+    v->n_halo = s->n_halo;
+    v->local_ids = s->local_ids;
+    v->send_idx = s->send_idx;
+    return TF_OK;
+}
+
+tf_status tf_shard_counts(tf_shard s, int64_t *recv_host, int64_t *send_host) {
+    if (!s || !recv_host || !send_host) {
+        set_error("tf_shard_counts: NULL argument");
+        return TF_ERR_INVALID;
+    }
+    for (int k = 0; k < s->nranks; ++k) recv_host[k] = s->recv[k], send_host[k] = s->send[k];
+    return TF_OK;
+}
+
+void tf_shard_free(tf_shard s) {
+    if (!s) return;
+    DeviceScope on(s->device);
+    if (s->local_ids) cudaFreeAsync(s->local_ids, s->stream);
+    if (s->send_idx) cudaFreeAsync(s->send_idx, s->stream);
+    cudaGetLastError();
+    delete s;
+}
+
+tf_status tf_gather_rows(const double *src, int32_t dim, const int32_t *idx, int64_t m, double *dst, void *stream) {
+    if (dim < 1 || dim > 3 || m < 0) {
+        set_error("tf_gather_rows: need 1 <= dim <= 3 and m >= 0");
+        return TF_ERR_INVALID;
+    }
+    if (m == 0) return TF_OK;
+    TF_TRY(require_device(src, "tf_gather_rows: src"));
+    TF_TRY(require_device(idx, "tf_gather_rows: idx"));
+    TF_TRY(require_device(dst, "tf_gather_rows: dst"));
+    return launch_gather_rows(src, dim, idx, m, dst, (cudaStream_t)stream);
+}
+
 tf_status tf_filter_both(tf_filter h, const double *x, const double *dc, double *sens_out, double *dens_out,
                          void *stream) {
     TF_TRY(check_apply(h, x, dc, sens_out, true));

@@ -1,10 +1,10 @@
-"""NEXT-4 on the GPU: the slab-sharded filter (paper_2012_08208_b200/sharded.py) emulated with K
-shards in one process on one GPU -- every shard builds its local filter with the library,
-packs its boundary values with tf_halo_pack, receives its halo from the other shards' packed
-buffers and applies the library filter; the assembled owned rows equal the unsharded filter
-and the oracle to 1e-10 (only the summation order differs). The transport itself (NCCL/gloo
-point-to-point) is exercised by tests/test_multirank.py."""
-import ctypes
+"""NEXT-4 end to end on one GPU: W shards of one filter problem run as threads of one process,
+each calling ShardedFilter.sensitivity / density (device plan, local build, tf_halo_pack, the
+exchange through LoopbackTransport, interior rows then boundary rows with tf_*_filter_range); the
+assembled owned rows equal the unsharded filter and the oracle to 1e-10 (only the summation order
+differs). The NCCL transport (DistTransport) is the same interface; the gloo test in
+tests/test_multirank.py exercises it across processes."""
+import threading
 
 import numpy as np
 import pytest
@@ -35,62 +35,88 @@ def assert_rel(g, r, what):
     assert not bad.any(), f"{what}: {bad.sum()} of {r.size} outside {RTOL}"
 
 
-def emulate(tf, c, rmin, x, dc, world):
+def run_shards(c, rmin, x, dc, world, iters=2):
+    """Every shard in its own thread (own CUDA stream); returns the assembled global outputs."""
     from paper_2012_08208_b200 import sharded
-    plans = sharded.make_plans(c, world, rmin)
-    shards = [sharded.ShardedFilter(c, rmin, k, world, plan=plans[k]) for k in range(world)]
-    xo = [dev(x[p.owned]) for p in plans]
-    dco = [dev(dc[p.owned]) for p in plans]
-    sens, dens = np.empty_like(x), np.empty_like(x)
-    packs = [sh.pack(xo[k], dco[k]) for k, sh in enumerate(shards)]
-    for k, sh in enumerate(shards):
-        rec = {j: packs[j][k] for j in sh.plan.halo_from}
-        sens[plans[k].owned] = sh.apply_with_halo(xo[k], dco[k], rec).cpu().numpy()
-    packs = [sh.pack(xo[k]) for k, sh in enumerate(shards)]
-    for k, sh in enumerate(shards):
-        rec = {j: packs[j][k] for j in sh.plan.halo_from}
-        dens[plans[k].owned] = sh.apply_with_halo(xo[k], None, rec, density=True).cpu().numpy()
-    for sh in shards:
-        sh.close()
-    return sens, dens, plans
+    hub = sharded.LoopbackTransport(world)
+    cd = dev(c)
+    sens, dens = np.full_like(x, np.nan), np.full_like(x, np.nan)
+    errs = []
+    stats = {}
+
+    def work(k):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                sf = sharded.ShardedFilter(cd, rmin, k, world, hub.endpoint(k))
+                ids = sf.plan.owned_ids.long()
+                xo, dco = dev(x)[ids], dev(dc)[ids]
+                for _ in range(iters):  # repeated calls reuse the buffers
+                    s = sf.sensitivity(xo, dco).clone()
+                    d = sf.density(xo).clone()
+                torch.cuda.current_stream().synchronize()
+                idn = ids.cpu().numpy()
+                sens[idn] = s.cpu().numpy()
+                dens[idn] = d.cpu().numpy()
+                stats[k] = (sf.plan.n_interior, sf.plan.n_owned, sf.plan.n_halo)
+                sf.close()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            hub.barrier.abort()
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return sens, dens, stats
 
 
-@pytest.mark.parametrize("case,world", [("c2", 2), ("c3", 4), ("kuhn", 3), ("random", 8), ("c3", 13)])
-def test_sharded_equals_unsharded(tf, case, world):
-    if case == "kuhn":
-        c, rmin = synth.kuhn_tets(30, 20, 16), 1.5
-        x = synth.uniform(910, 0, c.shape[0], 0.001, 1.0)
-        dc = (-3.0 * (x * x)) * synth.uniform(911, 0, c.shape[0], 0.5, 1.5)
+@pytest.mark.parametrize("case,world", [("c2", 2), ("c3", 4), ("kuhn_jitter", 3), ("random", 8),
+                                        ("ground", 2), ("c3", 13)])
+def test_sharded_equals_unsharded_and_oracle(tf, case, world):
+    if case == "kuhn_jitter":
+        c = synth.kuhn_mesh(12, 8, 6, jitter=0.15, stream=77)[0]
+        rmin = 1.5
     elif case == "random":
-        c, rmin = synth.random_points(912, 200_000, 3, 0.0, 40.0), 1.2
-        x = synth.uniform(913, 0, c.shape[0], 0.001, 1.0)
-        dc = -synth.uniform(914, 0, c.shape[0], 0.0, 1.0)
+        c = synth.random_points(909, 30000, 3, 0.0, 30.0)
+        rmin = 1.7
+    elif case == "ground":
+        c = synth.ground_structure(4, 400, 300)[0]
+        rmin = 3.0
     else:
-        c, x, dc, rmin = synth.workload(int(case[1]))
-    sens, dens, plans = emulate(tf, c, rmin, x, dc, world)
-    assert sum(p.n_halo for p in plans) > 0
+        c, _, _, rmin = synth.workload(int(case[1]))
+    n = c.shape[0]
+    x = synth.uniform(910, 0, n, 0.001, 1.0)
+    dc = -synth.uniform(911, 0, n, 0.5, 1.5) * x * x
+    sens, dens, stats = run_shards(c, rmin, x, dc, world)
+    assert sum(v[1] for v in stats.values()) == n
+    assert any(v[0] < v[1] for v in stats.values()) or world == 1  # boundary rows exist
     f = tf.tf_build_filter(dev(c), rmin)
-    assert_rel(sens, f.sensitivity(dev(x), dev(dc)).cpu().numpy(), f"{case}/{world} sharded sensitivity")
-    assert_rel(dens, f.density(dev(x)).cpu().numpy(), f"{case}/{world} sharded density")
+    assert_rel(sens, f.sensitivity(dev(x), dev(dc)).cpu().numpy(), f"{case}/{world} vs unsharded sensitivity")
+    assert_rel(dens, f.density(dev(x)).cpu().numpy(), f"{case}/{world} vs unsharded density")
     f.close()
-    if case in ("c2", "kuhn"):
-        H = oracle.build_celllist(c, rmin)
-        assert_rel(sens, oracle.apply_sensitivity(H, x, dc), "oracle sensitivity")
-        assert_rel(dens, oracle.apply_density(H, x), "oracle density")
+    if n <= 200_000:
+        ref = oracle.build_celllist(c, rmin)
+        assert_rel(sens, oracle.apply_sensitivity(ref, x, dc), f"{case}/{world} vs oracle sensitivity")
+        assert_rel(dens, oracle.apply_density(ref, x), f"{case}/{world} vs oracle density")
 
 
-def test_halo_pack(tf):
-    src = synth.uniform(915, 0, 10_000, -1.0, 1.0)
-    idx = np.asarray(synth.sample_rows(3, 10_000, 777), dtype=np.int32)
-    d = torch.empty(idx.shape[0], dtype=torch.float64, device="cuda")
-    s, i = dev(src), dev(idx)
-    tf._check(tf.lib().tf_halo_pack(ctypes.c_void_p(s.data_ptr()), ctypes.c_void_p(i.data_ptr()), idx.shape[0],
-                                    ctypes.c_void_p(d.data_ptr()), None))
-    assert np.array_equal(d.cpu().numpy(), src[idx])
-    assert tf.lib().tf_halo_pack(None, None, 0, None, None) == tf.TF_OK  # m = 0: no-op
+def test_filter_range_matches_full(tf):
+    """tf_*_filter_range: rows [r0, r1) bitwise the full call's, for ranges starting inside a row
+    block, empty ranges and the whole range."""
+    c = synth.random_points(912, 50000, 3, 0.0, 40.0)
+    rmin = 1.6
+    n = c.shape[0]
+    f = tf.tf_build_filter(dev(c), rmin)
+    x, dc = dev(synth.uniform(913, 0, n, 0.001, 1.0)), dev(-synth.uniform(914, 0, n, 0.0, 1.0))
+    full_s, full_d = f.sensitivity(x, dc), f.density(x)
+    for r0, r1 in [(0, n), (1234, 1234), (1, 17), (777, 40001), (n - 5, n)]:
+        out_s, out_d = torch.full_like(x, float("nan")), torch.full_like(x, float("nan"))
+        tf.tf_sensitivity_filter_range(f, x, dc, out_s, r0, r1)
+        tf.tf_density_filter_range(f, x, out_d, r0, r1)
+        assert torch.equal(out_s[r0:r1], full_s[r0:r1]) and torch.equal(out_d[r0:r1], full_d[r0:r1])
     with pytest.raises(tf.TopofiltError):
-        tf._check(tf.lib().tf_halo_pack(ctypes.c_void_p(src.ctypes.data), ctypes.c_void_p(i.data_ptr()), 5,
-                                        ctypes.c_void_p(d.data_ptr()), None))
-    with pytest.raises(tf.TopofiltError):
-        tf._check(tf.lib().tf_halo_pack(ctypes.c_void_p(s.data_ptr()), ctypes.c_void_p(i.data_ptr()), -1,
-                                        ctypes.c_void_p(d.data_ptr()), None))
+        tf.tf_density_filter_range(f, x, torch.empty_like(x), 5, 3)
+    f.close()

@@ -87,33 +87,25 @@ def test_reference_arm_rank_gating(tmp_path):
 
 
 def _halo_worker(rank, world, port, q):
-    """NEXT-4 transport: each rank sends the owned values its neighbours' halos need and
-    receives its own halo through DistTransport (batch_isend_irecv) over gloo."""
+    """NEXT-4 transport: every rank posts one send per peer and one receive per peer through
+    DistTransport (batch_isend_irecv) over gloo, with the sharded filter's buffer layout
+    ([x | dc] per peer, sizes differing per pair), then waits; received values are checked."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     sys.path.insert(0, ROOT)
     import numpy as np
     import torch
     import torch.distributed as dist
 
-    import synth
     from paper_2012_08208_b200 import sharded
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    c = synth.random_points(906, 3000, 3, 0.0, 12.0)
-    xg = synth.uniform(907, 0, c.shape[0], 0.0, 1.0)
-    plan = sharded.make_plans(c, world, 1.4)[rank]
-    x_owned = torch.from_numpy(xg[plan.owned])
-    # the GPU path packs with tf_halo_pack; here the same gather on CPU tensors
-    sends = {j: [x_owned[torch.from_numpy(idx.astype(np.int64))].contiguous()] for j, idx in plan.send_to.items()}
-    x_loc = torch.zeros(plan.n_owned + plan.n_halo, dtype=torch.float64)
-    x_loc[:plan.n_owned] = x_owned
-    recvs = {}
-    for j, g in plan.halo_from.items():
-        o = plan.halo_offset(j)
-        recvs[j] = [x_loc[o:o + g.shape[0]]]
-    sharded.DistTransport().exchange(sends, recvs)
-    ok = bool(np.array_equal(x_loc.numpy(), xg[plan.local_ids()]))
-    q.put((rank, ok, plan.n_halo, sorted(plan.halo_from)))
+    size = lambda a, b: 3 + 5 * a + 7 * b  # noqa: E731  points rank a sends to rank b
+    val = lambda a, b, m: torch.arange(2 * m, dtype=torch.float64) + 1000.0 * a + 100.0 * b  # noqa: E731
+    sends = {j: val(rank, j, size(rank, j)) for j in range(world) if j != rank}
+    recvs = {j: torch.zeros(2 * size(j, rank), dtype=torch.float64) for j in range(world) if j != rank}
+    sharded.DistTransport().exchange(sends, recvs).wait()
+    ok = all(bool(torch.equal(recvs[j], val(j, rank, size(j, rank)))) for j in recvs)
+    q.put((rank, ok, sum(t.numel() for t in recvs.values()), sorted(recvs)))
     dist.barrier()
     dist.destroy_process_group()
 
