@@ -195,7 +195,9 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                                                                       int64_t nwin, double *tbuf, int64_t n,
                                                                       double penal, int energy, int64_t wbeg,
                                                                       int64_t wend, int tpass, int64_t row_limit) {
-    constexpr bool SENS = MODE != 0, BOTH = MODE == 2;
+    // MODE 3: sensitivity without the t pass (ordinary launch): each entry gathers x_j and dc_j and
+    // forms t_j = x_j * dc_j itself (the same product, so the same sums bit for bit)
+    constexpr bool SENS = MODE != 0, BOTH = MODE == 2, DIRECT = MODE == 3;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *svals = reinterpret_cast<double *>(smem_raw);                           // [kStages][kStage]
     int64_t *srow = reinterpret_cast<int64_t *>(svals + kStages * kStage);          // [kStages][kRowCap]
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
         // prologue: the first kStages windows need no empty-wait (overlaps the t pass)
         if (lane == 0)
             for (; w < wend && rb[w] < row_limit && it < kStages; w += gridDim.x, ++it) issue(it);
-        if (SENS && tpass) {
+        if (SENS && !DIRECT && tpass == 1) {
             __syncwarp();
             cooperative_groups::this_grid().sync();
         }
@@ -261,7 +263,12 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
     }
 
     // ---------------- consumers
-    if (SENS && tpass) {
+    if (SENS && !DIRECT && tpass == 2) {
+        // t comes from the preceding k_tpass launch (programmatic dependent launch): the producer
+        // has been staging CSR windows already; the gathers wait for that grid's results
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
+    if (SENS && !DIRECT && tpass == 1) {
         // fused Hadamard pass t = x o dc (PAPER.md:447 np.multiply(density, sensitivity)),
         // then a grid-wide barrier: the SpMV gathers one array instead of two
         // NEXT-2 (energy != 0): dc is evaluated here from the element energies U passed in `dc`,
@@ -285,7 +292,7 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
         cooperative_groups::this_grid().sync();
     }
     // t was written in this launch: read it with plain cached loads, never the read-only path
-    const double *gsrc = SENS ? tbuf : x;
+    const double *gsrc = (SENS && !DIRECT) ? tbuf : x;
     const double2 *gtx = reinterpret_cast<const double2 *>(tbuf);  // BOTH: (t, x) pairs
     constexpr int RPW = 32 / G;  // rows per warp claim
     const int sub = lane & (G - 1);
@@ -338,6 +345,15 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                         }
 #pragma unroll
                         for (int u = 0; u < U; ++u) acc2 = fma(v[u], xg[u], acc2);
+                    } else if (DIRECT) {
+                        double dg[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            t[u] = (j[u] >= 0) ? __ldg(x + j[u]) : 0.0;
+                            dg[u] = (j[u] >= 0) ? __ldg(dc + j[u]) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) t[u] *= dg[u];
                     } else {
 #pragma unroll
                         for (int u = 0; u < U; ++u) t[u] = (j[u] >= 0) ? __ldca(gsrc + j[u]) : 0.0;
@@ -350,6 +366,8 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                             const double2 p = __ldca(gtx + jj);
                             acc = fma(sv[i], p.x, acc);
                             acc2 = fma(sv[i], p.y, acc2);
+                        } else if (DIRECT) {
+                            acc = fma(sv[i], __ldg(x + jj) * __ldg(dc + jj), acc);
                         } else {
                             acc = fma(sv[i], __ldca(gsrc + jj), acc);
                         }
@@ -381,6 +399,8 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                         const double2 p = __ldca(gtx + jj);
                         acc = fma(vals[k], p.x, acc);
                         acc2 = fma(vals[k], p.y, acc2);
+                    } else if (DIRECT) {
+                        acc = fma(vals[k], __ldg(x + jj) * __ldg(dc + jj), acc);
                     } else {
                         acc = fma(vals[k], __ldca(gsrc + jj), acc);
                     }
@@ -400,6 +420,16 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
     }
 }
 
+// t = x o dc as its own launch, for the programmatic-dependent sensitivity apply: it lets the
+// dependent SpMV grid launch at once (griddepcontrol.launch_dependents), so the SpMV's producers
+// stage the first CSR windows while this pass runs.
+__global__ void __launch_bounds__(256) k_tpass(const double *__restrict__ x, const double *__restrict__ dc,
+                                               double *__restrict__ t, int64_t n) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        t[i] = x[i] * dc[i];
+}
+
 // Windows [wbeg, wend) of the plan. SENS: tbuf == nullptr -> per-call scratch, t pass and a
 // cooperative launch (the normal API); tbuf given -> tpass selects whether this launch computes
 // t (cooperative) or reuses it (ordinary launch; the row-range chunks of the host pipeline).
@@ -407,7 +437,7 @@ template <int MODE, int G, int U>
 tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc, double *out, double *out2,
                          cudaStream_t s, double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf_ext,
                          int tpass, int64_t row_limit) {
-    constexpr bool SENS = MODE != 0;
+    constexpr bool SENS = MODE == 1 || MODE == 2;  // modes with the cooperative t pass
     const size_t smem = (size_t)kStages * (kStage * (sizeof(double) + sizeof(int32_t)) + kRowCap * sizeof(int64_t));
     auto kern = k_spmv<MODE, G, U>;
     // per-instantiation, per-device attribute (dynamic shared memory above 48 KB needs the
@@ -440,6 +470,34 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
     const int64_t *wlo = h->plan.wlo;
     int64_t nwin = h->plan.nblocks, n = h->n;
     double *tbuf = tbuf_ext;
+    if (MODE == 1 && !energy && tbuf_ext == nullptr && h->plan.pdl) {
+        // t pass as its own launch + the SpMV as a programmatic dependent launch (no cooperative
+        // launch, no grid-wide barrier; CSR staging overlaps the t pass)
+        TF_TRY(dalloc(&tbuf, (size_t)n, s, "sensitivity scratch t = x*dc"));
+        const unsigned tg = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)h->plan.grid * 2);
+        k_tpass<<<tg, 256, 0, s>>>(x, dc, tbuf, n);
+        TF_LAUNCH_CHECK();
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kThreads + 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const int tp = 2;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, rowptr, cols, vals, hs, x, dc, out, out2, rb, wlo, nwin,
+                                           tbuf, n, penal, energy, wbeg, wend, tp, row_limit);
+        count_launch();
+        dev_free(tbuf, s);
+        if (e != cudaSuccess) {
+            set_error("programmatic dependent launch failed: %s", cudaGetErrorString(e));
+            return TF_ERR_CUDA;
+        }
+        return TF_OK;
+    }
     if (SENS && (tbuf_ext == nullptr || tpass)) {
         // per-call scratch (stream-ordered) unless the caller owns it: concurrent applies on
         // different streams stay safe
@@ -469,7 +527,7 @@ template <int MODE, int G>
 tf_status launch_spmv_g(const tf_filter_s *h, const double *x, const double *dc, double *out, double *out2,
                         cudaStream_t s, double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf,
                         int tpass, int64_t row_limit) {
-    if ((MODE == 0 ? h->plan.unroll : MODE == 1 ? h->plan.unroll_sens : h->plan.unroll_both) >= 8)
+    if ((MODE == 0 ? h->plan.unroll : (MODE == 1 || MODE == 3) ? h->plan.unroll_sens : h->plan.unroll_both) >= 8)
         return launch_spmv_gu<MODE, G, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
     return launch_spmv_gu<MODE, G, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
 }
@@ -584,6 +642,15 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
         if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) h->plan.group = v;
     }
     h->plan.unroll_sens = h->plan.unroll;
+    // sensitivity without the t pass (two gathers per entry): measured slower at every size
+    // (config 3 84 vs 79 us, config 4 113 vs 102 us): off; tuning knob TOPOFILT_SENS_DIRECT_N (rows)
+    h->plan.direct_rows = 0;
+    if (const char *e = getenv("TOPOFILT_SENS_DIRECT_N")) h->plan.direct_rows = atoll(e);
+    // sensitivity as t pass + programmatic dependent SpMV launch (cold, in-event: config 3
+    // 79 -> 74 us, config 4 102 -> 98.6 us, config 5 2178 -> 2159 us in the bench step; knob
+    // TOPOFILT_SENS_PDL=0 restores the cooperative single launch)
+    h->plan.pdl = 1;
+    if (const char *e = getenv("TOPOFILT_SENS_PDL")) h->plan.pdl = atoi(e) != 0;
     if (const char *e = getenv("TOPOFILT_APPLY_U")) h->plan.unroll = h->plan.unroll_sens = atoi(e) >= 8 ? 8 : 4;
     if (const char *e = getenv("TOPOFILT_APPLY_U_SENS")) h->plan.unroll_sens = atoi(e) >= 8 ? 8 : 4;
     const unsigned grid = (unsigned)std::min<int64_t>((nblocks + 256) / 256, 65535);
@@ -678,6 +745,7 @@ tf_status launch_sensitivity(const tf_filter_s *h, const double *x, const double
                              cudaStream_t s) {
     NvtxRange r("tf_apply/sensitivity");
     if (h->stencil.K > 0) return launch_stencil(h, x, dc, out, true, s);
+    if (h->n <= h->plan.direct_rows) return launch_spmv<3>(h, x, dc, out, s);  // no t pass, ordinary launch
     return launch_spmv<1>(h, x, dc, out, s);
 }
 

@@ -212,6 +212,8 @@ struct ApplyPlan {
     int unroll = 4;           // loads in flight per lane in the row loop (4 or 8): density
     int unroll_sens = 4;      // the same for the sensitivity launches
     int unroll_both = 4;      // the same for the both-filters launches (16-byte gathers)
+    int64_t direct_rows = 0;  // sensitivity applies on filters with n <= this skip the t pass
+    int pdl = 0;              // sensitivity: t pass + programmatic dependent SpMV launch
     // row-range chunks of the host pipeline: windows [chunk_w[i], chunk_w[i+1]) cover rows
     // [chunk_r[i], chunk_r[i+1])
     int nchunks = -1;  // -1: not computed yet
