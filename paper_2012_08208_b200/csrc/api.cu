@@ -7,6 +7,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -41,6 +42,33 @@ tf_status dev_alloc(void **p, size_t bytes, cudaStream_t s, const char *what) {
         return (e == cudaErrorMemoryAllocation) ? TF_ERR_NOMEM : TF_ERR_CUDA;
     }
     return TF_OK;
+}
+
+static std::mutex g_pin_mu;
+static unsigned long long *g_pin_block = nullptr;
+static std::vector<unsigned long long *> g_pin_free;
+
+unsigned long long *pinned_slot_acquire() {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_block) {
+        constexpr int kSlots = 256;
+        if (cudaMallocHost((void **)&g_pin_block, (size_t)kSlots * 4 * sizeof(unsigned long long)) != cudaSuccess) {
+            cudaGetLastError();
+            g_pin_block = nullptr;
+            return nullptr;
+        }
+        for (int i = kSlots - 1; i >= 0; --i) g_pin_free.push_back(g_pin_block + 4 * i);
+    }
+    if (g_pin_free.empty()) return nullptr;
+    unsigned long long *p = g_pin_free.back();
+    g_pin_free.pop_back();
+    return p;
+}
+
+void pinned_slot_release(unsigned long long *p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(p);
 }
 
 void dev_free(void *p, cudaStream_t s) {
@@ -175,6 +203,7 @@ static void destroy(tf_filter_s *h) {
     }
     if (h->ev) cudaEventDestroy(h->ev);
     if (h->ev2) cudaEventDestroy(h->ev2);
+    if (h->lat_check) pinned_slot_release(h->lat_check);
     cudaGetLastError();  // nothing to report from a void call
     delete h;
 }
@@ -228,6 +257,38 @@ static tf_status build_common(const double *c, int64_t n, int dim, double rmin, 
             st = TF_ERR_CUDA;
         }
     }
+    if (st == TF_OK && h->lat_pending && !lattice_check_ok(h)) {
+        // the speculative exact lattice build did not hold up (verification or fill check): redo
+        // it without speculation (tested lattice mode or the cell list)
+        tf_filter_s *g = new (std::nothrow) tf_filter_s();
+        if (!g) {
+            destroy(h);
+            set_error("host allocation failed");
+            return TF_ERR_NOMEM;
+        }
+        g->device = h->device;
+        g->stream = s;
+        g->n = n;
+        g->dim = dim;
+        g->rmin = rmin;
+        destroy(h);
+        h = g;
+        st = build_filter_device(c, n, dim, rmin, flags | kBuildNoSpeculation, s, h);
+        h->cols_ascending = true;
+        if (st == TF_OK) st = make_apply_plan(h, s);
+        if (st == TF_OK) {
+            cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) {
+                set_error("tf_build_filter: %s", cudaGetErrorString(e));
+                st = TF_ERR_CUDA;
+            }
+        }
+    }
+    if (h->lat_check) {
+        pinned_slot_release(h->lat_check);
+        h->lat_check = nullptr;
+    }
+    h->lat_pending = false;
     build_trace().report(st == TF_OK ? "tf_build_filter" : "tf_build_filter (failed)");
     if (st != TF_OK) {
         destroy(h);

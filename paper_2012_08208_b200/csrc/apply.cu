@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
                                                                       const int64_t *__restrict__ wlo,
                                                                       int64_t nwin, double *tbuf, int64_t n,
                                                                       double penal, int energy, int64_t wbeg,
-                                                                      int64_t wend, int tpass, int64_t row_limit) {
+                                                                      int64_t wend, int tpass, int64_t row_limit,
+                                                                      int64_t row_begin) {
     // MODE 3: sensitivity without the t pass (ordinary launch): each entry gathers x_j and dc_j and
     // forms t_j = x_j * dc_j itself (the same product, so the same sums bit for bit)
     constexpr bool SENS = MODE != 0, BOTH = MODE == 2, DIRECT = MODE == 3;
@@ -204,7 +205,23 @@ __global__ void __launch_bounds__(kThreads + 32, kBlocksPerSM) k_spmv(const int6
     int32_t *scols = reinterpret_cast<int32_t *>(srow + kStages * kRowCap);         // [kStages][kStage]
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
     __shared__ int next_row[kStages];
+    __shared__ int64_t s_wbeg;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (row_begin > 0) {
+        // rows [row_begin, row_limit): start at the window holding row_begin (binary search of
+        // the row-block table; its rows before row_begin are recomputed with the same values)
+        if (tid == 0) {
+            int64_t lo = wbeg, hi = wend;  // first w in [wbeg, wend) with rb[w + 1] > row_begin
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (rb[mid + 1] <= row_begin) lo = mid + 1;
+                else hi = mid;
+            }
+            s_wbeg = lo;
+        }
+        __syncthreads();
+        wbeg = s_wbeg;
+    }
     if (tid == 0) {
         for (int st = 0; st < kStages; ++st) {
             mbar_init(&full[st], 1);
@@ -436,7 +453,7 @@ __global__ void __launch_bounds__(256) k_tpass(const double *__restrict__ x, con
 template <int MODE, int G, int U>
 tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc, double *out, double *out2,
                          cudaStream_t s, double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf_ext,
-                         int tpass, int64_t row_limit) {
+                         int tpass, int64_t row_limit, int64_t row_begin) {
     constexpr bool SENS = MODE == 1 || MODE == 2;  // modes with the cooperative t pass
     const size_t smem = (size_t)kStages * (kStage * (sizeof(double) + sizeof(int32_t)) + kRowCap * sizeof(int64_t));
     auto kern = k_spmv<MODE, G, U>;
@@ -489,7 +506,7 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
         cfg.numAttrs = 1;
         const int tp = 2;
         cudaError_t e = cudaLaunchKernelEx(&cfg, kern, rowptr, cols, vals, hs, x, dc, out, out2, rb, wlo, nwin,
-                                           tbuf, n, penal, energy, wbeg, wend, tp, row_limit);
+                                           tbuf, n, penal, energy, wbeg, wend, tp, row_limit, row_begin);
         count_launch();
         dev_free(tbuf, s);
         if (e != cudaSuccess) {
@@ -507,7 +524,7 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
                         (void *)&dc,     (void *)&out,  (void *)&out2,  (void *)&rb,     (void *)&wlo,
                         (void *)&nwin,
                         (void *)&tbuf,   (void *)&n,    (void *)&penal, (void *)&energy, (void *)&wbeg,
-                        (void *)&wend,   (void *)&tpass, (void *)&row_limit};
+                        (void *)&wend,   (void *)&tpass, (void *)&row_limit, (void *)&row_begin};
         cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads + 32), args, smem, s);
         count_launch();
         if (!tbuf_ext) dev_free(tbuf, s);
@@ -518,7 +535,7 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
         return TF_OK;
     }
     kern<<<grid, kThreads + 32, smem, s>>>(rowptr, cols, vals, hs, x, dc, out, out2, rb, wlo, nwin, tbuf, n, penal,
-                                           energy, wbeg, wend, 0, row_limit);
+                                           energy, wbeg, wend, 0, row_limit, row_begin);
     TF_LAUNCH_CHECK();
     return TF_OK;
 }
@@ -526,25 +543,25 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
 template <int MODE, int G>
 tf_status launch_spmv_g(const tf_filter_s *h, const double *x, const double *dc, double *out, double *out2,
                         cudaStream_t s, double penal, int energy, int64_t wbeg, int64_t wend, double *tbuf,
-                        int tpass, int64_t row_limit) {
+                        int tpass, int64_t row_limit, int64_t row_begin) {
     if ((MODE == 0 ? h->plan.unroll : (MODE == 1 || MODE == 3) ? h->plan.unroll_sens : h->plan.unroll_both) >= 8)
-        return launch_spmv_gu<MODE, G, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
-    return launch_spmv_gu<MODE, G, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
+        return launch_spmv_gu<MODE, G, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit, row_begin);
+    return launch_spmv_gu<MODE, G, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit, row_begin);
 }
 
 template <int MODE>
 tf_status launch_spmv(const tf_filter_s *h, const double *x, const double *dc, double *out, cudaStream_t s,
                       double penal = 0.0, int energy = 0, int64_t wbeg = 0, int64_t wend = -1,
                       double *tbuf = nullptr, int tpass = 1, double *out2 = nullptr,
-                      int64_t row_limit = INT64_MAX) {
+                      int64_t row_limit = INT64_MAX, int64_t row_begin = 0) {
     if (wend < 0) wend = h->plan.nblocks;
     switch (h->plan.group) {
-        case 1: return launch_spmv_g<MODE, 1>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
-        case 2: return launch_spmv_g<MODE, 2>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
-        case 4: return launch_spmv_g<MODE, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
-        case 8: return launch_spmv_g<MODE, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
-        case 16: return launch_spmv_g<MODE, 16>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
-        default: return launch_spmv_g<MODE, 32>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit);
+        case 1: return launch_spmv_g<MODE, 1>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit, row_begin);
+        case 2: return launch_spmv_g<MODE, 2>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit, row_begin);
+        case 4: return launch_spmv_g<MODE, 4>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit, row_begin);
+        case 8: return launch_spmv_g<MODE, 8>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit, row_begin);
+        case 16: return launch_spmv_g<MODE, 16>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit, row_begin);
+        default: return launch_spmv_g<MODE, 32>(h, x, dc, out, out2, s, penal, energy, wbeg, wend, tbuf, tpass, row_limit, row_begin);
     }
 }
 
@@ -658,10 +675,7 @@ tf_status make_apply_plan(tf_filter_s *h, cudaStream_t s) {
     TF_LAUNCH_CHECK();
     k_plan_windows<<<grid, 256, 0, s>>>(h->rowptr, h->plan.rb, nblocks, h->plan.wlo);
     TF_LAUNCH_CHECK();
-    // host copy of the row-block table; valid after the build's final stream synchronisation
-    h->plan.rb_host.resize(nblocks + 1);
-    TF_CUDA_TRY(cudaMemcpyAsync(h->plan.rb_host.data(), h->plan.rb, (nblocks + 1) * sizeof(int32_t),
-                                cudaMemcpyDeviceToHost, s));
+
     h->plan.nchunks = -1;  // host-pipeline chunks: computed on first use (ensure_chunk_plan)
     return TF_OK;
 }
@@ -780,21 +794,15 @@ tf_status launch_density_rows(const tf_filter_s *h, const double *x, double *out
     return launch_spmv<0>(h, x, nullptr, out, s, 0.0, 0, 0, -1, nullptr, 1, nullptr, nrows);
 }
 
-// Rows [r0, r1): windows from the one holding r0 (its rows before r0 are recomputed -- the same
-// values) to the first whose first row is >= r1. The sensitivity t pass covers all n entries.
-static int64_t window_of_row(const tf_filter_s *h, int64_t r0) {
-    const std::vector<int32_t> &rb = h->plan.rb_host;
-    if (rb.empty()) return 0;
-    const auto it = std::upper_bound(rb.begin(), rb.end(), (int32_t)r0);
-    return std::max<int64_t>(0, (int64_t)(it - rb.begin()) - 1);
-}
-
+// Rows [r0, r1): windows from the one holding r0 (found by each block with a binary search of
+// the row-block table; its rows before r0 are recomputed with the same values) to the first whose
+// first row is >= r1. The sensitivity t pass covers all n entries.
 tf_status launch_sensitivity_rowrange(const tf_filter_s *h, const double *x, const double *dc, double *out,
                                       int64_t r0, int64_t r1, cudaStream_t s) {
     NvtxRange r("tf_apply/sensitivity_range");
     if (r1 <= r0) return TF_OK;
     if (h->stencil.K > 0) return launch_stencil(h, x, dc, out, true, s);
-    return launch_spmv<1>(h, x, dc, out, s, 0.0, 0, window_of_row(h, r0), -1, nullptr, 1, nullptr, r1);
+    return launch_spmv<1>(h, x, dc, out, s, 0.0, 0, 0, -1, nullptr, 1, nullptr, r1, r0);
 }
 
 tf_status launch_density_rowrange(const tf_filter_s *h, const double *x, double *out, int64_t r0, int64_t r1,
@@ -802,7 +810,7 @@ tf_status launch_density_rowrange(const tf_filter_s *h, const double *x, double 
     NvtxRange r("tf_apply/density_range");
     if (r1 <= r0) return TF_OK;
     if (h->stencil.K > 0) return launch_stencil(h, x, nullptr, out, false, s);
-    return launch_spmv<0>(h, x, nullptr, out, s, 0.0, 0, window_of_row(h, r0), -1, nullptr, 1, nullptr, r1);
+    return launch_spmv<0>(h, x, nullptr, out, s, 0.0, 0, 0, -1, nullptr, 1, nullptr, r1, r0);
 }
 
 tf_status launch_density(const tf_filter_s *h, const double *x, double *out, cudaStream_t s) {

@@ -913,9 +913,11 @@ tf_status launch_fill_warp(const SortedPts &P, const uint32_t *keys, const Grid 
 
 tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, int flags, cudaStream_t s,
                               tf_filter_s *h) {
+    const bool speculate = (flags & kBuildNoSpeculation) == 0;
+    flags &= ~kBuildNoSpeculation;
     if (flags != TF_BUILD_CELL_LIST && flags != TF_BUILD_CELL_LIST_BINS) {
         bool used = false;
-        TF_TRY(build_lattice_csr(c, n, dim, rmin, s, h, &used));
+        TF_TRY(build_lattice_csr(c, n, dim, rmin, s, h, &used, speculate));
         if (used) return TF_OK;
         if (flags == TF_BUILD_LATTICE) {
             set_error("tf_build_filter_ex: TF_BUILD_LATTICE but the centroids are not a verified cube lattice");

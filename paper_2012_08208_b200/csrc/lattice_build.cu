@@ -653,6 +653,8 @@ int detect_rows(const double *A, int64_t P, int64_t n, int dim, LatModel *M, dou
 // Where detection reads centroids from: a prefix and a few gathered points (3 doubles each).
 struct PointSource {
     virtual tf_status prefix(int64_t P, std::vector<double> &A) = 0;
+    // the prefix and the last point (3 doubles, zero-padded) in one round trip
+    virtual tf_status prefix_last(int64_t P, int64_t n, std::vector<double> &A, double last[3]) = 0;
     virtual tf_status gather(const std::vector<int64_t> &idx, std::vector<double> &pts) = 0;
     virtual ~PointSource() = default;
 };
@@ -665,6 +667,14 @@ struct DevicePoints final : PointSource {  // the caller's device array (copies 
     tf_status prefix(int64_t P, std::vector<double> &A) override {
         A.resize((size_t)P * dim);
         TF_CUDA_TRY(cudaMemcpyAsync(A.data(), c, (size_t)P * dim * sizeof(double), cudaMemcpyDeviceToHost, s));
+        TF_CUDA_TRY(cudaStreamSynchronize(s));
+        return TF_OK;
+    }
+    tf_status prefix_last(int64_t P, int64_t n, std::vector<double> &A, double last[3]) override {
+        A.resize((size_t)P * dim);
+        last[0] = last[1] = last[2] = 0.0;
+        TF_CUDA_TRY(cudaMemcpyAsync(A.data(), c, (size_t)P * dim * sizeof(double), cudaMemcpyDeviceToHost, s));
+        TF_CUDA_TRY(cudaMemcpyAsync(last, c + (n - 1) * dim, (size_t)dim * sizeof(double), cudaMemcpyDeviceToHost, s));
         TF_CUDA_TRY(cudaStreamSynchronize(s));
         return TF_OK;
     }
@@ -694,6 +704,12 @@ struct HostPoints final : PointSource {  // a host array (tf_lattice_detect_host
         A.assign(c, c + (size_t)P * dim);
         return TF_OK;
     }
+    tf_status prefix_last(int64_t P, int64_t n, std::vector<double> &A, double last[3]) override {
+        A.assign(c, c + (size_t)P * dim);
+        last[0] = last[1] = last[2] = 0.0;
+        for (int d = 0; d < dim; ++d) last[d] = c[(n - 1) * dim + d];
+        return TF_OK;
+    }
     tf_status gather(const std::vector<int64_t> &idx, std::vector<double> &pts) override {
         pts.assign(idx.size() * 3, 0.0);
         for (size_t p = 0; p < idx.size(); ++p)
@@ -708,7 +724,8 @@ tf_status detect_model(PointSource &src, int64_t n, int dim, LatModel *M, bool *
     std::vector<double> A;
     double D[3];
     int64_t P = std::min<int64_t>(n, 4096);
-    TF_TRY(src.prefix(P, A));
+    double last[3];
+    TF_TRY(src.prefix_last(P, n, A, last));
     int st = detect_rows(A.data(), P, n, dim, M, D);
     if (st < 0 && P < n) {
         P = std::min<int64_t>(n, 1 << 16);
@@ -733,8 +750,28 @@ tf_status detect_model(PointSource &src, int64_t n, int dim, LatModel *M, bool *
         M->h[1] = M->h[0];
         M->h[2] = D[2];
     } else {
-        // 3D: ny divides rows; the first divisor d whose row T*nx*d leaves the y line is ny
+        // 3D: the last point is c0[T-1] + ((nx-1) hx, (ny-1) hy, (nz-1) hz) on a complete lattice:
+        // it gives ny (and with it nz, hz) without a second round trip; anything inconsistent falls
+        // back to probing rows T*nx*d for the divisors d of rows (one more round trip)
         M->h[1] = D[1];
+        {
+            const double *cl = M->c0[M->T - 1];
+            const double fy = (last[1] - cl[1]) / D[1];
+            const int64_t ny = (int64_t)llround(fy) + 1;
+            const double ex = last[0] - (cl[0] + (double)(M->nx - 1) * M->h[0]);
+            if (fabs(fy - (double)(ny - 1)) <= 1e-6 * std::max(1.0, fabs(fy)) && fabs(ex) <= tol && ny >= 1 &&
+                ny <= rows && rows % ny == 0) {
+                const int64_t nz = rows / ny;
+                const double hz = (nz > 1) ? (last[2] - cl[2]) / (double)(nz - 1) : M->h[0];
+                if (nz == 1 || hz > 0.0) {
+                    M->ny = ny;
+                    M->nz = nz;
+                    M->h[2] = hz;
+                    if (M->nx * M->ny * M->nz * M->T == n) *found = true;
+                    return TF_OK;  // the device verification checks every point against this model
+                }
+            }
+        }
         std::vector<int64_t> divs;
         for (int64_t d = 2; d * d <= rows; ++d)
             if (rows % d == 0) {
@@ -788,7 +825,7 @@ double dyadic_scale(const std::vector<double> &vs) {
 }  // namespace
 
 tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cudaStream_t s, tf_filter_s *h,
-                            bool *used) {
+                            bool *used, bool speculate) {
     *used = false;
     if (n < 4) return TF_OK;
     NvtxRange r_det("tf_build/lattice detect + verify");
@@ -919,6 +956,7 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     // lat_axis_class): each (class, type) list is the type table restricted to the offsets in the
     // grid at a representative position; Hs summed in ascending column order (the oracle's order).
     std::vector<unsigned char> blob;
+    std::vector<int32_t> cls_len;  // exact mode: row length of every (boundary class, type)
     size_t o_tab = 0, o_ccol = 0, o_cw = 0, o_mask = 0, o_pre = 0, o_len = 0, o_hs = 0;
     int ntab = 0, SP = 0;
     int64_t ncls = 0;
@@ -988,6 +1026,7 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
             o_mask = put(c_mask.data(), c_mask.size() * sizeof(uint32_t));
             o_pre = put(c_pre.data(), c_pre.size() * sizeof(int32_t));
             o_len = put(c_len.data(), c_len.size() * sizeof(int32_t));
+            cls_len = c_len;
             o_hs = put(c_hs.data(), c_hs.size() * sizeof(double));
         }
     };
@@ -1005,6 +1044,95 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
         const size_t need = (size_t)4 * SPx * 12 + (ncls <= (1 << 16) ? LatClasses::smem_bytes((int)ncls, Wc) : SIZE_MAX / 2);
         spec_fits = need <= (size_t)160 * 1024;
         if (spec_fits) make_blob(true);
+    }
+    if (speculate && spec_ok && spec_fits && va.q != 0.0 && (h->lat_check || (h->lat_check = pinned_slot_acquire()))) {
+        // ---- speculative exact build: no round trip for the verification or for nnz. nnz follows
+        // from the host tables (rows per boundary class x class length); the verification result,
+        // the fill's agreement flag and the scanned nnz land in pinned memory by the build's final
+        // synchronisation and are checked then (lattice_check_ok); a failed check rebuilds without
+        // speculation (tf_build_filter, api.cu)
+        int64_t nnz_h = 0;
+        auto axis_count = [&](int d, int cl) -> int64_t {
+            if (nd[d] < 2 * R[d] + 1) return 1;
+            return (cl == R[d]) ? nd[d] - 2 * R[d] : 1;
+        };
+        int64_t cid = 0;
+        for (int cz = 0; cz < L.C[2]; ++cz)
+            for (int cy = 0; cy < L.C[1]; ++cy)
+                for (int cx = 0; cx < L.C[0]; ++cx) {
+                    const int64_t rows = axis_count(0, cx) * (dim >= 2 ? axis_count(1, cy) : 1) *
+                                         (dim == 3 ? axis_count(2, cz) : 1);
+                    for (int sty = 0; sty < M.T; ++sty, ++cid) nnz_h += rows * (int64_t)cls_len[cid];
+                }
+        build_trace().mark("lattice tables (speculative)", s);
+        DevBuf<unsigned char> dblob;
+        TF_TRY(dblob.alloc(blob.size(), s, "lattice tables"));
+        TF_CUDA_TRY(cudaMemcpyAsync(dblob.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+        auto at = [&](size_t o) { return dblob.p + o; };
+        const int ntab_ = (int)tab.size();
+        const int LP = (std::max(1024, ntab_) + 1) & ~1;
+        int LW = (ntab_ + LP + 2 + 1) & ~1;
+        if ((size_t)2 * LW * sizeof(double) > (size_t)96 * 1024) LW = 0;
+#ifdef TF_LAT_NO_BULK
+        LW = 0;
+#endif
+        const LatCycle cyc{reinterpret_cast<const int32_t *>(at(o_ccol)), reinterpret_cast<const double *>(at(o_cw)),
+                           ntab_, SP, LW, LP};
+        const LatClasses cls{reinterpret_cast<const uint32_t *>(at(o_mask)),
+                             reinterpret_cast<const int32_t *>(at(o_pre)), reinterpret_cast<const int32_t *>(at(o_len)),
+                             reinterpret_cast<const double *>(at(o_hs)), (int)ncls, Wc};
+        DevBuf<int32_t> counts, flag;
+        TF_TRY(counts.alloc(n, s, "row counts"));
+        TF_TRY(flag.alloc(1, s, "lattice fill flag"));
+        TF_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int32_t), s));
+        {
+            const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 16);
+            if (dim == 3) k_lat_count_exact<3><<<g, 256, 0, s>>>(L, cls, counts.p);
+            else k_lat_count_exact<2><<<g, 256, 0, s>>>(L, cls, counts.p);
+            TF_LAUNCH_CHECK();
+        }
+        TF_TRY(dalloc(&h->rowptr, n + 3, s, "rowptr (+2 padding for 16-byte bulk copies)"));
+        TF_TRY(exclusive_scan_i32_i64(counts.p, h->rowptr, n, s));
+        TF_TRY(dalloc(&h->cols, nnz_h + 4, s, "cols (nnz int32, +4 padding for 16-byte bulk copies)"));
+        TF_TRY(dalloc(&h->vals, nnz_h + 4, s, "vals (nnz fp64, +4 padding)"));
+        TF_TRY(dalloc(&h->hs, n, s, "Hs"));
+        {
+            const size_t smem_cyc = (size_t)2 * LW * sizeof(double) + (size_t)4 * SP * (sizeof(int32_t) + sizeof(double)) +
+                                    LatClasses::smem_bytes((int)ncls, Wc);
+            auto kern = (dim == 3) ? k_lat_fill_exact<3> : k_lat_fill_exact<2>;
+            TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cyc));
+            int per_sm = 0;
+            TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem_cyc));
+            const int64_t warps_needed = (n + 31) / 32;
+            const unsigned grid = (unsigned)std::max<int64_t>(
+                1, std::min<int64_t>((int64_t)di.sms * std::max(1, per_sm), (warps_needed + 7) / 8));
+            kern<<<grid, 256, smem_cyc, s>>>(L, cyc, cls, h->rowptr, h->cols, h->vals, h->hs, flag.p);
+            TF_LAUNCH_CHECK();
+        }
+        if (!h->lat_check) h->lat_check = pinned_slot_acquire();
+        if (!h->lat_check) {
+            set_error("internal: no pinned slot for the speculative lattice build");
+            return TF_ERR_NOMEM;
+        }
+        memset(h->lat_check, 0xff, 4 * sizeof(unsigned long long));
+        TF_CUDA_TRY(cudaMemcpyAsync(h->lat_check, vout.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        h->lat_check[2] = 0;
+        TF_CUDA_TRY(cudaMemcpyAsync(&h->lat_check[2], flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        TF_CUDA_TRY(cudaMemcpyAsync(&h->lat_check[3], h->rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        build_trace().mark("lattice count + scan + fill (speculative)", s);
+        h->lat_pending = true;
+        h->lat_nnz_host = nnz_h;
+        h->nnz = nnz_h;
+        h->info.bin_side = 0.0;
+        for (int d = 0; d < 3; ++d) h->info.bins[d] = nd[d];
+        h->info.nbins = M.nx * M.ny * M.nz;
+        h->info.max_candidates = maxK;
+        h->max_row_hint = maxK;
+        h->info.large_rows = 0;
+        h->info.radix_passes = 0;
+        h->info.path = TF_PATH_LATTICE_EXACT;
+        *used = true;
+        return TF_OK;
     }
     unsigned long long vres[2];
     TF_CUDA_TRY(cudaMemcpyAsync(vres, vout.p, sizeof(vres), cudaMemcpyDeviceToHost, s));
@@ -1132,6 +1260,16 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     h->info.path = exact ? TF_PATH_LATTICE_EXACT : TF_PATH_LATTICE_TESTED;
     *used = true;
     return TF_OK;
+}
+
+bool lattice_check_ok(const tf_filter_s *h) {
+    const unsigned long long *k = h->lat_check;
+    if (!k) return false;
+    double dev;
+    memcpy(&dev, &k[0], sizeof(dev));
+    const bool verified = (k[1] & 3ull) == 0 && dev == 0.0;  // finite, exact, on the lattice
+    const int32_t fill_flag = (int32_t)(k[2] & 0xffffffffull);
+    return verified && fill_flag == 0 && (int64_t)k[3] == h->lat_nnz_host;
 }
 
 tf_status lattice_detect_host(const double *c, int64_t n, int dim, int32_t *T, int64_t cubes[3], double spacing[3]) {

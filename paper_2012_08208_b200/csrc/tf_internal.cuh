@@ -107,6 +107,10 @@ struct DeviceScope {
 // ------------------------------------------------------------------ memory
 // Stream-ordered device allocation with the test-only allocation limit.
 tf_status dev_alloc(void **p, size_t bytes, cudaStream_t s, const char *what);
+// 32-byte pinned host slots for small device -> host results read after a stream sync (a pool:
+// cudaMallocHost costs ~1 ms, too much per build); nullptr if pinned memory is unavailable
+unsigned long long *pinned_slot_acquire();
+void pinned_slot_release(unsigned long long *p);
 void dev_free(void *p, cudaStream_t s);
 void reset_alloc_budget();
 
@@ -203,7 +207,6 @@ struct SortedPtsView {
 struct ApplyPlan {
     int64_t nblocks = 0;      // row blocks
     int32_t *rb = nullptr;    // [nblocks+1] first row of each block
-    std::vector<int32_t> rb_host;  // host copy (row-range applies pick their first window from it)
     int block_nnz = 0;        // target nnz per block (window)
     int stage_cap = 0;        // staged-path capacity (nnz)
     int group = 1;            // lanes per row in the reduction phase (power of two <= 32)
@@ -251,6 +254,12 @@ struct StencilGeom {
 struct tf_filter_s {
     int device = -1;  // the CUDA device current at build time; every call must use it
     cudaStream_t stream = nullptr;  // the build stream: tf_free releases the memory stream-ordered on it
+    // speculative exact lattice build (lattice_build.cu): results of the verification pass, the
+    // fill's agreement flag and the scanned nnz land here (pinned) by the build's final sync and
+    // are checked then; lat_nnz_host is the nnz the host tables predicted
+    bool lat_pending = false;
+    unsigned long long *lat_check = nullptr;  // pinned: [0] dev bits, [1] flags, [2] fill flag, [3] nnz
+    int64_t lat_nnz_host = 0;
     int64_t n = 0, nnz = 0;
     int dim = 0;
     double rmin = 0;
@@ -305,7 +314,9 @@ tf_status radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys_alt, u
                            int64_t n, int bits, cudaStream_t s, uint32_t **keys_out,
                            uint32_t **vals_out, int *passes);
 
-// build.cu (flags: TF_BUILD_*; the lattice path is tried first unless TF_BUILD_CELL_LIST)
+// build.cu (flags: TF_BUILD_*, optionally | kBuildNoSpeculation; the lattice path is tried first
+// unless TF_BUILD_CELL_LIST)
+constexpr int kBuildNoSpeculation = 1 << 16;
 tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, int flags, cudaStream_t s,
                               tf_filter_s *h);
 // cl_build.cu: the group kernels of the cell-list build (count -> scan -> fill) on the sorted
@@ -314,7 +325,10 @@ tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_
                                  cudaStream_t s, tf_filter_s *h, bool *done);
 // lattice_build.cu: *used = false (and TF_OK) when the centroids are not a verified lattice
 tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cudaStream_t s, tf_filter_s *h,
-                            bool *used);
+                            bool *used, bool speculate = true);
+// after the build's final synchronisation: false if the speculative exact lattice build must be
+// redone (verification failed, or the fill disagreed with the predicted row lengths)
+bool lattice_check_ok(const tf_filter_s *h);
 // the detection step alone on a host array (no CUDA calls): T = 0 if not lattice-ordered
 tf_status lattice_detect_host(const double *c, int64_t n, int dim, int32_t *T, int64_t cubes[3], double spacing[3]);
 

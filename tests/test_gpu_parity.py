@@ -482,7 +482,7 @@ def test_launch_counter_and_stats(tf):
     k1 = tf.kernel_launches()
     assert k1 - k0 >= 8
     f.sensitivity(dev(x), dev(dc))
-    assert tf.kernel_launches() - k1 == 1
+    assert tf.kernel_launches() - k1 == 2  # t pass + the programmatic dependent SpMV launch
     st = f.stats()
     assert st["path"] == "cell_list"
     assert st["bin_side"] >= rmin * (1 + 1e-6)
