@@ -625,6 +625,239 @@ __global__ void __launch_bounds__(WARPS * 32) k_cl_fill(SortedPtsView P, Grid g,
     }
 }
 
+// ------------------------------------------------------------------ a7: fill, block per group
+// One block of kFillBWarps warps per group (kGroupQ = 32 queries). The group's sorted union is
+// staged in shared memory once -- exact fp64 coordinates and ids --, so every entry's candidate
+// data is a shared-memory load instead of a global gather (the warp-per-group fill was bound by
+// the L1 wavefronts of those gathers). Warp 0 expands the lanes' mask words into candidate lists
+// (lane = query, as k_cl_fill) while the other warps stage the union; then warp w writes the rows
+// of queries w, w + kFillBWarps, ... (lane = entry; two rows per pass, kFillRounds rounds each in
+// flight): the oracle's d^2 and weight, coalesced int32 / fp64 stores, Hs by a fixed-order lane
+// reduction. Shared memory: union x, y, z [LPmax] fp64 + ids [LPmax] int32 + masks [32][MS] + lists
+// [32][S] uint16.
+constexpr int kFillBWarps = 4;
+
+template <int DIM>
+__global__ void __launch_bounds__(kFillBWarps * 32) k_cl_fill_b(SortedPtsView P, Grid g,
+                                                                const GroupRec *__restrict__ rec,
+                                                                const int64_t *__restrict__ loff, int LPmax, int MS,
+                                                                int S, const int32_t *__restrict__ list,
+                                                                const uint32_t *__restrict__ mask,
+                                                                const int64_t *__restrict__ rowptr,
+                                                                int32_t *__restrict__ cols, double *__restrict__ vals,
+                                                                double *__restrict__ hs, int32_t *__restrict__ stats) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int T = kFillBWarps * 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double *ux = reinterpret_cast<double *>(smem_raw);
+    double *uy = ux + LPmax;
+    double *uz = uy + LPmax;
+    int32_t *uid = reinterpret_cast<int32_t *>(uz + ((DIM == 3) ? LPmax : 0));
+    uint32_t *sm = reinterpret_cast<uint32_t *>(uid + LPmax);  // [32][MS]
+    uint16_t *ent = reinterpret_cast<uint16_t *>(sm + 32 * MS);  // [32][S]
+    __shared__ int32_t s_len[32];
+    __shared__ int64_t s_base[32];
+    __shared__ int32_t s_qid[32];
+    const GroupRec R = rec[blockIdx.x];
+    const int L = R.L, LP = (L + 31) & ~31, nw = LP >> 5;
+    const int64_t base = loff[blockIdx.x];
+    const int nq = R.q1 - R.q0;
+    if (warp == 0) {
+        // masks of the group, transposed to [lane][word] (odd stride MS > nw, the padding zero)
+        for (int k0 = 0; k0 < MS; k0 += 4) {
+            uint32_t m[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) m[u] = (k0 + u < nw) ? mask[base + 32 * (k0 + u) + lane] : 0u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k0 + u < MS) sm[lane * MS + k0 + u] = m[u];
+        }
+        const int q = R.q0 + lane;
+        const bool have = lane < nq;
+        int32_t qid = 0;
+        int64_t rbase = 0;
+        int len = 0;
+        if (have) {
+            qid = P.id[q];
+            rbase = rowptr[qid];
+            len = (int)(rowptr[qid + 1] - rbase);
+        }
+        s_len[lane] = len;
+        s_base[lane] = rbase;
+        s_qid[lane] = qid;
+        __syncwarp();
+        // branch-free walk of the lane's words (two set bits or one word step per iteration)
+        const uint32_t *mw = sm + lane * MS;
+        uint16_t *my = ent + (size_t)lane * S;
+        int n = 0, k = 0;
+        uint32_t w = mw[0];
+        const int kend = have ? nw : 0;
+        while (__any_sync(0xffffffffu, k < kend)) {
+#pragma unroll 2
+            for (int u = 0; u < 2; ++u) {
+                const bool z = (w == 0);
+                const int b1 = __clz(w) & 31;
+                const uint32_t w1 = w ^ (0x80000000u >> b1);
+                const int b2 = __clz(w1) & 31;
+                const bool two = !z && (w1 != 0);
+                my[min(n, S - 1)] = (uint16_t)(32 * k + b1);
+                my[min(n + 1, S - 1)] = (uint16_t)(32 * k + b2);
+                n += z ? 0 : (two ? 2 : 1);
+                const uint32_t wn = mw[min(k + 1, MS - 1)];
+                w = z ? wn : (two ? (w1 ^ (0x80000000u >> b2)) : 0u);
+                k = z ? min(k + 1, nw) : k;
+            }
+        }
+        if (have && n != len) atomicOr(&stats[2], 1);  // count/fill agreement (always-on invariant)
+    } else {
+        // the union's exact coordinates and ids, staged once for the whole group
+        for (int t0 = (warp - 1) * 32; t0 < L; t0 += 4 * (T - 32)) {
+            int p[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = t0 + u * (T - 32) + lane;
+                p[u] = (t < L) ? list[base + t] : -1;
+            }
+            double xv[4], yv[4], zv[4];
+            int32_t iv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int pp = p[u] < 0 ? 0 : p[u];
+                xv[u] = P.x[pp];
+                yv[u] = P.y[pp];
+                zv[u] = (DIM == 3) ? P.z[pp] : 0.0;
+                iv[u] = P.id[pp];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = t0 + u * (T - 32) + lane;
+                if (t < L) {
+                    ux[t] = xv[u];
+                    uy[t] = yv[u];
+                    if (DIM == 3) uz[t] = zv[u];
+                    uid[t] = iv[u];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const double rmin = g.rmin;
+#ifdef TF_DEBUG_CHECKS
+    const double r2 = g.r2;
+#endif
+    for (int i0 = 2 * warp; i0 < nq; i0 += 2 * kFillBWarps) {
+        int li[2];
+        bool longrow[2];
+        int32_t qi[2];
+        int64_t bi[2];
+        double qx[2], qy[2], qz[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int i = min(i0 + h, nq - 1);
+            li[h] = (i0 + h < nq) ? s_len[i] : 0;
+            longrow[h] = li[h] > S - 2;
+            if (longrow[h]) li[h] = 0;
+            bi[h] = s_base[i];
+            qi[h] = s_qid[i];
+            qx[h] = P.x[R.q0 + i];
+            qy[h] = P.y[R.q0 + i];
+            qz[h] = (DIM == 3) ? P.z[R.q0 + i] : 0.0;
+        }
+        double cx[2][kFillRounds], cy[2][kFillRounds], cz[2][kFillRounds];
+        int32_t cid[2][kFillRounds];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int r = 0; r < kFillRounds; ++r) {
+                const int e = 32 * r + lane;
+                const int t = (e < li[h]) ? ent[(size_t)(i0 + h) * S + e] : 0;
+                cx[h][r] = ux[t];
+                cy[h][r] = uy[t];
+                cz[h][r] = (DIM == 3) ? uz[t] : 0.0;
+                cid[h][r] = uid[t];
+            }
+        double hsum[2] = {0.0, 0.0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int r = 0; r < kFillRounds; ++r) {
+                const int e = 32 * r + lane;
+                if (e < li[h]) {
+                    const double d2 = pair_d2<DIM>(qx[h], qy[h], qz[h], cx[h][r], cy[h][r], cz[h][r]);
+                    const double w = weight_of(rmin, d2);
+                    cols[bi[h] + e] = cid[h][r];
+                    vals[bi[h] + e] = w;
+                    hsum[h] += w;
+                    TF_DCHECK(d2 < r2);
+                }
+            }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            for (int e = 32 * kFillRounds + lane; e < li[h]; e += 32) {
+                const int t = ent[(size_t)(i0 + h) * S + e];
+                const double d2 = pair_d2<DIM>(qx[h], qy[h], qz[h], ux[t], uy[t], (DIM == 3) ? uz[t] : 0.0);
+                const double w = weight_of(rmin, d2);
+                cols[bi[h] + e] = uid[t];
+                vals[bi[h] + e] = w;
+                hsum[h] += w;
+                TF_DCHECK(d2 < r2);
+            }
+        // rows longer than the lists: lane = mask word of the row (word-parallel path)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (!longrow[h]) continue;
+            const int i = i0 + h;
+            int done = 0;
+            for (int k0 = 0; k0 < nw; k0 += 32) {
+                const int k = k0 + lane;
+                uint32_t w = (k < nw) ? sm[i * MS + k] : 0u;
+                const int c = __popc(w);
+                int inc = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += v;
+                }
+                int e = done + inc - c;
+                while (w) {
+                    const int b = __clz(w);
+                    const int t = 32 * k + b;
+                    const double d2 = pair_d2<DIM>(qx[h], qy[h], qz[h], ux[t], uy[t], (DIM == 3) ? uz[t] : 0.0);
+                    const double wt = weight_of(rmin, d2);
+                    cols[bi[h] + e] = uid[t];
+                    vals[bi[h] + e] = wt;
+                    hsum[h] += wt;
+                    ++e;
+                    w ^= 0x80000000u >> b;
+                }
+                done += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            hsum[0] += __shfl_xor_sync(0xffffffffu, hsum[0], o);
+            hsum[1] += __shfl_xor_sync(0xffffffffu, hsum[1], o);
+        }
+        if (lane == 0) {
+            hs[qi[0]] = hsum[0];
+            if (i0 + 1 < nq) hs[qi[1]] = hsum[1];
+        }
+    }
+}
+
+template <int DIM>
+tf_status launch_cl_fill_b(const SortedPtsView &P, const Grid &g, const GroupRec *rec, const int64_t *loff, int32_t G,
+                           int LPmax, int MS, int S, const int32_t *list, const uint32_t *mask, tf_filter_s *h,
+                           int32_t *stats, cudaStream_t s) {
+    const size_t smem = (size_t)LPmax * ((DIM == 3 ? 24 : 16) + 4) + (size_t)32 * MS * 4 + (size_t)32 * S * 2;
+    auto kern = k_cl_fill_b<DIM>;
+    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)G, kFillBWarps * 32, smem, s>>>(P, g, rec, loff, LPmax, MS, S, list, mask, h->rowptr, h->cols,
+                                                     h->vals, h->hs, stats);
+    TF_LAUNCH_CHECK();
+    return TF_OK;
+}
+
 template <int DIM>
 tf_status launch_cl_count(const SortedPtsView &P, const Grid &g, const GroupRec *rec, const int64_t *loff, int32_t G,
                           int LPmax, int32_t *list, uint32_t *mask, int32_t *counts, int32_t *stats, cudaStream_t s) {
@@ -738,6 +971,14 @@ tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_
     if ((S & 3) == 0) S += 2;
     const int MS = (LPmax / 32 + 1) | 1;
     const size_t per_warp = (size_t)32 * MS * 4 + (size_t)32 * S * 2;
+    // the block-per-group fill (union staged in shared memory) measured 8.90 vs 8.60 ms at config 5
+    // and 0.42 vs 0.47 ms at config 4: opt-in (TOPOFILT_CL_FILL=block, benchmarks and tests)
+    const char *fk = getenv("TOPOFILT_CL_FILL");
+    const size_t smem_b = (size_t)LPmax * ((dim == 3 ? 24 : 16) + 4) + (size_t)32 * MS * 4 + (size_t)32 * S * 2;
+    if (kGroupQ == 32 && fk && !strcmp(fk, "block") && smem_b <= di.smem_optin) {
+        if (dim == 3) TF_TRY((launch_cl_fill_b<3>(P, g, rec.p, loff.p, hG, LPmax, MS, S, list.p, mask.p, h, stats.p, s)));
+        else TF_TRY((launch_cl_fill_b<2>(P, g, rec.p, loff.p, hG, LPmax, MS, S, list.p, mask.p, h, stats.p, s)));
+    } else {
     int fw = env_int("TOPOFILT_CL_FILL_WARPS", 4);  // tuning knob (benchmarks only)
     while (fw > 1 && (size_t)fw * per_warp > di.smem_optin) fw >>= 1;
     if (dim == 3) {
@@ -748,6 +989,7 @@ tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_
         if (fw >= 4) TF_TRY((launch_cl_fill<2, 4>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
         else if (fw >= 2) TF_TRY((launch_cl_fill<2, 2>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
         else TF_TRY((launch_cl_fill<2, 1>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
+    }
     }
     build_trace().mark("fill", s);
     int32_t flag = 0;

@@ -134,3 +134,12 @@ def test_paper_right_left_triangles(tf):
     c = np.array(pts)
     check_against_oracle(tf, c, 2.0)
     check_paths_agree(tf, c, 2.0)
+
+
+def test_block_fill_variant(tf, monkeypatch):
+    """The opt-in block-per-group fill (TOPOFILT_CL_FILL=block) builds the same CSR."""
+    monkeypatch.setenv("TOPOFILT_CL_FILL", "block")
+    for c, rmin in ((synth.ground_structure(4, 400, 300)[0], 3.0), (synth.kuhn_mesh(10, 8, 6, jitter=0.1, stream=5)[0], 1.5),
+                    (np.concatenate([np.random.default_rng(2).uniform(0, 1.0, size=(900, 3)),
+                                     np.random.default_rng(3).uniform(0, 20, size=(3000, 3))]), 1.1)):
+        check_against_oracle(tf, c, rmin)
