@@ -16,7 +16,16 @@ timeout 300 $CMDL > gpurun_out/ev_prof_plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches.csv $CMDL > gpurun_out/ev_ncu_launch.log 2>&1; echo ncu1=$?
 CMD="python bench.py --steps 1 --warmup 0 --applies 2 --no-e2e --no-cpu-baseline"
 # the step's lattice fill and two applies, then the cell-list count and fill (bench's build_cell_list leg)
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_spmv|k_fill|k_count|k_lat_fill_exact" -c 8 -o gpurun_out/ev_prof $CMD > gpurun_out/ev_ncu_full.log 2>&1; echo ncu2=$?
+# (step: k_lat_fill_exact, 2 x (k_tpass, k_spmv<1>, k_spmv<0>); then the cell-list leg's k_cl_count, k_cl_fill)
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_spmv|k_cl_fill|k_cl_count|k_lat_fill_exact|k_tpass" -c 9 -o gpurun_out/ev_prof $CMD > gpurun_out/ev_ncu_full.log 2>&1; echo ncu2=$?
+# instructions per query of the cell-list build kernels: group kernels vs the per-bin kernels (config 5)
+timeout 900 ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_cl_count|k_cl_fill|k_count|k_fill" --csv --log-file gpurun_out/ev_build_inst_groups.csv python tools/cl_one.py 5 cell_list > /dev/null 2>&1; echo ncu3=$?
+timeout 900 ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_count|k_fill" --csv --log-file gpurun_out/ev_build_inst_bins.csv python tools/cl_one.py 5 cell_list_bins > /dev/null 2>&1; echo ncu4=$?
+TOPOFILT_TRACE=1 BUILD_PATHS=lattice,cell_list python tools/build_paths.py 1 2 3 4 5 > gpurun_out/ev_build_paths.jsonl 2> gpurun_out/ev_build_trace.log; echo paths=$?
+python tools/cl_check.py 3 4 5 > gpurun_out/ev_cl_check.jsonl 2>&1; echo clcheck=$?
+python tools/apply_mid_probe.py > gpurun_out/ev_apply_mid.jsonl 2>&1; echo mid=$?
+timeout 900 python bench.py --gpus 2 --dry-run --steps 3 --warmup 3 > gpurun_out/ev_bench_dry2.json 2> gpurun_out/ev_bench_dry2.err; echo dry2=$?
+timeout 900 python bench.py --gpus 4 --dry-run --config 3 --steps 3 --warmup 3 > gpurun_out/ev_bench_dry4_c3.json 2> gpurun_out/ev_bench_dry4_c3.err; echo dry4=$?
 timeout 300 python tools/helm_probe.py > gpurun_out/ev_helm_probe.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hz_apply -c 1 -o gpurun_out/ev_hz python tools/helm_probe.py ncu > gpurun_out/ev_ncu_hz.log 2>&1; echo ncu_hz=$?
 timeout 300 python tools/matrix_free_probe.py > gpurun_out/ev_mf_probe.log 2>&1 && \

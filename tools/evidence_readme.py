@@ -64,6 +64,11 @@ def main(rnd):
     dst = os.path.join(ROOT, "profiles", rnd)
     os.makedirs(dst, exist_ok=True)
     for a, b in [("ev_bench.json", "bench.json"), ("ev_bench_ref.json", "bench_reference.json"),
+                 ("ev_build_inst_groups.csv", "build_inst_groups.csv"), ("ev_build_inst_bins.csv", "build_inst_bins.csv"),
+                 ("ev_build_paths.jsonl", "build_paths.jsonl"), ("ev_build_trace.log", "build_trace.log"),
+                 ("ev_cl_check.jsonl", "cl_check.jsonl"), ("ev_apply_mid.jsonl", "apply_mid.jsonl"),
+                 ("ev_bench_dry2.json", "bench_dry_run_2shards.json"),
+                 ("ev_bench_dry4_c3.json", "bench_dry_run_4shards_c3.json"),
                  ("ev_configs.jsonl", "configs.jsonl"), ("ev_clocks.csv", "clocks_during_bench.csv"),
                  ("ev_launches.csv", "launches.csv"), ("ev_pytest_gpu.log", "pytest_gpu.log"),
                  ("ev_smoke.log", "smoke.log")]:
@@ -75,7 +80,7 @@ def main(rnd):
     with open(os.path.join(dst, "ncu_full_summary.txt"), "w") as f:
         subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), raw], stdout=f, check=True)
     write_survey_metrics(raw, os.path.join(dst, "survey_metrics.txt"))
-    for k in ("k_spmv", "k_fill", "k_count", "k_lat_fill_exact"):
+    for k in ("k_spmv", "k_cl_fill", "k_cl_count", "k_lat_fill_exact"):
         src = f"/tmp/src_{k}.csv"
         ncu(["-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{k}", "-c", "1"], src)
         with open(os.path.join(dst, f"{k}_source_hot.txt"), "w") as f:
@@ -88,14 +93,14 @@ def main(rnd):
 
     blocks = summary_blocks(os.path.join(dst, "ncu_full_summary.txt"))
     pick = lambda pat: next(b for b in blocks if pat in b["name"])  # noqa: E731
-    sens, dens, fill, count = pick("k_spmv<1"), pick("k_spmv<0"), pick("k_fill<"), pick("k_count")
+    sens, dens, fill, count = pick("k_spmv<1"), pick("k_spmv<0"), pick("k_cl_fill"), pick("k_cl_count")
     latfill = pick("k_lat_fill_exact")
     gb = 1e9
     traffic = {
         "source": f"ncu --set full --clock-control none, config 5 (profiles/{rnd}/ncu_full_summary.txt)",
         "k_spmv_sens_bytes_per_launch": (sens["dram__bytes_read.sum"] + sens["dram__bytes_write.sum"]) * gb,
     }
-    for key, b in (("k_count", count), ("k_fill", fill), ("k_lat_fill_exact", latfill), ("k_spmv_sens", sens),
+    for key, b in (("k_cl_count", count), ("k_cl_fill", fill), ("k_lat_fill_exact", latfill), ("k_spmv_sens", sens),
                    ("k_spmv_dens", dens)):
         traffic[key] = {"dram_read_bytes": b["dram__bytes_read.sum"] * gb,
                         "dram_write_bytes": b["dram__bytes_write.sum"] * gb,
@@ -142,7 +147,7 @@ def main(rnd):
     w("| kernel | duration (ncu) | DRAM read | DRAM write | issue active | DRAM % of peak |")
     w("|---|---|---|---|---|---|")
     for nm, b in (("k_spmv sensitivity", sens), ("k_spmv density", dens), ("k_lat_fill_exact (lattice build)", latfill),
-                  ("k_fill (cell-list build)", fill), ("k_count (cell-list build)", count)):
+                  ("k_cl_fill (cell-list build)", fill), ("k_cl_count (cell-list build)", count)):
         w(f"| {nm} | {b['gpu__time_duration.sum']:.3f} ms | {b['dram__bytes_read.sum']:.2f} GB | "
           f"{b['dram__bytes_write.sum']:.3f} GB | {b.get('smsp__issue_active.avg.pct_of_peak_sustained_active', 0):.0f}% | "
           f"{b.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 0):.0f}% |")
