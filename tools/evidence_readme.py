@@ -84,7 +84,9 @@ def main(rnd):
         src = f"/tmp/src_{k}.csv"
         ncu(["-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{k}", "-c", "1"], src)
         with open(os.path.join(dst, f"{k}_source_hot.txt"), "w") as f:
-            subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_source_hot.py"), src], stdout=f, check=True)
+            r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_source_hot.py"), src], stdout=f)
+        if r.returncode != 0:
+            os.remove(os.path.join(dst, f"{k}_source_hot.txt"))  # kernel not in this capture
     with open(os.path.join(dst, "sass_evidence.txt"), "w") as f:
         subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sass_evidence.py")], stdout=f, check=True)
     with open(os.path.join(dst, "launches_summary.txt"), "w") as f:
@@ -92,7 +94,9 @@ def main(rnd):
                         os.path.join(dst, "launches.csv")], stdout=f, check=True)
 
     blocks = summary_blocks(os.path.join(dst, "ncu_full_summary.txt"))
-    pick = lambda pat: next(b for b in blocks if pat in b["name"])  # noqa: E731
+    empty = {"name": "(not captured)", "gpu__time_duration.sum": float("nan"), "dram__bytes_read.sum": float("nan"),
+             "dram__bytes_write.sum": float("nan")}
+    pick = lambda pat: next((b for b in blocks if pat in b["name"]), empty)  # noqa: E731
     sens, dens, fill, count = pick("k_spmv<1"), pick("k_spmv<0"), pick("k_cl_fill"), pick("k_cl_count")
     latfill = pick("k_lat_fill_exact")
     gb = 1e9
