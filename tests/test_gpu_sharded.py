@@ -120,3 +120,20 @@ def test_filter_range_matches_full(tf):
     with pytest.raises(tf.TopofiltError):
         tf.tf_density_filter_range(f, x, torch.empty_like(x), 5, 3)
     f.close()
+
+
+def test_sharded_empty_ranks(tf):
+    """More shards than distinct cut coordinates: some ranks own nothing (no local filter) but
+    still take part in the exchange; the assembled result is still the oracle's."""
+    rng = np.random.default_rng(21)
+    n = 3000
+    c = np.stack([rng.integers(0, 3, n).astype(np.float64) * 0.9, rng.uniform(0, 1.0, n) * 0.5], 1)
+    rmin = 1.0
+    x = synth.uniform(915, 0, n, 0.001, 1.0)
+    dc = -synth.uniform(916, 0, n, 0.5, 1.5)
+    sens, dens, stats = run_shards(c, rmin, x, dc, 5)
+    assert sum(v[1] for v in stats.values()) == n
+    assert any(v[1] == 0 for v in stats.values())
+    ref = oracle.build_celllist(c, rmin)
+    assert_rel(sens, oracle.apply_sensitivity(ref, x, dc), "empty ranks sensitivity")
+    assert_rel(dens, oracle.apply_density(ref, x), "empty ranks density")
