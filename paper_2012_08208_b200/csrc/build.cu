@@ -143,11 +143,14 @@ __global__ void __launch_bounds__(256) k_cellstart(const uint32_t *__restrict__ 
 // SoA copy of the centroids in sorted order (exact bytes; no shift, no rounding).
 __global__ void __launch_bounds__(256) k_gather_sorted(const double *__restrict__ c, int64_t n, int dim,
                                                        const uint32_t *__restrict__ ids,
-                                                       double *__restrict__ sxyz) {
+                                                       double *__restrict__ sxyz, double4 *__restrict__ aos) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = ids[p];
-        for (int d = 0; d < dim; ++d) sxyz[d * n + p] = c[i * dim + d];
+        double v[3] = {0.0, 0.0, 0.0};
+        for (int d = 0; d < dim; ++d) sxyz[d * n + p] = v[d] = c[i * dim + d];
+        // the group kernels gather whole points: (x, y, z, id) in one 32-byte sector
+        if (aos) aos[p] = make_double4(v[0], v[1], v[2], __longlong_as_double((long long)i));
     }
 }
 
@@ -978,9 +981,14 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     TF_LAUNCH_CHECK();
     DevBuf<double> sxyz;
     TF_TRY(sxyz.alloc((size_t)dim * n, s, "sorted centroids"));
-    k_gather_sorted<<<grid_n, threads, 0, s>>>(c, n, dim, vs, sxyz.p);
+    bool legacy = (flags == TF_BUILD_CELL_LIST_BINS);
+    if (const char *e = getenv("TOPOFILT_CL")) legacy = legacy || !strcmp(e, "bins");  // benchmarks
+    DevBuf<double4> aos;
+    if (!legacy) TF_TRY(aos.alloc(n, s, "sorted centroids (AoS)"));
+    k_gather_sorted<<<grid_n, threads, 0, s>>>(c, n, dim, vs, sxyz.p, aos.p);
     TF_LAUNCH_CHECK();
     SortedPts P;
+    P.a = aos.p;
     P.x = sxyz.p;
     P.y = sxyz.p + n;
     P.z = (dim == 3) ? sxyz.p + 2 * n : sxyz.p + n;
@@ -990,8 +998,6 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
 
     // a5-a7 by query groups (cl_build.cu) unless the per-bin kernels are asked for or a group's
     // neighbourhood union exceeds the group kernels' shared-memory capacity
-    bool legacy = (flags == TF_BUILD_CELL_LIST_BINS);
-    if (const char *e = getenv("TOPOFILT_CL")) legacy = legacy || !strcmp(e, "bins");  // benchmarks
     if (!legacy) {
         bool done = false;
         TF_TRY(build_cell_list_groups(P, ks_keys, g, n, s, h, &done));

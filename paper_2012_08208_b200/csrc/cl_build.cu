@@ -79,6 +79,19 @@ __device__ __forceinline__ f2u f2_fma(f2u a, f2u b, f2u c) {
     return r;
 }
 
+// ---- one sorted point (x, y, z, id) as a single 256-bit load of its 32-byte AoS record
+struct PtRec {
+    double x, y, z;
+    int32_t id;
+};
+__device__ __forceinline__ PtRec load_pt(const double4 *a, int p) {
+    PtRec r;
+    double w;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(w) : "l"(a + p));
+    r.id = (int32_t)__double_as_longlong(w);
+    return r;
+}
+
 // ---- units and groups
 // Unit u = (bin row, x block of kUnitBins bins); its points are one contiguous sorted range.
 __device__ __forceinline__ void unit_range(int64_t u, const Grid &g, int nxb, const int32_t *cs, int32_t &s,
@@ -307,9 +320,10 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_cl_count(SortedPtsView P, 
                 if (ok[u][h]) {
                     const int p = (int)Q4[t];
                     list[base + t] = p;
-                    xs[u][h] = P.x[p];
-                    ys[u][h] = P.y[p];
-                    if (DIM == 3) zs[u][h] = P.z[p];
+                    const PtRec c = load_pt(P.a, p);
+                    xs[u][h] = c.x;
+                    ys[u][h] = c.y;
+                    if (DIM == 3) zs[u][h] = c.z;
                 }
             }
 #pragma unroll
@@ -549,10 +563,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_cl_fill(SortedPtsView P, Grid g,
             for (int r = 0; r < kFillRounds; ++r) {
                 const int e = 32 * r + lane;
                 const int p = (e < li[h]) ? list[base + ent[(size_t)(i0 + h) * S + e]] : list[base];
-                cx[h][r] = P.x[p];
-                cy[h][r] = P.y[p];
-                cz[h][r] = (DIM == 3) ? P.z[p] : 0.0;
-                cid[h][r] = P.id[p];
+                const PtRec c = load_pt(P.a, p);
+                cx[h][r] = c.x;
+                cy[h][r] = c.y;
+                cz[h][r] = (DIM == 3) ? c.z : 0.0;
+                cid[h][r] = c.id;
             }
         double hsum[2] = {0.0, 0.0};
 #pragma unroll
@@ -573,9 +588,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_cl_fill(SortedPtsView P, Grid g,
         for (int h = 0; h < 2; ++h)
             for (int e = 32 * kFillRounds + lane; e < li[h]; e += 32) {
                 const int p = list[base + ent[(size_t)(i0 + h) * S + e]];
-                const double d2 = pair_d2<DIM>(qx[h], qy[h], qz[h], P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0);
+                const PtRec c = load_pt(P.a, p);
+                const double d2 = pair_d2<DIM>(qx[h], qy[h], qz[h], c.x, c.y, (DIM == 3) ? c.z : 0.0);
                 const double w = weight_of(rmin, d2);
-                cols[bi[h] + e] = P.id[p];
+                cols[bi[h] + e] = c.id;
                 vals[bi[h] + e] = w;
                 hsum[h] += w;
                 TF_DCHECK(d2 < r2);

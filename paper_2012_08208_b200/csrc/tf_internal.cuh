@@ -201,6 +201,7 @@ struct SortedPtsView {
     const double *x, *y, *z;  // SoA, sorted by (bin key, id)
     const int32_t *id;
     const int32_t *cs;        // cell start [nbins+1]
+    const double4 *a;         // AoS copy (x, y, z, id bits): one 32-byte sector per gathered point
 };
 
 // ------------------------------------------------------------------ apply plan
