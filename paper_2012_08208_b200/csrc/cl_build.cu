@@ -641,6 +641,338 @@ __global__ void __launch_bounds__(WARPS * 32) k_cl_fill(SortedPtsView P, Grid g,
     }
 }
 
+// ------------------------------------------------------------------ a7: fill, warp per group, row by row
+// The default fill (round 2, second version). Warp per group; the rows of the group's queries are
+// written one after the other, and the expansion of a row's mask words into its candidate list is
+// done by the whole warp, right before the row is written:
+//  expansion (lane = mask word of the row): popcount, warp scan of the counts -> each lane appends
+//    the bit positions of its own word at its offset of the row's list (ascending = ascending
+//    column). Lists are double-buffered per warp ([2][S] uint16), so the list of row i + 1 is built
+//    while the candidate points of row i are in flight;
+//  emission (lane = entry): ROUNDS 32-entry rounds in flight: sorted position from the group's
+//    union list, the whole point in one 256-bit load, the oracle's d^2 and weight, coalesced
+//    int32 / fp64 stores, Hs by a fixed-order lane reduction.
+// Against k_cl_fill this keeps no transposed mask copy and no per-query lists in shared memory
+// (10.5 KB -> < 0.5 KB per warp at config 5) and has no serial per-lane walk at the start of a group;
+// the occupancy limit becomes the register count (launch bounds: kFill2MinBlocks blocks of 4 warps).
+#ifndef TF_CL_FILL2_MINB
+#define TF_CL_FILL2_MINB 8
+#endif
+constexpr int kFill2Warps = 4;
+constexpr int kFill2MinBlocks = TF_CL_FILL2_MINB;
+
+// list of query i of the group: expand the set bits of its mask words (mk[32 * k + i], k < nw) into
+// dst[0..n) (candidate indices, ascending); returns n (uniform). Entries beyond cap are dropped.
+__device__ __forceinline__ int expand_row(const uint32_t *__restrict__ mk, int i, int nw, uint16_t *dst, int cap,
+                                          int lane) {
+    int done = 0;
+    for (int k0 = 0; k0 < nw; k0 += 32) {
+        const int k = k0 + lane;
+        uint32_t w = (k < nw) ? mk[32 * k + i] : 0u;
+        const int c = __popc(w);
+        int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        int e = done + inc - c;
+        const int t0 = 32 * k;
+        while (w) {
+            const int b = __clz(w);
+            if (e < cap) dst[e] = (uint16_t)(t0 + b);
+            ++e;
+            w ^= 0x80000000u >> b;
+        }
+        done += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    return done;
+}
+
+template <int DIM, int ROUNDS>
+__global__ void __launch_bounds__(kFill2Warps * 32, kFill2MinBlocks)
+    k_cl_fill2(SortedPtsView P, Grid g, const GroupRec *__restrict__ rec, const int64_t *__restrict__ loff, int32_t G,
+               int S, const int32_t *__restrict__ list, const uint32_t *__restrict__ mask,
+               const int64_t *__restrict__ rowptr, int32_t *__restrict__ cols, double *__restrict__ vals,
+               double *__restrict__ hs, int32_t *__restrict__ stats) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t gi = (int32_t)blockIdx.x * kFill2Warps + warp;
+    if (gi >= G) return;
+    uint16_t *ent = reinterpret_cast<uint16_t *>(smem_raw) + (size_t)warp * 2 * S;  // [2][S]
+    const GroupRec R = rec[gi];
+    const int nq = R.q1 - R.q0;
+    const int L = R.L, nw = (L + 31) >> 5;
+    const int64_t base = loff[gi];
+    const uint32_t *mk = mask + base;
+    const int32_t *ul = list + base;
+    const int q = R.q0 + lane;
+    const bool have = lane < nq;
+    int32_t qid = 0;
+    int64_t rbase = 0;
+    int len = 0;
+    double qxl = 0.0, qyl = 0.0, qzl = 0.0;
+    if (have) {
+        const PtRec c = load_pt(P.a, q);
+        qid = c.id;
+        qxl = c.x, qyl = c.y, qzl = c.z;
+        rbase = rowptr[qid];
+        len = (int)(rowptr[qid + 1] - rbase);
+    }
+    const double rmin = g.rmin;
+#ifdef TF_DEBUG_CHECKS
+    const double r2 = g.r2;
+#endif
+    int bad = 0;
+    int n_next = expand_row(mk, 0, nw, ent, S, lane);
+    __syncwarp();
+    for (int i = 0; i < nq; ++i) {
+        const uint16_t *my = ent + (size_t)(i & 1) * S;
+        const int li = __shfl_sync(0xffffffffu, len, i);
+        const int64_t bi = __shfl_sync(0xffffffffu, rbase, i);
+        const int32_t qi = __shfl_sync(0xffffffffu, qid, i);
+        const double qx = __shfl_sync(0xffffffffu, qxl, i), qy = __shfl_sync(0xffffffffu, qyl, i);
+        const double qz = (DIM == 3) ? __shfl_sync(0xffffffffu, qzl, i) : 0.0;
+        bad |= (n_next != li);  // count/fill agreement (always-on invariant)
+        const bool longrow = li > S;
+        const int lr = longrow ? 0 : li;
+        // candidate points of the first ROUNDS rounds: loads first
+        PtRec c[ROUNDS];
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r) {
+            const int e = 32 * r + lane;
+            const int p = ul[(e < lr) ? my[e] : 0];
+            c[r] = load_pt(P.a, p);
+        }
+        // the next row's list, while those are in flight
+        if (i + 1 < nq) n_next = expand_row(mk, i + 1, nw, ent + (size_t)((i + 1) & 1) * S, S, lane);
+        double hsum = 0.0;
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r) {
+            const int e = 32 * r + lane;
+            if (e < lr) {
+                const double d2 = pair_d2<DIM>(qx, qy, qz, c[r].x, c[r].y, c[r].z);
+                const double w = weight_of(rmin, d2);
+                cols[bi + e] = c[r].id;
+                vals[bi + e] = w;
+                hsum += w;
+                TF_DCHECK(d2 < r2);
+            }
+        }
+        for (int e = 32 * ROUNDS + lane; e < lr; e += 32) {
+            const PtRec cc = load_pt(P.a, ul[my[e]]);
+            const double d2 = pair_d2<DIM>(qx, qy, qz, cc.x, cc.y, cc.z);
+            const double w = weight_of(rmin, d2);
+            cols[bi + e] = cc.id;
+            vals[bi + e] = w;
+            hsum += w;
+            TF_DCHECK(d2 < r2);
+        }
+        if (longrow) {
+            // rows longer than the list (dense clusters): lane = mask word, each lane emits its bits
+            int done = 0;
+            for (int k0 = 0; k0 < nw; k0 += 32) {
+                const int k = k0 + lane;
+                uint32_t w = (k < nw) ? mk[32 * k + i] : 0u;
+                const int cnt = __popc(w);
+                int inc = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += v;
+                }
+                int e = done + inc - cnt;
+                while (w) {
+                    const int b = __clz(w);
+                    const PtRec cc = load_pt(P.a, ul[32 * k + b]);
+                    const double d2 = pair_d2<DIM>(qx, qy, qz, cc.x, cc.y, cc.z);
+                    const double wt = weight_of(rmin, d2);
+                    cols[bi + e] = cc.id;
+                    vals[bi + e] = wt;
+                    hsum += wt;
+                    TF_DCHECK(d2 < r2);
+                    ++e;
+                    w ^= 0x80000000u >> b;
+                }
+                done += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
+        if (lane == 0) hs[qi] = hsum;
+        __syncwarp();
+    }
+    if (bad) atomicOr(&stats[2], 1);
+}
+
+template <int DIM, int ROUNDS>
+tf_status launch_cl_fill2(const SortedPtsView &P, const Grid &g, const GroupRec *rec, const int64_t *loff, int32_t G,
+                          int S, const int32_t *list, const uint32_t *mask, tf_filter_s *h, int32_t *stats,
+                          cudaStream_t s) {
+    const size_t smem = (size_t)kFill2Warps * 2 * S * sizeof(uint16_t);
+    auto kern = k_cl_fill2<DIM, ROUNDS>;
+    kern<<<(unsigned)(((int64_t)G + kFill2Warps - 1) / kFill2Warps), kFill2Warps * 32, smem, s>>>(
+        P, g, rec, loff, G, S, list, mask, h->rowptr, h->cols, h->vals, h->hs, stats);
+    TF_LAUNCH_CHECK();
+    return TF_OK;
+}
+
+// ------------------------------------------------------------------ a7: fill, warp per group, masks from L1
+// k_cl_fill with two changes for occupancy (the fill is latency-bound at 5 blocks of 4 warps per SM):
+// the walk reads each lane's mask words straight from global memory (word k of query q at [k][q]:
+// the group's words stay L1-resident; the next word is loaded one step ahead), so no transposed mask
+// copy in shared memory (10.5 -> 5.8 KB per warp at config 5); rows are written one at a time with
+// ROUNDS rounds in flight, which fits 64 registers (8 blocks per SM).
+#ifndef TF_CL_FILL3_MINB
+#define TF_CL_FILL3_MINB 8
+#endif
+template <int DIM, int ROUNDS>
+__global__ void __launch_bounds__(128, TF_CL_FILL3_MINB)
+    k_cl_fill3(SortedPtsView P, Grid g, const GroupRec *__restrict__ rec, const int64_t *__restrict__ loff, int32_t G,
+               int S, const int32_t *__restrict__ list, const uint32_t *__restrict__ mask,
+               const int64_t *__restrict__ rowptr, int32_t *__restrict__ cols, double *__restrict__ vals,
+               double *__restrict__ hs, int32_t *__restrict__ stats) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t gi = (int32_t)blockIdx.x * 4 + warp;
+    if (gi >= G) return;
+    uint16_t *ent = reinterpret_cast<uint16_t *>(smem_raw) + (size_t)warp * 32 * S;  // [32][S]
+    const GroupRec R = rec[gi];
+    const int nq = R.q1 - R.q0;
+    const int L = R.L, nw = (L + 31) >> 5;
+    const int64_t base = loff[gi];
+    const uint32_t *mk = mask + base + lane;  // word k of this lane's query at mk[32 * k]
+    const int32_t *ul = list + base;
+    const bool have = lane < nq;
+    int32_t qid = 0;
+    int64_t rbase = 0;
+    int len = 0;
+    double qxl = 0.0, qyl = 0.0, qzl = 0.0;
+    if (have) {
+        const PtRec c = load_pt(P.a, R.q0 + lane);
+        qid = c.id;
+        qxl = c.x, qyl = c.y, qzl = c.z;
+        rbase = rowptr[qid];
+        len = (int)(rowptr[qid + 1] - rbase);
+    }
+    {
+        // branch-free walk: every step either emits up to two set bits of the current word or moves
+        // to the next word (loaded one step ahead)
+        uint16_t *my = ent + (size_t)lane * S;
+        const int kend = have ? nw : 0;
+        int n = 0, k = 0;
+        uint32_t w = (kend > 0) ? mk[0] : 0u;
+        uint32_t wnext = (kend > 1) ? mk[32] : 0u;
+        while (__any_sync(0xffffffffu, k < kend)) {
+#pragma unroll 2
+            for (int u = 0; u < 2; ++u) {
+                const bool z = (w == 0);
+                const int b1 = __clz(w) & 31;
+                const uint32_t w1 = w ^ (0x80000000u >> b1);
+                const int b2 = __clz(w1) & 31;
+                const bool two = !z && (w1 != 0);
+                my[min(n, S - 1)] = (uint16_t)(32 * k + b1);
+                my[min(n + 1, S - 1)] = (uint16_t)(32 * k + b2);
+                n += z ? 0 : (two ? 2 : 1);
+                const bool step = z && (k < kend);
+                const uint32_t wl = (step && k + 2 < kend) ? mk[32 * (k + 2)] : 0u;
+                w = z ? wnext : (two ? (w1 ^ (0x80000000u >> b2)) : 0u);
+                wnext = step ? wl : wnext;
+                k = step ? k + 1 : k;
+            }
+        }
+        if (have && n != len) atomicOr(&stats[2], 1);  // count/fill agreement (always-on invariant)
+    }
+    __syncwarp();
+    const double rmin = g.rmin;
+#ifdef TF_DEBUG_CHECKS
+    const double r2 = g.r2;
+#endif
+    for (int i = 0; i < nq; ++i) {
+        const uint16_t *my = ent + (size_t)i * S;
+        const int li = __shfl_sync(0xffffffffu, len, i);
+        const int64_t bi = __shfl_sync(0xffffffffu, rbase, i);
+        const int32_t qi = __shfl_sync(0xffffffffu, qid, i);
+        const double qx = __shfl_sync(0xffffffffu, qxl, i), qy = __shfl_sync(0xffffffffu, qyl, i);
+        const double qz = (DIM == 3) ? __shfl_sync(0xffffffffu, qzl, i) : 0.0;
+        const bool longrow = li > S - 2;
+        const int lr = longrow ? 0 : li;
+        PtRec c[ROUNDS];
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r) {
+            const int e = 32 * r + lane;
+            c[r] = load_pt(P.a, ul[(e < lr) ? my[e] : 0]);
+        }
+        double hsum = 0.0;
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r) {
+            const int e = 32 * r + lane;
+            if (e < lr) {
+                const double d2 = pair_d2<DIM>(qx, qy, qz, c[r].x, c[r].y, c[r].z);
+                const double w = weight_of(rmin, d2);
+                cols[bi + e] = c[r].id;
+                vals[bi + e] = w;
+                hsum += w;
+                TF_DCHECK(d2 < r2);
+            }
+        }
+        for (int e = 32 * ROUNDS + lane; e < lr; e += 32) {
+            const PtRec cc = load_pt(P.a, ul[my[e]]);
+            const double d2 = pair_d2<DIM>(qx, qy, qz, cc.x, cc.y, cc.z);
+            const double w = weight_of(rmin, d2);
+            cols[bi + e] = cc.id;
+            vals[bi + e] = w;
+            hsum += w;
+            TF_DCHECK(d2 < r2);
+        }
+        if (longrow) {
+            // rows longer than the lists (dense clusters): lane = mask word, each lane emits its bits
+            int done = 0;
+            for (int k0 = 0; k0 < nw; k0 += 32) {
+                const int k = k0 + lane;
+                uint32_t w = (k < nw) ? mask[base + 32 * k + i] : 0u;
+                const int cnt = __popc(w);
+                int inc = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += v;
+                }
+                int e = done + inc - cnt;
+                while (w) {
+                    const int b = __clz(w);
+                    const PtRec cc = load_pt(P.a, ul[32 * k + b]);
+                    const double d2 = pair_d2<DIM>(qx, qy, qz, cc.x, cc.y, cc.z);
+                    const double wt = weight_of(rmin, d2);
+                    cols[bi + e] = cc.id;
+                    vals[bi + e] = wt;
+                    hsum += wt;
+                    TF_DCHECK(d2 < r2);
+                    ++e;
+                    w ^= 0x80000000u >> b;
+                }
+                done += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
+        if (lane == 0) hs[qi] = hsum;
+    }
+}
+
+template <int DIM, int ROUNDS>
+tf_status launch_cl_fill3(const SortedPtsView &P, const Grid &g, const GroupRec *rec, const int64_t *loff, int32_t G,
+                          int S, const int32_t *list, const uint32_t *mask, tf_filter_s *h, int32_t *stats,
+                          cudaStream_t s) {
+    const size_t smem = (size_t)4 * 32 * S * sizeof(uint16_t);
+    auto kern = k_cl_fill3<DIM, ROUNDS>;
+    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)(((int64_t)G + 3) / 4), 128, smem, s>>>(P, g, rec, loff, G, S, list, mask, h->rowptr, h->cols,
+                                                             h->vals, h->hs, stats);
+    TF_LAUNCH_CHECK();
+    return TF_OK;
+}
+
 // ------------------------------------------------------------------ a7: fill, block per group
 // One block of kFillBWarps warps per group (kGroupQ = 32 queries). The group's sorted union is
 // staged in shared memory once -- exact fp64 coordinates and ids --, so every entry's candidate
@@ -990,6 +1322,37 @@ tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_
     // the block-per-group fill (union staged in shared memory) measured 8.90 vs 8.60 ms at config 5
     // and 0.42 vs 0.47 ms at config 4: opt-in (TOPOFILT_CL_FILL=block, benchmarks and tests)
     const char *fk = getenv("TOPOFILT_CL_FILL");
+    if (kGroupQ == 32 && !(fk && (!strcmp(fk, "block") || !strcmp(fk, "walk") || !strcmp(fk, "rows")))) {
+        // default: the walk fill with the mask words read from L1 and one row at a time in flight
+        const int rounds = std::min(3, (std::min(maxrow, 96) + 31) / 32);
+#define TF_FILL3(D, R) TF_TRY((launch_cl_fill3<D, R>(P, g, rec.p, loff.p, hG, S, list.p, mask.p, h, stats.p, s)))
+        if (dim == 3) {
+            if (rounds >= 3) TF_FILL3(3, 3);
+            else if (rounds == 2) TF_FILL3(3, 2);
+            else TF_FILL3(3, 1);
+        } else {
+            if (rounds >= 3) TF_FILL3(2, 3);
+            else if (rounds == 2) TF_FILL3(2, 2);
+            else TF_FILL3(2, 1);
+        }
+#undef TF_FILL3
+    } else if (kGroupQ == 32 && fk && !strcmp(fk, "rows")) {
+        // default: row-by-row fill; list stride = longest row rounded up to 32 (capped), rounds in
+        // flight from the longest row
+        const int S2 = std::max(32, (std::min(maxrow, 1024) + 31) & ~31);
+        const int rounds = std::min(3, (std::min(maxrow, 96) + 31) / 32);
+#define TF_FILL2(D, R) TF_TRY((launch_cl_fill2<D, R>(P, g, rec.p, loff.p, hG, S2, list.p, mask.p, h, stats.p, s)))
+        if (dim == 3) {
+            if (rounds >= 3) TF_FILL2(3, 3);
+            else if (rounds == 2) TF_FILL2(3, 2);
+            else TF_FILL2(3, 1);
+        } else {
+            if (rounds >= 3) TF_FILL2(2, 3);
+            else if (rounds == 2) TF_FILL2(2, 2);
+            else TF_FILL2(2, 1);
+        }
+#undef TF_FILL2
+    } else {
     const size_t smem_b = (size_t)LPmax * ((dim == 3 ? 24 : 16) + 4) + (size_t)32 * MS * 4 + (size_t)32 * S * 2;
     if (kGroupQ == 32 && fk && !strcmp(fk, "block") && smem_b <= di.smem_optin) {
         if (dim == 3) TF_TRY((launch_cl_fill_b<3>(P, g, rec.p, loff.p, hG, LPmax, MS, S, list.p, mask.p, h, stats.p, s)));
@@ -1005,6 +1368,7 @@ tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_
         if (fw >= 4) TF_TRY((launch_cl_fill<2, 4>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
         else if (fw >= 2) TF_TRY((launch_cl_fill<2, 2>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
         else TF_TRY((launch_cl_fill<2, 1>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
+    }
     }
     }
     build_trace().mark("fill", s);
