@@ -136,9 +136,13 @@ def test_paper_right_left_triangles(tf):
     check_paths_agree(tf, c, 2.0)
 
 
-def test_block_fill_variant(tf, monkeypatch):
-    """The opt-in block-per-group fill (TOPOFILT_CL_FILL=block) builds the same CSR."""
-    monkeypatch.setenv("TOPOFILT_CL_FILL", "block")
+@pytest.mark.parametrize("kernel", ["walk3", "split", "rows", "walk", "block"])
+def test_fill_kernel_variants(tf, monkeypatch, kernel):
+    """Every fill kernel of the group path builds the oracle's CSR: k_cl_fill3 (walk3: the default for
+    3D-sized unions), k_cl_fill4 (split: the default for small unions), and the opt-in k_cl_fill2 (rows),
+    k_cl_fill (walk) and k_cl_fill_b (block) -- on a 2D ground structure, a jittered Kuhn mesh and a
+    dense cluster whose rows exceed the per-lane lists (word-parallel long-row path)."""
+    monkeypatch.setenv("TOPOFILT_CL_FILL", kernel)
     for c, rmin in ((synth.ground_structure(4, 400, 300)[0], 3.0), (synth.kuhn_mesh(10, 8, 6, jitter=0.1, stream=5)[0], 1.5),
                     (np.concatenate([np.random.default_rng(2).uniform(0, 1.0, size=(900, 3)),
                                      np.random.default_rng(3).uniform(0, 20, size=(3000, 3))]), 1.1)):

@@ -1,7 +1,7 @@
 # quick iteration on the cell-list build: bitwise check + timing (configs 3 4 5), group-kernel tests,
 # optional ncu metrics (NCU_CFG=4|5)
 set -x
-python tools/cl_check.py 3 4 5 > gpurun_out/cl_check.jsonl 2>&1; echo clcheck=$?; cat gpurun_out/cl_check.jsonl | cut -c1-420
+python tools/cl_check.py ${CFGS:-3 4 5} > gpurun_out/cl_check.jsonl 2>&1; echo clcheck=$?; cat gpurun_out/cl_check.jsonl | cut -c1-420
 TOPOFILT_TRACE=1 BUILD_PATHS=cell_list python tools/build_paths.py 4 5 2>&1 | grep -v '^{' | tail -4
 timeout 900 python -m pytest tests/test_gpu_cl_groups.py tests/test_gpu_fuzz.py -m gpu -q -x > gpurun_out/cl_tests.log 2>&1; echo pytest=$?; tail -3 gpurun_out/cl_tests.log
 for c in ${NCU_CFG:-}; do
