@@ -52,6 +52,11 @@ constexpr int kUnitBins = 32;     // bins per unit along x: a group spans at mos
 constexpr int kGroupQ = TF_CL_GROUPQ;  // queries per group (they share one sorted union); 32 per fill warp
 constexpr int kHalves = kGroupQ / 32;
 constexpr int kMaxUnion = 6144;   // largest union (candidates) the group kernels take
+constexpr int kListCap = 256;     // per-lane list capacity of the fills; longer rows take the word-parallel path
+// The sorted union handed from the count to the fill is a list of 16-bit codes (run << kRunShift) |
+// offset-in-run (sorted position = run start + offset): half the bytes and sectors of a position list.
+constexpr int kRunShift = 12;
+constexpr int kMaxRun = 1 << kRunShift;  // longest union run the codes can address
 constexpr float kFarCC = 1e30f;   // |c|^2 of padding candidates / q of idle lanes: never "in"
 
 struct GroupRec {
@@ -136,14 +141,15 @@ __device__ __forceinline__ void group_run(int r, const GroupRec &G, const Grid &
     len = cs[rb + xh + 1] - s;
 }
 
-// Thread per unit: the unit's group records and padded union sizes; stats[0] = max union.
+// Thread per unit: the unit's group records and padded union sizes; stats[0] = max union,
+// stats[1] = longest union run.
 template <int DIM>
 __global__ void __launch_bounds__(256) k_cl_groups(const int32_t *__restrict__ cs, const uint32_t *__restrict__ keys,
                                                    Grid g, int nxb, int64_t U, const int32_t *__restrict__ goff,
                                                    GroupRec *__restrict__ rec, int32_t *__restrict__ lp,
                                                    int32_t *__restrict__ stats) {
     constexpr int NR = (DIM == 3) ? 9 : 3;
-    int best = 0;
+    int best = 0, longest = 0;
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < U; u += (int64_t)gridDim.x * blockDim.x) {
         int32_t s, e;
         unit_range(u, g, nxb, cs, s, e);
@@ -161,6 +167,7 @@ __global__ void __launch_bounds__(256) k_cl_groups(const int32_t *__restrict__ c
                 int rs, rl;
                 group_run<DIM>(r, G, g, cs, rs, rl);
                 L += rl;
+                longest = max(longest, rl);
             }
             G.L = L;
             rec[gi] = G;
@@ -168,8 +175,11 @@ __global__ void __launch_bounds__(256) k_cl_groups(const int32_t *__restrict__ c
             best = max(best, L);
         }
     }
-    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if ((threadIdx.x & 31) == 0 && best > 0) atomicMax(&stats[0], best);
+    for (int o = 16; o > 0; o >>= 1) {
+        best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+        longest = max(longest, __shfl_xor_sync(0xffffffffu, longest, o));
+    }
+    if ((threadIdx.x & 31) == 0 && best > 0) atomicMax(&stats[0], best), atomicMax(&stats[1], longest);
 }
 
 // Per-group origin and the R4c error band. o = centre of the union box; Mx, My, Mz bound
@@ -214,7 +224,7 @@ constexpr int kCountWarps = TF_CL_COUNT_WARPS;
 template <int DIM>
 __global__ void __launch_bounds__(kCountWarps * 32) k_cl_count(SortedPtsView P, Grid g, const GroupRec *__restrict__ rec,
                                                                 const int64_t *__restrict__ loff, int LPmax,
-                                                                int32_t *__restrict__ list, uint32_t *__restrict__ mask,
+                                                                uint16_t *__restrict__ list, uint32_t *__restrict__ mask,
                                                                 int32_t *__restrict__ counts,
                                                                 int32_t *__restrict__ stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -282,22 +292,23 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_cl_count(SortedPtsView P, 
     //   even passes: ka = Q3, va = Q4, kb = Q0, vb = Q1;  odd: ka = Q0, va = Q1, kb = Q3, vb = Q4
     uint32_t *KA = (passes & 1) ? Q0 : Q3, *VA = (passes & 1) ? Q1 : Q4;
     uint32_t *KB = (passes & 1) ? Q3 : Q0, *VB = (passes & 1) ? Q4 : Q1;
-    // (2b) stage (id - lo, sorted-SoA position) in run order
+    // (2b) stage (id - lo, run code of the sorted-SoA position) in run order
     {
         int r = 0;
         for (int t0 = 0; t0 < L; t0 += 4 * T) {
-            int id[4], pp[4];
+            int id[4];
+            uint32_t cd[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int t = t0 + u * T + tid;
                 while (r < NR - 1 && t >= run_x[r + 1]) ++r;
-                pp[u] = run_s[r] + (t - run_x[r]);
-                id[u] = (t < L) ? P.id[pp[u]] : 0;
+                cd[u] = ((uint32_t)r << kRunShift) | (uint32_t)(t - run_x[r]);
+                id[u] = (t < L) ? P.id[run_s[r] + (t - run_x[r])] : 0;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int t = t0 + u * T + tid;
-                if (t < L) KA[t] = (uint32_t)(id[u] - lo), VA[t] = (uint32_t)pp[u];
+                if (t < L) KA[t] = (uint32_t)(id[u] - lo), VA[t] = cd[u];
             }
         }
     }
@@ -321,9 +332,9 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_cl_count(SortedPtsView P, 
                 ok[u][h] = (j < LP / 2) && (t < L);
                 xs[u][h] = ys[u][h] = zs[u][h] = 0.0;
                 if (ok[u][h]) {
-                    const int p = (int)Q4[t];
-                    list[base + t] = p;
-                    const PtRec c = load_pt(P.a, p);
+                    const uint32_t cd = Q4[t];
+                    list[base + t] = (uint16_t)cd;
+                    const PtRec c = load_pt(P.a, run_s[cd >> kRunShift] + (int)(cd & (kMaxRun - 1)));
                     xs[u][h] = c.x;
                     ys[u][h] = c.y;
                     if (DIM == 3) zs[u][h] = c.z;
@@ -448,7 +459,8 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_cl_count(SortedPtsView P, 
                         u = __fmaf_rn(my, Af[4 * j + 2 + hh], u);
                     }
                     if (__float_as_uint(u) <= dbits && t < L) {
-                        const PtRec c = load_pt(P.a, (int)Q4[t]);
+                        const uint32_t cd = Q4[t];
+                        const PtRec c = load_pt(P.a, run_s[cd >> kRunShift] + (int)(cd & (kMaxRun - 1)));
                         if (pair_d2<DIM>(qxd[h], qyd[h], qzd[h], c.x, c.y, (DIM == 3) ? c.z : 0.0) < r2)
                             w |= 0x80000000u >> b;
                     }
@@ -475,377 +487,6 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_cl_count(SortedPtsView P, 
     }
 }
 
-// ------------------------------------------------------------------ a7: fill (group kernel)
-// Warp per half group (32 queries), two phases.
-//  expansion (lane = query): the half's mask words are staged in shared memory transposed to
-//    [lane][word] (odd stride); each lane walks its own words -- up to two set bits or one word step
-//    per iteration, independently of the other lanes -- and appends the candidate indices
-//    (ascending = ascending column) to its list ent[lane][0..len);
-//  emission (lane = entry): two rows per pass, their first kFillRounds 32-entry rounds in flight
-//    together: sorted-SoA position from the group's union list, exact fp64 coordinates and id,
-//    the oracle's d^2 and weight, coalesced int32 / fp64 stores, Hs by a fixed-order lane reduction.
-// Shared memory per warp: masks [32][MS] uint32 (MS odd, > words) + lists [32][S] uint16.
-#ifndef TF_CL_FILL_ROUNDS
-#define TF_CL_FILL_ROUNDS 3
-#endif
-constexpr int kFillRounds = TF_CL_FILL_ROUNDS;
-constexpr int kListCap = 256;  // per-lane list capacity; longer rows take the word-parallel path
-
-template <int DIM, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_cl_fill(SortedPtsView P, Grid g, const GroupRec *__restrict__ rec,
-                                                        const int64_t *__restrict__ loff, int32_t G, int MS, int S,
-                                                        const int32_t *__restrict__ list,
-                                                        const uint32_t *__restrict__ mask,
-                                                        const int64_t *__restrict__ rowptr,
-                                                        int32_t *__restrict__ cols, double *__restrict__ vals,
-                                                        double *__restrict__ hs, int32_t *__restrict__ stats) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int32_t wi = (int32_t)blockIdx.x * WARPS + warp;
-    const int32_t gi = wi / kHalves, half = wi % kHalves;
-    if (gi >= G) return;
-    const size_t per_warp = (size_t)32 * MS * 4 + (size_t)32 * S * 2;
-    uint32_t *sm = reinterpret_cast<uint32_t *>(smem_raw + (size_t)warp * per_warp);  // [32][MS]
-    uint16_t *ent = reinterpret_cast<uint16_t *>(sm + 32 * MS);                       // [32][S]
-    GroupRec R = rec[gi];
-    R.q0 += 32 * half;  // this warp's queries
-    R.q1 = min(R.q1, R.q0 + 32);
-    if (R.q0 >= R.q1) return;
-    const int L = R.L, LP = (L + 31) & ~31, nw = LP >> 5;
-    const int64_t base = loff[gi];
-    const uint32_t *mk = mask + kHalves * base + 32 * half;
-    for (int k0 = 0; k0 < MS; k0 += 4) {
-        uint32_t m[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) m[u] = (k0 + u < nw) ? mk[kGroupQ * (k0 + u) + lane] : 0u;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (k0 + u < MS) sm[lane * MS + k0 + u] = m[u];
-    }
-    const int q = R.q0 + lane;
-    const bool have = q < R.q1;
-    int32_t qid = 0;
-    int64_t rbase = 0;
-    int len = 0;
-    if (have) {
-        qid = P.id[q];
-        rbase = rowptr[qid];
-        len = (int)(rowptr[qid + 1] - rbase);
-    }
-    __syncwarp();
-    {
-        // branch-free walk: every iteration either emits the lane's next set bit or steps to its
-        // next word (mw has MS >= nw + 1 words per lane, the extra one zero)
-        const uint32_t *mw = sm + lane * MS;
-        uint16_t *my = ent + (size_t)lane * S;
-        int n = 0, k = 0;
-        uint32_t w = mw[0];
-        const int kend = have ? nw : 0;
-        while (__any_sync(0xffffffffu, k < kend)) {
-#pragma unroll 2
-            for (int u = 0; u < 2; ++u) {
-                // up to two set bits of the current word, or one word step
-                const bool z = (w == 0);
-                const int b1 = __clz(w) & 31;
-                const uint32_t w1 = w ^ (0x80000000u >> b1);
-                const int b2 = __clz(w1) & 31;
-                const bool two = !z && (w1 != 0);
-                my[min(n, S - 1)] = (uint16_t)(32 * k + b1);
-                my[min(n + 1, S - 1)] = (uint16_t)(32 * k + b2);
-                n += z ? 0 : (two ? 2 : 1);
-                const uint32_t wn = mw[min(k + 1, MS - 1)];
-                w = z ? wn : (two ? (w1 ^ (0x80000000u >> b2)) : 0u);
-                k = z ? min(k + 1, nw) : k;
-            }
-        }
-        if (have && n != len) atomicOr(&stats[2], 1);  // count/fill agreement (always-on invariant)
-    }
-    __syncwarp();
-    const double rmin = g.rmin;
-#ifdef TF_DEBUG_CHECKS
-    const double r2 = g.r2;
-#endif
-    const int nq = R.q1 - R.q0;
-    for (int i0 = 0; i0 < nq; i0 += 2) {
-        int li[2];
-        bool longrow[2];
-        int32_t qi[2];
-        int64_t bi[2];
-        double qx[2], qy[2], qz[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int i = min(i0 + h, nq - 1);
-            li[h] = (i0 + h < nq) ? __shfl_sync(0xffffffffu, len, i) : 0;
-            longrow[h] = li[h] > S - 2;
-            if (longrow[h]) li[h] = 0;
-            bi[h] = __shfl_sync(0xffffffffu, rbase, i);
-            qi[h] = __shfl_sync(0xffffffffu, qid, i);
-            qx[h] = P.x[R.q0 + i];
-            qy[h] = P.y[R.q0 + i];
-            qz[h] = (DIM == 3) ? P.z[R.q0 + i] : 0.0;
-        }
-        double cx[2][kFillRounds], cy[2][kFillRounds], cz[2][kFillRounds];
-        int32_t cid[2][kFillRounds];
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int r = 0; r < kFillRounds; ++r) {
-                const int e = 32 * r + lane;
-                const int p = (e < li[h]) ? list[base + ent[(size_t)(i0 + h) * S + e]] : list[base];
-                const PtRec c = load_pt(P.a, p);
-                cx[h][r] = c.x;
-                cy[h][r] = c.y;
-                cz[h][r] = (DIM == 3) ? c.z : 0.0;
-                cid[h][r] = c.id;
-            }
-        double hsum[2] = {0.0, 0.0};
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int r = 0; r < kFillRounds; ++r) {
-                const int e = 32 * r + lane;
-                if (e < li[h]) {
-                    const double d2 = pair_d2<DIM>(qx[h], qy[h], qz[h], cx[h][r], cy[h][r], cz[h][r]);
-                    const double w = weight_of(rmin, d2);
-                    cols[bi[h] + e] = cid[h][r];
-                    vals[bi[h] + e] = w;
-                    hsum[h] += w;
-                    TF_DCHECK(d2 < r2);
-                }
-            }
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-            for (int e = 32 * kFillRounds + lane; e < li[h]; e += 32) {
-                const int p = list[base + ent[(size_t)(i0 + h) * S + e]];
-                const PtRec c = load_pt(P.a, p);
-                const double d2 = pair_d2<DIM>(qx[h], qy[h], qz[h], c.x, c.y, (DIM == 3) ? c.z : 0.0);
-                const double w = weight_of(rmin, d2);
-                cols[bi[h] + e] = c.id;
-                vals[bi[h] + e] = w;
-                hsum[h] += w;
-                TF_DCHECK(d2 < r2);
-            }
-        // rows longer than the lists (dense clusters): lane = mask word of the row, positions from
-        // a warp scan of the words' popcounts, each lane emits its word's bits
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            if (!longrow[h]) continue;
-            const int i = i0 + h;
-            int done = 0;
-            for (int k0 = 0; k0 < nw; k0 += 32) {
-                const int k = k0 + lane;
-                uint32_t w = (k < nw) ? sm[i * MS + k] : 0u;
-                const int c = __popc(w);
-                int inc = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += v;
-                }
-                int e = done + inc - c;
-                while (w) {
-                    const int b = __clz(w);
-                    const int p = list[base + 32 * k + b];
-                    const double d2 = pair_d2<DIM>(qx[h], qy[h], qz[h], P.x[p], P.y[p], (DIM == 3) ? P.z[p] : 0.0);
-                    const double wt = weight_of(rmin, d2);
-                    cols[bi[h] + e] = P.id[p];
-                    vals[bi[h] + e] = wt;
-                    hsum[h] += wt;
-                    TF_DCHECK(d2 < r2);
-                    ++e;
-                    w ^= 0x80000000u >> b;
-                }
-                done += __shfl_sync(0xffffffffu, inc, 31);
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            hsum[0] += __shfl_xor_sync(0xffffffffu, hsum[0], o);
-            hsum[1] += __shfl_xor_sync(0xffffffffu, hsum[1], o);
-        }
-        if (lane == 0) {
-            hs[qi[0]] = hsum[0];
-            if (i0 + 1 < nq) hs[qi[1]] = hsum[1];
-        }
-    }
-}
-
-// ------------------------------------------------------------------ a7: fill, warp per group, row by row
-// The default fill (round 2, second version). Warp per group; the rows of the group's queries are
-// written one after the other, and the expansion of a row's mask words into its candidate list is
-// done by the whole warp, right before the row is written:
-//  expansion (lane = mask word of the row): popcount, warp scan of the counts -> each lane appends
-//    the bit positions of its own word at its offset of the row's list (ascending = ascending
-//    column). Lists are double-buffered per warp ([2][S] uint16), so the list of row i + 1 is built
-//    while the candidate points of row i are in flight;
-//  emission (lane = entry): ROUNDS 32-entry rounds in flight: sorted position from the group's
-//    union list, the whole point in one 256-bit load, the oracle's d^2 and weight, coalesced
-//    int32 / fp64 stores, Hs by a fixed-order lane reduction.
-// Against k_cl_fill this keeps no transposed mask copy and no per-query lists in shared memory
-// (10.5 KB -> < 0.5 KB per warp at config 5) and has no serial per-lane walk at the start of a group;
-// the occupancy limit becomes the register count (launch bounds: kFill2MinBlocks blocks of 4 warps).
-#ifndef TF_CL_FILL2_MINB
-#define TF_CL_FILL2_MINB 8
-#endif
-constexpr int kFill2Warps = 4;
-constexpr int kFill2MinBlocks = TF_CL_FILL2_MINB;
-
-// list of query i of the group: expand the set bits of its mask words (mk[32 * k + i], k < nw) into
-// dst[0..n) (candidate indices, ascending); returns n (uniform). Entries beyond cap are dropped.
-__device__ __forceinline__ int expand_row(const uint32_t *__restrict__ mk, int i, int nw, uint16_t *dst, int cap,
-                                          int lane) {
-    int done = 0;
-    for (int k0 = 0; k0 < nw; k0 += 32) {
-        const int k = k0 + lane;
-        uint32_t w = (k < nw) ? mk[32 * k + i] : 0u;
-        const int c = __popc(w);
-        int inc = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += v;
-        }
-        int e = done + inc - c;
-        const int t0 = 32 * k;
-        while (w) {
-            const int b = __clz(w);
-            if (e < cap) dst[e] = (uint16_t)(t0 + b);
-            ++e;
-            w ^= 0x80000000u >> b;
-        }
-        done += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    return done;
-}
-
-template <int DIM, int ROUNDS>
-__global__ void __launch_bounds__(kFill2Warps * 32, kFill2MinBlocks)
-    k_cl_fill2(SortedPtsView P, Grid g, const GroupRec *__restrict__ rec, const int64_t *__restrict__ loff, int32_t G,
-               int S, const int32_t *__restrict__ list, const uint32_t *__restrict__ mask,
-               const int64_t *__restrict__ rowptr, int32_t *__restrict__ cols, double *__restrict__ vals,
-               double *__restrict__ hs, int32_t *__restrict__ stats) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int32_t gi = (int32_t)blockIdx.x * kFill2Warps + warp;
-    if (gi >= G) return;
-    uint16_t *ent = reinterpret_cast<uint16_t *>(smem_raw) + (size_t)warp * 2 * S;  // [2][S]
-    const GroupRec R = rec[gi];
-    const int nq = R.q1 - R.q0;
-    const int L = R.L, nw = (L + 31) >> 5;
-    const int64_t base = loff[gi];
-    const uint32_t *mk = mask + base;
-    const int32_t *ul = list + base;
-    const int q = R.q0 + lane;
-    const bool have = lane < nq;
-    int32_t qid = 0;
-    int64_t rbase = 0;
-    int len = 0;
-    double qxl = 0.0, qyl = 0.0, qzl = 0.0;
-    if (have) {
-        const PtRec c = load_pt(P.a, q);
-        qid = c.id;
-        qxl = c.x, qyl = c.y, qzl = c.z;
-        rbase = rowptr[qid];
-        len = (int)(rowptr[qid + 1] - rbase);
-    }
-    const double rmin = g.rmin;
-#ifdef TF_DEBUG_CHECKS
-    const double r2 = g.r2;
-#endif
-    int bad = 0;
-    int n_next = expand_row(mk, 0, nw, ent, S, lane);
-    __syncwarp();
-    for (int i = 0; i < nq; ++i) {
-        const uint16_t *my = ent + (size_t)(i & 1) * S;
-        const int li = __shfl_sync(0xffffffffu, len, i);
-        const int64_t bi = __shfl_sync(0xffffffffu, rbase, i);
-        const int32_t qi = __shfl_sync(0xffffffffu, qid, i);
-        const double qx = __shfl_sync(0xffffffffu, qxl, i), qy = __shfl_sync(0xffffffffu, qyl, i);
-        const double qz = (DIM == 3) ? __shfl_sync(0xffffffffu, qzl, i) : 0.0;
-        bad |= (n_next != li);  // count/fill agreement (always-on invariant)
-        const bool longrow = li > S;
-        const int lr = longrow ? 0 : li;
-        // candidate points of the first ROUNDS rounds: loads first
-        PtRec c[ROUNDS];
-#pragma unroll
-        for (int r = 0; r < ROUNDS; ++r) {
-            const int e = 32 * r + lane;
-            const int p = ul[(e < lr) ? my[e] : 0];
-            c[r] = load_pt(P.a, p);
-        }
-        // the next row's list, while those are in flight
-        if (i + 1 < nq) n_next = expand_row(mk, i + 1, nw, ent + (size_t)((i + 1) & 1) * S, S, lane);
-        double hsum = 0.0;
-#pragma unroll
-        for (int r = 0; r < ROUNDS; ++r) {
-            const int e = 32 * r + lane;
-            if (e < lr) {
-                const double d2 = pair_d2<DIM>(qx, qy, qz, c[r].x, c[r].y, c[r].z);
-                const double w = weight_of(rmin, d2);
-                cols[bi + e] = c[r].id;
-                vals[bi + e] = w;
-                hsum += w;
-                TF_DCHECK(d2 < r2);
-            }
-        }
-        for (int e = 32 * ROUNDS + lane; e < lr; e += 32) {
-            const PtRec cc = load_pt(P.a, ul[my[e]]);
-            const double d2 = pair_d2<DIM>(qx, qy, qz, cc.x, cc.y, cc.z);
-            const double w = weight_of(rmin, d2);
-            cols[bi + e] = cc.id;
-            vals[bi + e] = w;
-            hsum += w;
-            TF_DCHECK(d2 < r2);
-        }
-        if (longrow) {
-            // rows longer than the list (dense clusters): lane = mask word, each lane emits its bits
-            int done = 0;
-            for (int k0 = 0; k0 < nw; k0 += 32) {
-                const int k = k0 + lane;
-                uint32_t w = (k < nw) ? mk[32 * k + i] : 0u;
-                const int cnt = __popc(w);
-                int inc = cnt;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += v;
-                }
-                int e = done + inc - cnt;
-                while (w) {
-                    const int b = __clz(w);
-                    const PtRec cc = load_pt(P.a, ul[32 * k + b]);
-                    const double d2 = pair_d2<DIM>(qx, qy, qz, cc.x, cc.y, cc.z);
-                    const double wt = weight_of(rmin, d2);
-                    cols[bi + e] = cc.id;
-                    vals[bi + e] = wt;
-                    hsum += wt;
-                    TF_DCHECK(d2 < r2);
-                    ++e;
-                    w ^= 0x80000000u >> b;
-                }
-                done += __shfl_sync(0xffffffffu, inc, 31);
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
-        if (lane == 0) hs[qi] = hsum;
-        __syncwarp();
-    }
-    if (bad) atomicOr(&stats[2], 1);
-}
-
-template <int DIM, int ROUNDS>
-tf_status launch_cl_fill2(const SortedPtsView &P, const Grid &g, const GroupRec *rec, const int64_t *loff, int32_t G,
-                          int S, const int32_t *list, const uint32_t *mask, tf_filter_s *h, int32_t *stats,
-                          cudaStream_t s) {
-    const size_t smem = (size_t)kFill2Warps * 2 * S * sizeof(uint16_t);
-    auto kern = k_cl_fill2<DIM, ROUNDS>;
-    kern<<<(unsigned)(((int64_t)G + kFill2Warps - 1) / kFill2Warps), kFill2Warps * 32, smem, s>>>(
-        P, g, rec, loff, G, S, list, mask, h->rowptr, h->cols, h->vals, h->hs, stats);
-    TF_LAUNCH_CHECK();
-    return TF_OK;
-}
-
 // ------------------------------------------------------------------ a7: fill, warp per group, masks from L1
 // k_cl_fill with two changes for occupancy (the fill is latency-bound at 5 blocks of 4 warps per SM):
 // the walk reads each lane's mask words straight from global memory (word k of query q at [k][q]:
@@ -858,7 +499,7 @@ tf_status launch_cl_fill2(const SortedPtsView &P, const Grid &g, const GroupRec 
 template <int DIM, int ROUNDS>
 __global__ void __launch_bounds__(128, TF_CL_FILL3_MINB)
     k_cl_fill3(SortedPtsView P, Grid g, const GroupRec *__restrict__ rec, const int64_t *__restrict__ loff, int32_t G,
-               int S, const int32_t *__restrict__ list, const uint32_t *__restrict__ mask,
+               int S, const uint16_t *__restrict__ list, const uint32_t *__restrict__ mask,
                const int64_t *__restrict__ rowptr, int32_t *__restrict__ cols, double *__restrict__ vals,
                double *__restrict__ hs, int32_t *__restrict__ stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -876,7 +517,17 @@ __global__ void __launch_bounds__(128, TF_CL_FILL3_MINB)
     const int64_t base = loff[gi];
     constexpr int WS = kGroupQ;  // words of one query are WS apart
     const uint32_t *mk = mask + kHalves * base + 32 * half + lane;  // word k of this lane's query at mk[WS * k]
-    const int32_t *ul = list + base;
+    const uint16_t *ul = list + base;
+    // run starts of the union (code -> sorted position)
+    __shared__ int32_t s_run[4][16];
+    int32_t *srun = s_run[warp];
+    {
+        constexpr int NR = (DIM == 3) ? 9 : 3;
+        int rs = 0, rl = 0;
+        if (lane < NR) group_run<DIM>(lane, R, g, P.cs, rs, rl);
+        if (lane < 16) srun[lane] = rs;
+    }
+    auto pos_of = [&](uint32_t cd) { return srun[cd >> kRunShift] + (int)(cd & (kMaxRun - 1)); };
     const bool have = lane < nq;
     int32_t qid = 0;
     int64_t rbase = 0;
@@ -935,7 +586,7 @@ __global__ void __launch_bounds__(128, TF_CL_FILL3_MINB)
 #pragma unroll
         for (int r = 0; r < ROUNDS; ++r) {
             const int e = 32 * r + lane;
-            c[r] = load_pt(P.a, ul[(e < lr) ? my[e] : 0]);
+            c[r] = load_pt(P.a, pos_of(ul[(e < lr) ? my[e] : 0]));
         }
         double hsum = 0.0;
 #pragma unroll
@@ -951,7 +602,7 @@ __global__ void __launch_bounds__(128, TF_CL_FILL3_MINB)
             }
         }
         for (int e = 32 * ROUNDS + lane; e < lr; e += 32) {
-            const PtRec cc = load_pt(P.a, ul[my[e]]);
+            const PtRec cc = load_pt(P.a, pos_of(ul[my[e]]));
             const double d2 = pair_d2<DIM>(qx, qy, qz, cc.x, cc.y, cc.z);
             const double w = weight_of(rmin, d2);
             cols[bi + e] = cc.id;
@@ -975,7 +626,7 @@ __global__ void __launch_bounds__(128, TF_CL_FILL3_MINB)
                 int e = done + inc - cnt;
                 while (w) {
                     const int b = __clz(w);
-                    const PtRec cc = load_pt(P.a, ul[32 * k + b]);
+                    const PtRec cc = load_pt(P.a, pos_of(ul[32 * k + b]));
                     const double d2 = pair_d2<DIM>(qx, qy, qz, cc.x, cc.y, cc.z);
                     const double wt = weight_of(rmin, d2);
                     cols[bi + e] = cc.id;
@@ -996,7 +647,7 @@ __global__ void __launch_bounds__(128, TF_CL_FILL3_MINB)
 
 template <int DIM, int ROUNDS>
 tf_status launch_cl_fill3(const SortedPtsView &P, const Grid &g, const GroupRec *rec, const int64_t *loff, int32_t G,
-                          int S, const int32_t *list, const uint32_t *mask, tf_filter_s *h, int32_t *stats,
+                          int S, const uint16_t *list, const uint32_t *mask, tf_filter_s *h, int32_t *stats,
                           cudaStream_t s) {
     const size_t smem = (size_t)4 * 32 * S * sizeof(uint16_t);
     auto kern = k_cl_fill3<DIM, ROUNDS>;
@@ -1018,7 +669,7 @@ tf_status launch_cl_fill3(const SortedPtsView &P, const Grid &g, const GroupRec 
 template <int DIM, int ROUNDS>
 __global__ void __launch_bounds__(128) k_cl_fill4(SortedPtsView P, Grid g, const GroupRec *__restrict__ rec,
                                                   const int64_t *__restrict__ loff, int LPmax, int S,
-                                                  const int32_t *__restrict__ list, const uint32_t *__restrict__ mask,
+                                                  const uint16_t *__restrict__ list, const uint32_t *__restrict__ mask,
                                                   const int64_t *__restrict__ rowptr, int32_t *__restrict__ cols,
                                                   double *__restrict__ vals, double *__restrict__ hs,
                                                   int32_t *__restrict__ stats) {
@@ -1034,7 +685,18 @@ __global__ void __launch_bounds__(128) k_cl_fill4(SortedPtsView P, Grid g, const
     const int L = R.L, nw = (L + 31) >> 5;
     const int64_t base = loff[blockIdx.x];
     const uint32_t *mk = mask + base + lane;  // word k of this lane's query at mk[32 * k]
-    const int32_t *ul = list + base;
+    const uint16_t *ul = list + base;
+    // run starts of the union (code -> sorted position), one copy per warp (no block barrier)
+    __shared__ int32_t s_run[4][16];
+    int32_t *srun = s_run[warp];
+    {
+        constexpr int NR = (DIM == 3) ? 9 : 3;
+        int rs = 0, rl = 0;
+        if (lane < NR) group_run<DIM>(lane, R, g, P.cs, rs, rl);
+        if (lane < 16) srun[lane] = rs;
+        __syncwarp();
+    }
+    auto pos_of = [&](uint32_t cd) { return srun[cd >> kRunShift] + (int)(cd & (kMaxRun - 1)); };
     const bool have = lane < nq;
     int32_t qid = 0;
     int64_t rbase = 0;
@@ -1053,7 +715,7 @@ __global__ void __launch_bounds__(128) k_cl_fill4(SortedPtsView P, Grid g, const
 #pragma unroll
     for (int u = 0; u < SU; ++u) {
         const int t = u * 128 + tid;
-        sp[u] = load_pt(P.a, ul[t < L ? t : 0]);
+        sp[u] = load_pt(P.a, pos_of(ul[t < L ? t : 0]));
     }
     {
         // (1) this warp's quarter of the words
@@ -1102,7 +764,7 @@ __global__ void __launch_bounds__(128) k_cl_fill4(SortedPtsView P, Grid g, const
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int t = t0 + u * 128 + tid;
-            c[u] = load_pt(P.a, ul[t < L ? t : 0]);
+            c[u] = load_pt(P.a, pos_of(ul[t < L ? t : 0]));
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1199,7 +861,7 @@ __global__ void __launch_bounds__(128) k_cl_fill4(SortedPtsView P, Grid g, const
 
 template <int DIM, int ROUNDS>
 tf_status launch_cl_fill4(const SortedPtsView &P, const Grid &g, const GroupRec *rec, const int64_t *loff, int32_t G,
-                          int LPmax, int S, const int32_t *list, const uint32_t *mask, tf_filter_s *h, int32_t *stats,
+                          int LPmax, int S, const uint16_t *list, const uint32_t *mask, tf_filter_s *h, int32_t *stats,
                           cudaStream_t s) {
     const size_t smem = (size_t)LPmax * ((DIM == 3 ? 24 : 16) + 4) + (size_t)32 * S * sizeof(uint16_t);
     auto kern = k_cl_fill4<DIM, ROUNDS>;
@@ -1210,266 +872,15 @@ tf_status launch_cl_fill4(const SortedPtsView &P, const Grid &g, const GroupRec 
     return TF_OK;
 }
 
-// ------------------------------------------------------------------ a7: fill, block per group
-// One block of kFillBWarps warps per group (kGroupQ = 32 queries). The group's sorted union is
-// staged in shared memory once -- exact fp64 coordinates and ids --, so every entry's candidate
-// data is a shared-memory load instead of a global gather (the warp-per-group fill was bound by
-// the L1 wavefronts of those gathers). Warp 0 expands the lanes' mask words into candidate lists
-// (lane = query, as k_cl_fill) while the other warps stage the union; then warp w writes the rows
-// of queries w, w + kFillBWarps, ... (lane = entry; two rows per pass, kFillRounds rounds each in
-// flight): the oracle's d^2 and weight, coalesced int32 / fp64 stores, Hs by a fixed-order lane
-// reduction. Shared memory: union x, y, z [LPmax] fp64 + ids [LPmax] int32 + masks [32][MS] + lists
-// [32][S] uint16.
-constexpr int kFillBWarps = 4;
-
-template <int DIM>
-__global__ void __launch_bounds__(kFillBWarps * 32) k_cl_fill_b(SortedPtsView P, Grid g,
-                                                                const GroupRec *__restrict__ rec,
-                                                                const int64_t *__restrict__ loff, int LPmax, int MS,
-                                                                int S, const int32_t *__restrict__ list,
-                                                                const uint32_t *__restrict__ mask,
-                                                                const int64_t *__restrict__ rowptr,
-                                                                int32_t *__restrict__ cols, double *__restrict__ vals,
-                                                                double *__restrict__ hs, int32_t *__restrict__ stats) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int T = kFillBWarps * 32;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double *ux = reinterpret_cast<double *>(smem_raw);
-    double *uy = ux + LPmax;
-    double *uz = uy + LPmax;
-    int32_t *uid = reinterpret_cast<int32_t *>(uz + ((DIM == 3) ? LPmax : 0));
-    uint32_t *sm = reinterpret_cast<uint32_t *>(uid + LPmax);  // [32][MS]
-    uint16_t *ent = reinterpret_cast<uint16_t *>(sm + 32 * MS);  // [32][S]
-    __shared__ int32_t s_len[32];
-    __shared__ int64_t s_base[32];
-    __shared__ int32_t s_qid[32];
-    const GroupRec R = rec[blockIdx.x];
-    const int L = R.L, LP = (L + 31) & ~31, nw = LP >> 5;
-    const int64_t base = loff[blockIdx.x];
-    const int nq = R.q1 - R.q0;
-    if (warp == 0) {
-        // masks of the group, transposed to [lane][word] (odd stride MS > nw, the padding zero)
-        for (int k0 = 0; k0 < MS; k0 += 4) {
-            uint32_t m[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) m[u] = (k0 + u < nw) ? mask[base + 32 * (k0 + u) + lane] : 0u;
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (k0 + u < MS) sm[lane * MS + k0 + u] = m[u];
-        }
-        const int q = R.q0 + lane;
-        const bool have = lane < nq;
-        int32_t qid = 0;
-        int64_t rbase = 0;
-        int len = 0;
-        if (have) {
-            qid = P.id[q];
-            rbase = rowptr[qid];
-            len = (int)(rowptr[qid + 1] - rbase);
-        }
-        s_len[lane] = len;
-        s_base[lane] = rbase;
-        s_qid[lane] = qid;
-        __syncwarp();
-        // branch-free walk of the lane's words (two set bits or one word step per iteration)
-        const uint32_t *mw = sm + lane * MS;
-        uint16_t *my = ent + (size_t)lane * S;
-        int n = 0, k = 0;
-        uint32_t w = mw[0];
-        const int kend = have ? nw : 0;
-        while (__any_sync(0xffffffffu, k < kend)) {
-#pragma unroll 2
-            for (int u = 0; u < 2; ++u) {
-                const bool z = (w == 0);
-                const int b1 = __clz(w) & 31;
-                const uint32_t w1 = w ^ (0x80000000u >> b1);
-                const int b2 = __clz(w1) & 31;
-                const bool two = !z && (w1 != 0);
-                my[min(n, S - 1)] = (uint16_t)(32 * k + b1);
-                my[min(n + 1, S - 1)] = (uint16_t)(32 * k + b2);
-                n += z ? 0 : (two ? 2 : 1);
-                const uint32_t wn = mw[min(k + 1, MS - 1)];
-                w = z ? wn : (two ? (w1 ^ (0x80000000u >> b2)) : 0u);
-                k = z ? min(k + 1, nw) : k;
-            }
-        }
-        if (have && n != len) atomicOr(&stats[2], 1);  // count/fill agreement (always-on invariant)
-    } else {
-        // the union's exact coordinates and ids, staged once for the whole group
-        for (int t0 = (warp - 1) * 32; t0 < L; t0 += 4 * (T - 32)) {
-            int p[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = t0 + u * (T - 32) + lane;
-                p[u] = (t < L) ? list[base + t] : -1;
-            }
-            double xv[4], yv[4], zv[4];
-            int32_t iv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int pp = p[u] < 0 ? 0 : p[u];
-                xv[u] = P.x[pp];
-                yv[u] = P.y[pp];
-                zv[u] = (DIM == 3) ? P.z[pp] : 0.0;
-                iv[u] = P.id[pp];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = t0 + u * (T - 32) + lane;
-                if (t < L) {
-                    ux[t] = xv[u];
-                    uy[t] = yv[u];
-                    if (DIM == 3) uz[t] = zv[u];
-                    uid[t] = iv[u];
-                }
-            }
-        }
-    }
-    __syncthreads();
-    const double rmin = g.rmin;
-#ifdef TF_DEBUG_CHECKS
-    const double r2 = g.r2;
-#endif
-    for (int i0 = 2 * warp; i0 < nq; i0 += 2 * kFillBWarps) {
-        int li[2];
-        bool longrow[2];
-        int32_t qi[2];
-        int64_t bi[2];
-        double qx[2], qy[2], qz[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int i = min(i0 + h, nq - 1);
-            li[h] = (i0 + h < nq) ? s_len[i] : 0;
-            longrow[h] = li[h] > S - 2;
-            if (longrow[h]) li[h] = 0;
-            bi[h] = s_base[i];
-            qi[h] = s_qid[i];
-            qx[h] = P.x[R.q0 + i];
-            qy[h] = P.y[R.q0 + i];
-            qz[h] = (DIM == 3) ? P.z[R.q0 + i] : 0.0;
-        }
-        double cx[2][kFillRounds], cy[2][kFillRounds], cz[2][kFillRounds];
-        int32_t cid[2][kFillRounds];
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int r = 0; r < kFillRounds; ++r) {
-                const int e = 32 * r + lane;
-                const int t = (e < li[h]) ? ent[(size_t)(i0 + h) * S + e] : 0;
-                cx[h][r] = ux[t];
-                cy[h][r] = uy[t];
-                cz[h][r] = (DIM == 3) ? uz[t] : 0.0;
-                cid[h][r] = uid[t];
-            }
-        double hsum[2] = {0.0, 0.0};
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int r = 0; r < kFillRounds; ++r) {
-                const int e = 32 * r + lane;
-                if (e < li[h]) {
-                    const double d2 = pair_d2<DIM>(qx[h], qy[h], qz[h], cx[h][r], cy[h][r], cz[h][r]);
-                    const double w = weight_of(rmin, d2);
-                    cols[bi[h] + e] = cid[h][r];
-                    vals[bi[h] + e] = w;
-                    hsum[h] += w;
-                    TF_DCHECK(d2 < r2);
-                }
-            }
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-            for (int e = 32 * kFillRounds + lane; e < li[h]; e += 32) {
-                const int t = ent[(size_t)(i0 + h) * S + e];
-                const double d2 = pair_d2<DIM>(qx[h], qy[h], qz[h], ux[t], uy[t], (DIM == 3) ? uz[t] : 0.0);
-                const double w = weight_of(rmin, d2);
-                cols[bi[h] + e] = uid[t];
-                vals[bi[h] + e] = w;
-                hsum[h] += w;
-                TF_DCHECK(d2 < r2);
-            }
-        // rows longer than the lists: lane = mask word of the row (word-parallel path)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            if (!longrow[h]) continue;
-            const int i = i0 + h;
-            int done = 0;
-            for (int k0 = 0; k0 < nw; k0 += 32) {
-                const int k = k0 + lane;
-                uint32_t w = (k < nw) ? sm[i * MS + k] : 0u;
-                const int c = __popc(w);
-                int inc = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += v;
-                }
-                int e = done + inc - c;
-                while (w) {
-                    const int b = __clz(w);
-                    const int t = 32 * k + b;
-                    const double d2 = pair_d2<DIM>(qx[h], qy[h], qz[h], ux[t], uy[t], (DIM == 3) ? uz[t] : 0.0);
-                    const double wt = weight_of(rmin, d2);
-                    cols[bi[h] + e] = uid[t];
-                    vals[bi[h] + e] = wt;
-                    hsum[h] += wt;
-                    ++e;
-                    w ^= 0x80000000u >> b;
-                }
-                done += __shfl_sync(0xffffffffu, inc, 31);
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            hsum[0] += __shfl_xor_sync(0xffffffffu, hsum[0], o);
-            hsum[1] += __shfl_xor_sync(0xffffffffu, hsum[1], o);
-        }
-        if (lane == 0) {
-            hs[qi[0]] = hsum[0];
-            if (i0 + 1 < nq) hs[qi[1]] = hsum[1];
-        }
-    }
-}
-
-template <int DIM>
-tf_status launch_cl_fill_b(const SortedPtsView &P, const Grid &g, const GroupRec *rec, const int64_t *loff, int32_t G,
-                           int LPmax, int MS, int S, const int32_t *list, const uint32_t *mask, tf_filter_s *h,
-                           int32_t *stats, cudaStream_t s) {
-    const size_t smem = (size_t)LPmax * ((DIM == 3 ? 24 : 16) + 4) + (size_t)32 * MS * 4 + (size_t)32 * S * 2;
-    auto kern = k_cl_fill_b<DIM>;
-    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)G, kFillBWarps * 32, smem, s>>>(P, g, rec, loff, LPmax, MS, S, list, mask, h->rowptr, h->cols,
-                                                     h->vals, h->hs, stats);
-    TF_LAUNCH_CHECK();
-    return TF_OK;
-}
-
 template <int DIM>
 tf_status launch_cl_count(const SortedPtsView &P, const Grid &g, const GroupRec *rec, const int64_t *loff, int32_t G,
-                          int LPmax, int32_t *list, uint32_t *mask, int32_t *counts, int32_t *stats, cudaStream_t s) {
+                          int LPmax, uint16_t *list, uint32_t *mask, int32_t *counts, int32_t *stats, cudaStream_t s) {
     const size_t smem = (size_t)5 * LPmax * sizeof(uint32_t);
     auto kern = k_cl_count<DIM>;
     TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<(unsigned)G, kCountWarps * 32, smem, s>>>(P, g, rec, loff, LPmax, list, mask, counts, stats);
     TF_LAUNCH_CHECK();
     return TF_OK;
-}
-
-template <int DIM, int WARPS>
-tf_status launch_cl_fill(const SortedPtsView &P, const Grid &g, const GroupRec *rec, const int64_t *loff, int32_t G,
-                         int MS, int S, const int32_t *list, const uint32_t *mask, tf_filter_s *h, int32_t *stats,
-                         cudaStream_t s) {
-    const size_t smem = (size_t)WARPS * ((size_t)32 * MS * 4 + (size_t)32 * S * 2);
-    auto kern = k_cl_fill<DIM, WARPS>;
-    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)(((int64_t)G * kHalves + WARPS - 1) / WARPS), WARPS * 32, smem, s>>>(P, g, rec, loff, G, MS, S, list, mask,
-                                                                     h->rowptr, h->cols, h->vals, h->hs, stats);
-    TF_LAUNCH_CHECK();
-    return TF_OK;
-}
-
-int env_int(const char *name, int dflt) {
-    const char *e = getenv(name);
-    return (e && *e) ? atoi(e) : dflt;
 }
 
 }  // namespace
@@ -1508,19 +919,21 @@ tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_
     else k_cl_groups<2><<<gridU, threads, 0, s>>>(P.cs, sorted_keys, g, nxb, U, goff.p, rec.p, lp.p, stats.p);
     TF_LAUNCH_CHECK();
     TF_TRY(exclusive_scan_i32_i64(lp.p, loff.p, Gmax, s));
-    int32_t hG = 0, hmax = 0;
+    int32_t hG = 0, hmax = 0, hrun = 0;
     int64_t hTot = 0;
     TF_CUDA_TRY(cudaMemcpyAsync(&hG, goff.p + U, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     TF_CUDA_TRY(cudaMemcpyAsync(&hmax, stats.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    TF_CUDA_TRY(cudaMemcpyAsync(&hrun, stats.p + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     TF_CUDA_TRY(cudaMemcpyAsync(&hTot, loff.p + Gmax, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     TF_CUDA_TRY(cudaStreamSynchronize(s));
     build_trace().mark("groups+sync", s);
     h->info.max_candidates = hmax;
-    if (hmax > kMaxUnion || hG <= 0) return TF_OK;  // per-bin kernels take it
+    if (hmax > kMaxUnion || hrun >= kMaxRun || hG <= 0) return TF_OK;  // per-bin kernels take it
     const int LPmax = (hmax + 31) & ~31;
 
     // a5 count: sorted unions + mask words + row lengths
-    DevBuf<int32_t> list, counts;
+    DevBuf<uint16_t> list;
+    DevBuf<int32_t> counts;
     DevBuf<uint32_t> mask;
     TF_TRY(list.alloc(hTot, s, "group unions"));
     TF_TRY(mask.alloc((size_t)kHalves * hTot, s, "group masks"));
@@ -1551,21 +964,18 @@ tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_
     TF_TRY(dalloc(&h->hs, n, s, "Hs"));
     build_trace().mark("alloc_csr", s);
     // per-lane list stride S >= longest row (capped: longer rows take the word-parallel path),
-    // S = 2 mod 4 uint16 so lanes at equal list positions hit different banks; mask stride MS odd
+    // S = 2 mod 4 uint16 so lanes at equal list positions hit different banks
     int S = std::max(2, (std::min(maxrow, kListCap) + 3) & ~1);  // +2 slots for the walk's idle writes
     if ((S & 3) == 0) S += 2;
-    const int MS = (LPmax / 32 + 1) | 1;
-    const size_t per_warp = (size_t)32 * MS * 4 + (size_t)32 * S * 2;
-    // the block-per-group fill (union staged in shared memory) measured 8.90 vs 8.60 ms at config 5
-    // and 0.42 vs 0.47 ms at config 4: opt-in (TOPOFILT_CL_FILL=block, benchmarks and tests)
+    const int rounds = std::min(3, (std::min(maxrow, 96) + 31) / 32);  // 32-entry rounds in flight per row
+    // k_cl_fill4 (block per group, union staged in shared memory) measured faster only for small
+    // unions (config 4: 366 vs 402 us; config 5: 8.9 vs 6.65 ms), so it takes the builds whose blocks
+    // need <= 12 KB (2D neighbourhoods); k_cl_fill3 (warp per group) takes the rest.
+    // TOPOFILT_CL_FILL=split / walk3 force either kernel (tests, benchmarks).
     const char *fk = getenv("TOPOFILT_CL_FILL");
     const size_t smem4 = (size_t)LPmax * ((dim == 3 ? 24 : 16) + 4) + (size_t)32 * S * 2;
-    // block-per-group fill with the union staged in shared memory: measured faster only for small
-    // unions (config 4: 366 vs 402 us; config 5: 8.9 vs 6.65 ms), so it takes the builds whose blocks
-    // need <= 12 KB (2D neighbourhoods); TOPOFILT_CL_FILL=split / walk3 force either kernel
-    const bool want4 = fk ? !strcmp(fk, "split") : (smem4 <= 12 * 1024);
+    const bool want4 = (fk && *fk) ? !strcmp(fk, "split") : (smem4 <= 12 * 1024);
     if (kGroupQ == 32 && want4 && smem4 <= di.smem_optin) {
-        const int rounds = std::min(3, (std::min(maxrow, 96) + 31) / 32);
 #define TF_FILL4(D, R) TF_TRY((launch_cl_fill4<D, R>(P, g, rec.p, loff.p, hG, LPmax, S, list.p, mask.p, h, stats.p, s)))
         if (dim == 3) {
             if (rounds >= 3) TF_FILL4(3, 3);
@@ -1577,9 +987,7 @@ tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_
             else TF_FILL4(2, 1);
         }
 #undef TF_FILL4
-    } else if (!(fk && (!strcmp(fk, "block") || !strcmp(fk, "walk") || !strcmp(fk, "rows")))) {
-        // default: the walk fill with the mask words read from L1 and one row at a time in flight
-        const int rounds = std::min(3, (std::min(maxrow, 96) + 31) / 32);
+    } else {
 #define TF_FILL3(D, R) TF_TRY((launch_cl_fill3<D, R>(P, g, rec.p, loff.p, hG, S, list.p, mask.p, h, stats.p, s)))
         if (dim == 3) {
             if (rounds >= 3) TF_FILL3(3, 3);
@@ -1591,40 +999,6 @@ tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_
             else TF_FILL3(2, 1);
         }
 #undef TF_FILL3
-    } else if (kGroupQ == 32 && fk && !strcmp(fk, "rows")) {
-        // default: row-by-row fill; list stride = longest row rounded up to 32 (capped), rounds in
-        // flight from the longest row
-        const int S2 = std::max(32, (std::min(maxrow, 1024) + 31) & ~31);
-        const int rounds = std::min(3, (std::min(maxrow, 96) + 31) / 32);
-#define TF_FILL2(D, R) TF_TRY((launch_cl_fill2<D, R>(P, g, rec.p, loff.p, hG, S2, list.p, mask.p, h, stats.p, s)))
-        if (dim == 3) {
-            if (rounds >= 3) TF_FILL2(3, 3);
-            else if (rounds == 2) TF_FILL2(3, 2);
-            else TF_FILL2(3, 1);
-        } else {
-            if (rounds >= 3) TF_FILL2(2, 3);
-            else if (rounds == 2) TF_FILL2(2, 2);
-            else TF_FILL2(2, 1);
-        }
-#undef TF_FILL2
-    } else {
-    const size_t smem_b = (size_t)LPmax * ((dim == 3 ? 24 : 16) + 4) + (size_t)32 * MS * 4 + (size_t)32 * S * 2;
-    if (kGroupQ == 32 && fk && !strcmp(fk, "block") && smem_b <= di.smem_optin) {
-        if (dim == 3) TF_TRY((launch_cl_fill_b<3>(P, g, rec.p, loff.p, hG, LPmax, MS, S, list.p, mask.p, h, stats.p, s)));
-        else TF_TRY((launch_cl_fill_b<2>(P, g, rec.p, loff.p, hG, LPmax, MS, S, list.p, mask.p, h, stats.p, s)));
-    } else {
-    int fw = env_int("TOPOFILT_CL_FILL_WARPS", 4);  // tuning knob (benchmarks only)
-    while (fw > 1 && (size_t)fw * per_warp > di.smem_optin) fw >>= 1;
-    if (dim == 3) {
-        if (fw >= 4) TF_TRY((launch_cl_fill<3, 4>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
-        else if (fw >= 2) TF_TRY((launch_cl_fill<3, 2>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
-        else TF_TRY((launch_cl_fill<3, 1>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
-    } else {
-        if (fw >= 4) TF_TRY((launch_cl_fill<2, 4>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
-        else if (fw >= 2) TF_TRY((launch_cl_fill<2, 2>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
-        else TF_TRY((launch_cl_fill<2, 1>(P, g, rec.p, loff.p, hG, MS, S, list.p, mask.p, h, stats.p, s)));
-    }
-    }
     }
     build_trace().mark("fill", s);
     int32_t flag = 0;

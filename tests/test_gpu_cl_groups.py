@@ -136,12 +136,13 @@ def test_paper_right_left_triangles(tf):
     check_paths_agree(tf, c, 2.0)
 
 
-@pytest.mark.parametrize("kernel", ["walk3", "split", "rows", "walk", "block"])
+@pytest.mark.parametrize("kernel", ["walk3", "split"])
 def test_fill_kernel_variants(tf, monkeypatch, kernel):
-    """Every fill kernel of the group path builds the oracle's CSR: k_cl_fill3 (walk3: the default for
-    3D-sized unions), k_cl_fill4 (split: the default for small unions), and the opt-in k_cl_fill2 (rows),
-    k_cl_fill (walk) and k_cl_fill_b (block) -- on a 2D ground structure, a jittered Kuhn mesh and a
-    dense cluster whose rows exceed the per-lane lists (word-parallel long-row path)."""
+    """Both fill kernels of the group path build the oracle's CSR whichever one the size rule would pick:
+    k_cl_fill3 (walk3: warp per group, the default for 3D-sized unions) and k_cl_fill4 (split: block per
+    group with the union staged in shared memory, the default for small unions) -- on a 2D ground
+    structure, a jittered Kuhn mesh and a dense cluster whose rows exceed the per-lane lists
+    (word-parallel long-row path)."""
     monkeypatch.setenv("TOPOFILT_CL_FILL", kernel)
     for c, rmin in ((synth.ground_structure(4, 400, 300)[0], 3.0), (synth.kuhn_mesh(10, 8, 6, jitter=0.1, stream=5)[0], 1.5),
                     (np.concatenate([np.random.default_rng(2).uniform(0, 1.0, size=(900, 3)),
