@@ -148,7 +148,10 @@ __global__ void __launch_bounds__(256) k_gather_sorted(const double *__restrict_
          p += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = ids[p];
         double v[3] = {0.0, 0.0, 0.0};
-        for (int d = 0; d < dim; ++d) sxyz[d * n + p] = v[d] = c[i * dim + d];
+        for (int d = 0; d < dim; ++d) {
+            v[d] = c[i * dim + d];
+            if (sxyz) sxyz[d * n + p] = v[d];
+        }
         // the group kernels gather whole points: (x, y, z, id) in one 32-byte sector
         if (aos) aos[p] = make_double4(v[0], v[1], v[2], __longlong_as_double((long long)i));
     }
@@ -979,19 +982,19 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     k_cellstart<<<(unsigned)std::min<int64_t>((n + threads) / threads, (int64_t)di.sms * 16), threads, 0, s>>>(
         ks, n, g.nbins, cs.p);
     TF_LAUNCH_CHECK();
+    // sorted copies of the centroids: the group kernels read whole points (AoS); the per-bin kernels
+    // read SoA, which is only written when they run (asked for, or as the fallback below)
     DevBuf<double> sxyz;
-    TF_TRY(sxyz.alloc((size_t)dim * n, s, "sorted centroids"));
     bool legacy = (flags == TF_BUILD_CELL_LIST_BINS);
     if (const char *e = getenv("TOPOFILT_CL")) legacy = legacy || !strcmp(e, "bins");  // benchmarks
     DevBuf<double4> aos;
-    if (!legacy) TF_TRY(aos.alloc(n, s, "sorted centroids (AoS)"));
-    k_gather_sorted<<<grid_n, threads, 0, s>>>(c, n, dim, vs, sxyz.p, aos.p);
+    if (legacy) TF_TRY(sxyz.alloc((size_t)dim * n, s, "sorted centroids"));
+    else TF_TRY(aos.alloc(n, s, "sorted centroids (AoS)"));
+    k_gather_sorted<<<grid_n, threads, 0, s>>>(c, n, dim, vs, legacy ? sxyz.p : nullptr, legacy ? nullptr : aos.p);
     TF_LAUNCH_CHECK();
     SortedPts P;
     P.a = aos.p;
-    P.x = sxyz.p;
-    P.y = sxyz.p + n;
-    P.z = (dim == 3) ? sxyz.p + 2 * n : sxyz.p + n;
+    P.x = P.y = P.z = nullptr;
     P.id = reinterpret_cast<const int32_t *>(vs);
     P.cs = cs.p;
     const uint32_t *ks_keys = ks;  // sorted bin keys (the warp fill decodes each query's bin)
@@ -1002,7 +1005,14 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
         bool done = false;
         TF_TRY(build_cell_list_groups(P, ks_keys, g, n, s, h, &done));
         if (done) return TF_OK;
+        // fallback (a union beyond the group kernels' capacity): the per-bin kernels need the SoA copy
+        TF_TRY(sxyz.alloc((size_t)dim * n, s, "sorted centroids"));
+        k_gather_sorted<<<grid_n, threads, 0, s>>>(c, n, dim, vs, sxyz.p, nullptr);
+        TF_LAUNCH_CHECK();
     }
+    P.x = sxyz.p;
+    P.y = sxyz.p + n;
+    P.z = (dim == 3) ? sxyz.p + 2 * n : sxyz.p + n;
 
     // largest neighbourhood -> shared-memory capacity of the count / fill passes
     DevBuf<int32_t> counts, stats;

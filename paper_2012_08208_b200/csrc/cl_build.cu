@@ -141,7 +141,7 @@ __device__ __forceinline__ void group_run(int r, const GroupRec &G, const Grid &
     len = cs[rb + xh + 1] - s;
 }
 
-// Thread per unit: the unit's group records and padded union sizes; stats[0] = max union,
+// Warp per unit, lane per group: the unit's group records and padded union sizes; stats[0] = max union,
 // stats[1] = longest union run.
 template <int DIM>
 __global__ void __launch_bounds__(256) k_cl_groups(const int32_t *__restrict__ cs, const uint32_t *__restrict__ keys,
@@ -150,12 +150,15 @@ __global__ void __launch_bounds__(256) k_cl_groups(const int32_t *__restrict__ c
                                                    int32_t *__restrict__ stats) {
     constexpr int NR = (DIM == 3) ? 9 : 3;
     int best = 0, longest = 0;
-    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < U; u += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t u = wid; u < U; u += nwarp) {
         int32_t s, e;
         unit_range(u, g, nxb, cs, s, e);
         const int32_t row = (int32_t)(u / nxb);
-        int32_t gi = goff[u];
-        for (int32_t q0 = s; q0 < e; q0 += kGroupQ, ++gi) {
+        // warp per unit, lane per group of the unit
+        for (int32_t q0 = s + lane * kGroupQ; q0 < e; q0 += 32 * kGroupQ) {
+            const int32_t gi = goff[u] + (q0 - s) / kGroupQ;
             GroupRec G;
             G.q0 = q0;
             G.q1 = min(q0 + kGroupQ, e);
@@ -915,8 +918,9 @@ tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_
     k_cl_units<<<gridU, threads, 0, s>>>(P.cs, g, nxb, U, ng.p);
     TF_LAUNCH_CHECK();
     TF_TRY(exclusive_scan_i32_i32(ng.p, goff.p, U + 1, s));
-    if (dim == 3) k_cl_groups<3><<<gridU, threads, 0, s>>>(P.cs, sorted_keys, g, nxb, U, goff.p, rec.p, lp.p, stats.p);
-    else k_cl_groups<2><<<gridU, threads, 0, s>>>(P.cs, sorted_keys, g, nxb, U, goff.p, rec.p, lp.p, stats.p);
+    const unsigned gridG = (unsigned)std::min<int64_t>((U * 32 + threads - 1) / threads, (int64_t)di.sms * 32);
+    if (dim == 3) k_cl_groups<3><<<gridG, threads, 0, s>>>(P.cs, sorted_keys, g, nxb, U, goff.p, rec.p, lp.p, stats.p);
+    else k_cl_groups<2><<<gridG, threads, 0, s>>>(P.cs, sorted_keys, g, nxb, U, goff.p, rec.p, lp.p, stats.p);
     TF_LAUNCH_CHECK();
     TF_TRY(exclusive_scan_i32_i64(lp.p, loff.p, Gmax, s));
     int32_t hG = 0, hmax = 0, hrun = 0;

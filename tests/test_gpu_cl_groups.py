@@ -1,4 +1,4 @@
-"""The group kernels of the cell-list build (cl_build.cu: k_cl_count / k_cl_fill)
+"""The group kernels of the cell-list build (cl_build.cu: k_cl_count / k_cl_fill3 / k_cl_fill4)
 against the oracle and against the per-bin kernels (TF_BUILD_CELL_LIST_BINS): the whole CSR
 bit-exact, Hs within 1e-12. Cases aimed at the group design's own edges: the fp32 band (pairs at
 and within a few ulps of rmin), rows longer than the fill's per-lane lists, unions beyond the group

@@ -18,7 +18,7 @@ CMD="python bench.py --steps 1 --warmup 0 --applies 2 --no-e2e --no-cpu-baseline
 # the step's lattice fill and two applies, then the cell-list count and fill (bench's build_cell_list leg)
 # (step: k_lat_fill_exact, 2 x (k_tpass, k_spmv<1>, k_spmv<0>); the path-stats build's k_lat_fill_exact; then the
 # cell-list leg's k_cl_count, k_cl_fill)
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_spmv|k_cl_fill|k_cl_count|k_lat_fill_exact|k_tpass" -c 11 -o gpurun_out/ev_prof $CMD > gpurun_out/ev_ncu_full.log 2>&1; echo ncu2=$?
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_spmv|k_cl_fill|k_cl_count|k_lat_fill_exact|k_tpass" -c 16 -o gpurun_out/ev_prof $CMD > gpurun_out/ev_ncu_full.log 2>&1; echo ncu2=$?
 # instructions per query of the cell-list build kernels: group kernels vs the per-bin kernels (config 5)
 timeout 900 ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_cl_count|k_cl_fill|k_count|k_fill" --csv --log-file gpurun_out/ev_build_inst_groups.csv python tools/cl_one.py 5 cell_list > /dev/null 2>&1; echo ncu3=$?
 timeout 900 ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_count|k_fill" --csv --log-file gpurun_out/ev_build_inst_bins.csv python tools/cl_one.py 5 cell_list_bins > /dev/null 2>&1; echo ncu4=$?
