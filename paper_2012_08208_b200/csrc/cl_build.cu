@@ -12,21 +12,28 @@
 //                contiguous x-runs [bx0-1, bx1+1] of the bin rows around it;
 //   k_cl_count   block per group: (1) stages the union, (2) sorts it by point id with the block
 //                radix sort (smem_sort.cuh), so the union is in ascending COLUMN order, (3) writes
-//                that sorted list (sorted-SoA positions) for the fill, (4) sweeps it: lane = query,
-//                every union candidate tested with packed fp32x2 math in EDM form (R4c), one sign
-//                bit per test funnel-shifted (SHF.L.W) into a per-query 32-bit mask word, band
-//                candidates caught by a running unsigned minimum (VIMNMX3) and decided by the
-//                exact fp64 test; (5) stores the words (coalesced, word k of query q at [k][q]) and
-//                the row length = popcount;
-//   k_cl_fill    warp per group: lane = query walks its mask words (branch-free, two bits per
-//                step) into a list of candidate indices, then lane = entry writes each row: exact
-//                fp64 coordinates, the oracle's d^2 and weight, coalesced int32 / fp64 stores, Hs by
-//                a fixed-order lane reduction. No pair is tested twice: the set bits ARE the
-//                accepted pairs.
+//                that sorted list for the fill as 16-bit run codes (run << 12 | offset in the run:
+//                sorted position = run start + offset), (4) sweeps it: lane = query, every union
+//                candidate tested with packed fp32x2 math in EDM form (R4c), one sign bit per test
+//                funnel-shifted (SHF.L.W) into a per-query 32-bit mask word, band candidates caught
+//                by a running unsigned minimum (VIMNMX3) and decided by the exact fp64 test; (5)
+//                stores the words (coalesced, word k of query q at [k][q]) and the row length =
+//                popcount;
+//   k_cl_fill3   warp per group (the default for 3D-sized unions): lane = query walks its mask
+//                words straight from L1 (branch-free, two bits per step, next word loaded a step
+//                ahead) into a list of candidate indices, then lane = entry writes the rows one at a
+//                time: the candidate's whole point (x, y, z, id) in ONE 256-bit load of the AoS copy
+//                of the sorted centroids, the oracle's d^2 and weight, coalesced int32 / fp64 stores,
+//                Hs by a fixed-order lane reduction. 64 registers, 5.8 KB of shared memory per warp:
+//                8 blocks of 4 warps per SM;
+//   k_cl_fill4   block per group (small unions, i.e. 2D): the walk is split over the four warps (a
+//                quarter of every query's words each), the union's exact coordinates are staged in
+//                shared memory once, warp w writes rows w, w + 4, ...
+// No pair is tested twice: the set bits ARE the accepted pairs.
 // The per-bin kernels of build.cu (k_count / k_fill) stay as TF_BUILD_CELL_LIST_BINS and as the
-// fallback for unions beyond kMaxUnion. Measured: both group kernels are bound
-// by L1 wavefronts -- the sweep's broadcast candidate loads and the sort in the count, the
-// per-entry coordinate gathers in the fill.
+// fallback for unions beyond kMaxUnion (or runs beyond kMaxRun). Measured: the
+// count is bound by shared-memory wavefronts (the sweep's broadcast candidate loads and the sort),
+// the fill by the L2 -> L1 sectors of its per-entry point gathers (one 32-byte sector per entry).
 //
 // Exactness (R2-R4, R4c): a bit is set only if the fp32 value proves d^2 < r^2 with
 // the derived error bound, or the exact fp64 test (pair_d2, uncontracted) says so; the fill's

@@ -25,7 +25,11 @@ def main():
         cd = torch.from_numpy(c).cuda()
         n, dim = c.shape
         for path in os.environ.get("BUILD_PATHS", "lattice,cell_list").split(","):
-            f = tf.tf_build_filter(cd, rmin, path=path)
+            try:
+                f = tf.tf_build_filter(cd, rmin, path=path)
+            except tf.TopofiltError as e:  # e.g. the lattice path asked for on a non-lattice cloud
+                print(json.dumps({"config": cfg, "path": path, "skipped": str(e)[:120]}), flush=True)
+                continue
             nnz, got = f.nnz, f.stats()["path"]
             f.close()
             ts = []

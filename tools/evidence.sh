@@ -19,6 +19,12 @@ CMD="python bench.py --steps 1 --warmup 0 --applies 2 --no-e2e --no-cpu-baseline
 # (step: k_lat_fill_exact, 2 x (k_tpass, k_spmv<1>, k_spmv<0>); the path-stats build's k_lat_fill_exact; then the
 # cell-list leg's k_cl_count, k_cl_fill)
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_spmv|k_cl_fill|k_cl_count|k_lat_fill_exact|k_tpass" -c 16 -o gpurun_out/ev_prof $CMD > gpurun_out/ev_ncu_full.log 2>&1; echo ncu2=$?
+# the report is too large to bring back (gpurun_out <= 64 MiB): export the pages here, drop the report
+ncu -i gpurun_out/ev_prof.ncu-rep --page raw --csv > gpurun_out/ev_prof_raw.csv 2>/dev/null
+for k in k_spmv k_cl_fill k_cl_count k_lat_fill_exact; do
+ncu -i gpurun_out/ev_prof.ncu-rep --page source --csv --print-source cuda,sass -k regex:$k -c 1 > gpurun_out/ev_src_$k.csv 2>/dev/null
+done
+rm -f gpurun_out/ev_prof.ncu-rep
 # instructions per query of the cell-list build kernels: group kernels vs the per-bin kernels (config 5)
 timeout 900 ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_cl_count|k_cl_fill|k_count|k_fill" --csv --log-file gpurun_out/ev_build_inst_groups.csv python tools/cl_one.py 5 cell_list > /dev/null 2>&1; echo ncu3=$?
 timeout 900 ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_count|k_fill" --csv --log-file gpurun_out/ev_build_inst_bins.csv python tools/cl_one.py 5 cell_list_bins > /dev/null 2>&1; echo ncu4=$?

@@ -75,14 +75,18 @@ def main(rnd):
         if os.path.exists(os.path.join(EV, a)):
             shutil.copy(os.path.join(EV, a), os.path.join(dst, b))
     rep = os.path.join(EV, "ev_prof.ncu-rep")
-    raw = "/tmp/ev_raw.csv"
-    ncu(["-i", rep, "--page", "raw", "--csv"], raw)
+    raw = os.path.join(EV, "ev_prof_raw.csv")  # exported on the GPU box (the report itself is too large to bring back)
+    if not os.path.exists(raw):
+        raw = "/tmp/ev_raw.csv"
+        ncu(["-i", rep, "--page", "raw", "--csv"], raw)
     with open(os.path.join(dst, "ncu_full_summary.txt"), "w") as f:
         subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), raw], stdout=f, check=True)
     write_survey_metrics(raw, os.path.join(dst, "survey_metrics.txt"))
     for k in ("k_spmv", "k_cl_fill", "k_cl_count", "k_lat_fill_exact"):
-        src = f"/tmp/src_{k}.csv"
-        ncu(["-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{k}", "-c", "1"], src)
+        src = os.path.join(EV, f"ev_src_{k}.csv")
+        if not os.path.exists(src):
+            src = f"/tmp/src_{k}.csv"
+            ncu(["-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{k}", "-c", "1"], src)
         with open(os.path.join(dst, f"{k}_source_hot.txt"), "w") as f:
             r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_source_hot.py"), src], stdout=f)
         if r.returncode != 0:
