@@ -503,18 +503,22 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_cl_count(SortedPtsView P, 
 // the group's words stay L1-resident; the next word is loaded one step ahead), so no transposed mask
 // copy in shared memory (10.5 -> 5.8 KB per warp at config 5); rows are written one at a time with
 // ROUNDS rounds in flight, which fits 64 registers (8 blocks per SM).
+#ifndef TF_CL_FILL3_WARPS
+#define TF_CL_FILL3_WARPS 4
+#endif
+constexpr int kFill3Warps = TF_CL_FILL3_WARPS;  // warps per block: consecutive groups, i.e. neighbours along x
 #ifndef TF_CL_FILL3_MINB
-#define TF_CL_FILL3_MINB 8
+#define TF_CL_FILL3_MINB (32 / TF_CL_FILL3_WARPS)
 #endif
 template <int DIM, int ROUNDS>
-__global__ void __launch_bounds__(128, TF_CL_FILL3_MINB)
+__global__ void __launch_bounds__(kFill3Warps * 32, TF_CL_FILL3_MINB)
     k_cl_fill3(SortedPtsView P, Grid g, const GroupRec *__restrict__ rec, const int64_t *__restrict__ loff, int32_t G,
                int S, const uint16_t *__restrict__ list, const uint32_t *__restrict__ mask,
                const int64_t *__restrict__ rowptr, int32_t *__restrict__ cols, double *__restrict__ vals,
                double *__restrict__ hs, int32_t *__restrict__ stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int32_t wi = (int32_t)blockIdx.x * 4 + warp;
+    const int32_t wi = (int32_t)blockIdx.x * kFill3Warps + warp;
     const int32_t gi = wi / kHalves, half = wi % kHalves;  // this warp's 32 queries of the group
     if (gi >= G) return;
     uint16_t *ent = reinterpret_cast<uint16_t *>(smem_raw) + (size_t)warp * 32 * S;  // [32][S]
@@ -529,7 +533,7 @@ __global__ void __launch_bounds__(128, TF_CL_FILL3_MINB)
     const uint32_t *mk = mask + kHalves * base + 32 * half + lane;  // word k of this lane's query at mk[WS * k]
     const uint16_t *ul = list + base;
     // run starts of the union (code -> sorted position)
-    __shared__ int32_t s_run[4][16];
+    __shared__ int32_t s_run[kFill3Warps][16];
     int32_t *srun = s_run[warp];
     {
         constexpr int NR = (DIM == 3) ? 9 : 3;
@@ -659,11 +663,11 @@ template <int DIM, int ROUNDS>
 tf_status launch_cl_fill3(const SortedPtsView &P, const Grid &g, const GroupRec *rec, const int64_t *loff, int32_t G,
                           int S, const uint16_t *list, const uint32_t *mask, tf_filter_s *h, int32_t *stats,
                           cudaStream_t s) {
-    const size_t smem = (size_t)4 * 32 * S * sizeof(uint16_t);
+    const size_t smem = (size_t)kFill3Warps * 32 * S * sizeof(uint16_t);
     auto kern = k_cl_fill3<DIM, ROUNDS>;
     TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)(((int64_t)G * kHalves + 3) / 4), 128, smem, s>>>(P, g, rec, loff, G, S, list, mask, h->rowptr,
-                                                                       h->cols, h->vals, h->hs, stats);
+    kern<<<(unsigned)(((int64_t)G * kHalves + kFill3Warps - 1) / kFill3Warps), kFill3Warps * 32, smem, s>>>(
+        P, g, rec, loff, G, S, list, mask, h->rowptr, h->cols, h->vals, h->hs, stats);
     TF_LAUNCH_CHECK();
     return TF_OK;
 }
