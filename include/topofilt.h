@@ -77,6 +77,8 @@ typedef struct {
 #define TF_PATH_LATTICE_EXACT 2  /* lattice-ordered centroids exactly on a dyadic grid: the pair
                                     test and weight of each table entry are position-independent
                                     and evaluated once on the host (R22) */
+#define TF_PATH_DENSE 3          /* ablation (TF_BUILD_DENSE): every pair (i, j) visited, the
+                                    paper's own all-pairs method */
 
 /* Build statistics (diagnostics; all host values). For lattice-path builds, bins = cubes per
  * axis, nbins = cubes, max_candidates = the largest per-type table, bin_side = 0. */
@@ -122,6 +124,11 @@ TF_API tf_status tf_build_filter(const double *centroids, int64_t n, int dim, do
  *   flags = TF_BUILD_CELL_LIST: always the cell list.
  *   flags = TF_BUILD_LATTICE: the lattice path or TF_ERR_INVALID (tests, benchmarks).
  *   flags = TF_BUILD_CELL_LIST_BINS: the cell list with its per-bin kernels (tests, benchmarks).
+ *   flags = TF_BUILD_DENSE: ABLATION, O(n^2): the paper's own all-pairs build (its Euclidean
+ *     distance matrix, PAPER.md:390-396 and listing PAPER.md:442-445) as tiled kernels that visit
+ *     every pair with the same exact pair expression; no cell list. Same CSR; Hs bitwise the
+ *     ascending-column sum. For measuring what the cell list buys (tools/dense_probe.py); refuses
+ *     n > 4,000,000 (TF_ERR_INVALID).
  * Other arguments and errors as tf_build_filter; TF_ERR_INVALID for unknown flags.
  */
 /*
@@ -141,6 +148,7 @@ TF_API tf_status tf_lattice_detect_host(const double *centroids_host, int64_t n,
 #define TF_BUILD_CELL_LIST_BINS 3 /* the cell list with the per-bin count/fill kernels (the
                                      round-1 kernels; also the fallback for neighbourhoods beyond
                                      the group kernels' shared memory) */
+#define TF_BUILD_DENSE 4          /* ablation: all-pairs build, O(n^2) (see above) */
 TF_API tf_status tf_build_filter_ex(const double *centroids, int64_t n, int dim, double rmin, int flags,
                                     void *stream, tf_filter *out);
 

@@ -39,8 +39,8 @@ EXPORTS = [
 
 
 # tf_build_filter_ex flags (TF_BUILD_*) and tf_build_info.path values (TF_PATH_*)
-BUILD_FLAGS = {"auto": 0, "cell_list": 1, "lattice": 2, "cell_list_bins": 3}
-BUILD_PATHS = {0: "cell_list", 1: "lattice_tested", 2: "lattice_exact"}
+BUILD_FLAGS = {"auto": 0, "cell_list": 1, "lattice": 2, "cell_list_bins": 3, "dense": 4}
+BUILD_PATHS = {0: "cell_list", 1: "lattice_tested", 2: "lattice_exact", 3: "dense"}
 
 
 class TopofiltError(RuntimeError):

@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtopofilt.so")
-SOURCES = ["api.cu", "build.cu", "cl_build.cu", "lattice_build.cu", "radix.cu", "scan.cu", "apply.cu", "stencil.cu", "oc.cu", "helmholtz.cu", "shard.cu"]
+SOURCES = ["api.cu", "build.cu", "cl_build.cu", "dense_build.cu", "lattice_build.cu", "radix.cu", "scan.cu", "apply.cu", "stencil.cu", "oc.cu", "helmholtz.cu", "shard.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

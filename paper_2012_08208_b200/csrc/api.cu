@@ -341,8 +341,12 @@ tf_status tf_build_filter_ex(const double *centroids, int64_t n, int dim, double
     try {
         TF_TRY(check_build_args(n, dim, rmin, out));
         if (flags != TF_BUILD_AUTO && flags != TF_BUILD_CELL_LIST && flags != TF_BUILD_LATTICE &&
-            flags != TF_BUILD_CELL_LIST_BINS) {
+            flags != TF_BUILD_CELL_LIST_BINS && flags != TF_BUILD_DENSE) {
             set_error("tf_build_filter_ex: unknown flags %d", flags);
+            return TF_ERR_INVALID;
+        }
+        if (flags == TF_BUILD_DENSE && n > 4000000) {
+            set_error("tf_build_filter_ex: TF_BUILD_DENSE is an O(n^2) ablation; n = %lld > 4,000,000", (long long)n);
             return TF_ERR_INVALID;
         }
         TF_TRY(require_device(centroids, "centroids"));

@@ -921,6 +921,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
                               tf_filter_s *h) {
     const bool speculate = (flags & kBuildNoSpeculation) == 0;
     flags &= ~kBuildNoSpeculation;
+    if (flags == TF_BUILD_DENSE) return build_dense_csr(c, n, dim, rmin, s, h);  // ablation (dense_build.cu)
     if (flags != TF_BUILD_CELL_LIST && flags != TF_BUILD_CELL_LIST_BINS) {
         bool used = false;
         TF_TRY(build_lattice_csr(c, n, dim, rmin, s, h, &used, speculate));

@@ -324,6 +324,8 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
 // points; *done = false (TF_OK, nothing allocated in h) when a union exceeds their capacity
 tf_status build_cell_list_groups(const SortedPtsView &P, const uint32_t *sorted_keys, const Grid &g, int64_t n,
                                  cudaStream_t s, tf_filter_s *h, bool *done);
+// dense_build.cu: the all-pairs ablation (TF_BUILD_DENSE)
+tf_status build_dense_csr(const double *c, int64_t n, int dim, double rmin, cudaStream_t s, tf_filter_s *h);
 // lattice_build.cu: *used = false (and TF_OK) when the centroids are not a verified lattice
 tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cudaStream_t s, tf_filter_s *h,
                             bool *used, bool speculate = true);
