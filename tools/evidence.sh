@@ -38,3 +38,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hz
 timeout 300 python tools/matrix_free_probe.py > gpurun_out/ev_mf_probe.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^(k_stencil|k_lattice)$" -c 2 -o gpurun_out/ev_mf python tools/matrix_free_probe.py > gpurun_out/ev_ncu_mf.log 2>&1; echo ncu_mf=$?
 timeout 600 python tools/shard_probe.py 2 4 8 > gpurun_out/ev_shard_probe.jsonl 2> gpurun_out/ev_shard_probe.err; echo shard=$?
+timeout 600 python tools/dense_probe.py > gpurun_out/ev_dense_probe.jsonl 2> gpurun_out/ev_dense_probe.err; echo dense=$?

@@ -241,6 +241,18 @@ def main(rnd):
               f"halo {100 * r['halo_frac']:.0f}% of owned, {r['halo_mb_per_sens_apply']:.1f} MB per apply; "
               f"all local rows {r['sens_us_all_local_rows'] + r['dens_us_all_local_rows']:.0f} vs owned rows "
               f"{r['sens_us'] + r['dens_us']:.0f} µs)" for r in rows if r["world"] > 1) + ".\n")
+    dp = os.path.join(EV, "ev_dense_probe.jsonl")
+    if os.path.exists(dp):
+        shutil.copy(dp, os.path.join(dst, "dense_probe.jsonl"))
+    dp = os.path.join(dst, "dense_probe.jsonl")
+    if os.path.exists(dp):
+        drows = [json.loads(l) for l in open(dp) if l.strip().startswith("{")]
+        w("Ablation, the paper's all-pairs build on the same GPU (`dense_probe.jsonl`, `tools/dense_probe.py`; "
+          "`TF_BUILD_DENSE`: every pair visited as the paper's distance matrix does, exact fp64 pair tests, "
+          "no N x N storage) against the cell list: " + "; ".join(
+              f"{r['input']} (n = {r['n']:,}): {r['dense_ms']:.2f} ms vs {r['cell_list_ms']:.2f} ms "
+              f"({r['speedup_cell_list']:.0f}x; the fp64 distance matrix would take {r['edm_bytes_fp64'] / 1e9:.1f} GB)"
+              for r in drows) + ".\n")
     probe = os.path.join(EV, "ev_helm_probe.log")
     if os.path.exists(probe):
         shutil.copy(probe, os.path.join(dst, "helm_probe.log"))
