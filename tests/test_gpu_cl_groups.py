@@ -101,6 +101,26 @@ def test_union_beyond_capacity_falls_back(tf):
     f.close()
 
 
+@pytest.mark.parametrize("npts,groups_run", [(4000, True), (4400, False)])
+def test_union_run_code_limit(tf, npts, groups_run):
+    """The sorted union travels from the count to the fill as 16-bit codes (run << 12 | offset), so a
+    union run may hold at most 4,095 points. One bin with 4,000 points (unions of ~4,050 <= 6,144,
+    runs < 4,096): the group kernels run, offsets up to ~4,000 are exercised and every row takes the
+    long-row path; with 4,400 points the run no longer fits the code and the per-bin kernels take
+    the build. Either way the CSR is the oracle's."""
+    rng = np.random.default_rng(17)
+    c = np.concatenate([rng.uniform(0.05, 0.45, size=(npts, 2)), rng.uniform(2.0, 60.0, size=(50, 2))])
+    ref = oracle.build_celllist(c, 0.6)
+    f = tf.tf_build_filter(dev(c), 0.6, path="cell_list")
+    assert (f.stats()["groups"] > 0) == groups_run
+    rowptr, cols, vals, hs = (t.cpu().numpy() for t in f.csr())
+    np.testing.assert_array_equal(rowptr, ref.rowptr)
+    np.testing.assert_array_equal(cols, ref.cols)
+    np.testing.assert_array_equal(vals, ref.vals)
+    np.testing.assert_allclose(hs, ref.hs, rtol=1e-12)
+    f.close()
+
+
 def test_sparse_rows_wide_groups(tf):
     """Long sparse x-rows: a group's 32 points span many bins (wide union box, wide fp32 band),
     groups are cut at 32-bin unit boundaries and at bin-row ends."""
