@@ -196,6 +196,50 @@ __global__ void __launch_bounds__(256) k_lat_count_exact(LatDev m, LatClasses cl
     }
 }
 
+// Exact mode row pointers in closed form (speculative build): the row length depends on the row's
+// boundary class only, so the prefix sum over rows in lattice order splits per axis into a prefix
+// over the classes before the row's position plus (interior positions before it) x (the interior
+// class's total): rowptr = Z(k) + Y(j | cz) + X(i | cy, cz) + T(t | cx, cy, cz), all from a few
+// host-built int64 tables -- no count pass, no scan.
+struct LatRowptrTabs {
+    const int64_t *tp;   // [ncls] entries of the cube's types before t
+    const int64_t *px;   // [C2*C1][C0+1] prefix over x classes of the cube totals
+    const int64_t *sxr;  // [C2*C1] cube total of the interior x class
+    const int64_t *py;   // [C2][C1+1] prefix over y classes of the x-line totals
+    const int64_t *syr;  // [C2] x-line total of the interior y class
+    const int64_t *pz;   // [C2+1] prefix over z classes of the plane totals
+    int64_t szr;         // plane total of the interior z class
+    int64_t total;       // nnz
+};
+__device__ __forceinline__ int64_t lat_axis_prefix(int p, int n, int R, const int64_t *P, int64_t SR) {
+    if (n < 2 * R + 1) return P[p];
+    const int c = lat_axis_class(p, n, R);
+    return (c <= R) ? P[c] + (int64_t)max(0, p - R) * SR : P[c] + (int64_t)(n - 2 * R - 1) * SR;
+}
+template <int DIM>
+__global__ void __launch_bounds__(256) k_lat_rowptr_exact(LatDev m, LatRowptrTabs tb, int64_t *__restrict__ rowptr) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= m.n; r += (int64_t)gridDim.x * blockDim.x) {
+        if (r == m.n) {
+            rowptr[r] = tb.total;
+            continue;
+        }
+        const uint32_t u = (uint32_t)r;
+        const int t = (int)(u % (uint32_t)m.T);
+        const uint32_t cube = u / (uint32_t)m.T;
+        const int i = (int)(cube % (uint32_t)m.nx);
+        const uint32_t rr = cube / (uint32_t)m.nx;
+        const int j = (int)(rr % (uint32_t)m.ny), k = (int)(rr / (uint32_t)m.ny);
+        const int cy = lat_axis_class(j, m.ny, m.R[1]);
+        const int cz = (DIM == 3) ? lat_axis_class(k, m.nz, m.R[2]) : 0;
+        const int yz = cz * m.C[1] + cy;
+        int64_t v = tb.tp[lat_class_id<DIM>(m, t, i, j, k)];
+        v += lat_axis_prefix(i, m.nx, m.R[0], tb.px + (size_t)yz * (m.C[0] + 1), tb.sxr[yz]);
+        v += lat_axis_prefix(j, m.ny, m.R[1], tb.py + (size_t)cz * (m.C[1] + 1), tb.syr[cz]);
+        if (DIM == 3) v += lat_axis_prefix(k, m.nz, m.R[2], tb.pz, tb.szr);
+        rowptr[r] = v;
+    }
+}
+
 // Cycle table of the exact fill, four shifted copies so that any four consecutive entries are one
 // 16-byte-aligned vector read: copy s holds entries s, s+1, ... of the extended cycle sequence
 // (types 0..T-1 concatenated, S entries; entries S.. repeat the start one cycle later, coloff + T).
@@ -1081,18 +1125,61 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
         const LatClasses cls{reinterpret_cast<const uint32_t *>(at(o_mask)),
                              reinterpret_cast<const int32_t *>(at(o_pre)), reinterpret_cast<const int32_t *>(at(o_len)),
                              reinterpret_cast<const double *>(at(o_hs)), (int)ncls, Wc};
-        DevBuf<int32_t> counts, flag;
-        TF_TRY(counts.alloc(n, s, "row counts"));
+        DevBuf<int32_t> flag;
         TF_TRY(flag.alloc(1, s, "lattice fill flag"));
         TF_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int32_t), s));
+        // row pointers in closed form (k_lat_rowptr_exact): per-axis class prefixes of the class lengths
+        DevBuf<int64_t> rpt;
         {
-            const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)di.sms * 16);
-            if (dim == 3) k_lat_count_exact<3><<<g, 256, 0, s>>>(L, cls, counts.p);
-            else k_lat_count_exact<2><<<g, 256, 0, s>>>(L, cls, counts.p);
+            const int C0 = L.C[0], C1 = L.C[1], C2 = L.C[2], T = M.T;
+            auto axis_total = [&](int d, const int64_t *P, int64_t SR) -> int64_t {
+                return (nd[d] < 2 * R[d] + 1) ? P[nd[d]] : P[L.C[d]] + (int64_t)(nd[d] - 2 * R[d] - 1) * SR;
+            };
+            const size_t o_tp = 0, o_px = o_tp + ncls, o_sxr = o_px + (size_t)C2 * C1 * (C0 + 1),
+                         o_py = o_sxr + (size_t)C2 * C1, o_syr = o_py + (size_t)C2 * (C1 + 1), o_pz = o_syr + C2,
+                         o_end = o_pz + C2 + 1;
+            std::vector<int64_t> rt(o_end, 0);
+            int64_t szr = 0;
+            for (int cz = 0; cz < C2; ++cz) {
+                for (int cy = 0; cy < C1; ++cy) {
+                    const int yz = cz * C1 + cy;
+                    int64_t *px = &rt[o_px + (size_t)yz * (C0 + 1)];
+                    for (int cx = 0; cx < C0; ++cx) {
+                        int64_t cube = 0;
+                        for (int t = 0; t < T; ++t) {
+                            const size_t c = ((size_t)yz * C0 + cx) * T + t;
+                            rt[o_tp + c] = cube;
+                            cube += cls_len[c];
+                        }
+                        px[cx + 1] = px[cx] + cube;
+                        if (cx == R[0]) rt[o_sxr + yz] = cube;
+                    }
+                    int64_t *py = &rt[o_py + (size_t)cz * (C1 + 1)];
+                    const int64_t line = axis_total(0, px, rt[o_sxr + yz]);
+                    py[cy + 1] = py[cy] + line;
+                    if (cy == R[1]) rt[o_syr + cz] = line;
+                }
+                const int64_t plane = (dim >= 2) ? axis_total(1, &rt[o_py + (size_t)cz * (C1 + 1)], rt[o_syr + cz])
+                                                 : rt[o_py + (size_t)cz * (C1 + 1) + 1];
+                rt[o_pz + cz + 1] = rt[o_pz + cz] + plane;
+                if (cz == R[2]) szr = plane;
+            }
+            const int64_t total = (dim == 3) ? axis_total(2, &rt[o_pz], szr) : rt[o_pz + 1];
+            if (total != nnz_h) {
+                set_error("internal: lattice row-pointer tables disagree with nnz (%lld vs %lld)", (long long)total,
+                          (long long)nnz_h);
+                return TF_ERR_CUDA;
+            }
+            TF_TRY(rpt.alloc(o_end, s, "lattice row-pointer tables"));
+            TF_CUDA_TRY(cudaMemcpyAsync(rpt.p, rt.data(), o_end * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+            TF_TRY(dalloc(&h->rowptr, n + 3, s, "rowptr (+2 padding for 16-byte bulk copies)"));
+            const LatRowptrTabs tb{rpt.p + o_tp, rpt.p + o_px, rpt.p + o_sxr, rpt.p + o_py, rpt.p + o_syr,
+                                   rpt.p + o_pz, szr, total};
+            const unsigned g = (unsigned)std::min<int64_t>((n + 256) / 256, (int64_t)di.sms * 16);
+            if (dim == 3) k_lat_rowptr_exact<3><<<g, 256, 0, s>>>(L, tb, h->rowptr);
+            else k_lat_rowptr_exact<2><<<g, 256, 0, s>>>(L, tb, h->rowptr);
             TF_LAUNCH_CHECK();
         }
-        TF_TRY(dalloc(&h->rowptr, n + 3, s, "rowptr (+2 padding for 16-byte bulk copies)"));
-        TF_TRY(exclusive_scan_i32_i64(counts.p, h->rowptr, n, s));
         TF_TRY(dalloc(&h->cols, nnz_h + 4, s, "cols (nnz int32, +4 padding for 16-byte bulk copies)"));
         TF_TRY(dalloc(&h->vals, nnz_h + 4, s, "vals (nnz fp64, +4 padding)"));
         TF_TRY(dalloc(&h->hs, n, s, "Hs"));
