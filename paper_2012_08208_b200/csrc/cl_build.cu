@@ -796,11 +796,14 @@ __global__ void __launch_bounds__(128) k_cl_fill4(SortedPtsView P, Grid g, const
 #ifdef TF_DEBUG_CHECKS
     const double r2 = g.r2;
 #endif
+    // Hs: the lanes' partial sums of a warp's (up to 8) rows are parked in shared memory and reduced
+    // together after the rows are written (a 5-step shuffle tree per row was 15% of the kernel's
+    // instructions on short 2D rows); fixed order, so Hs is reproducible run to run
+    __shared__ double s_hs[4][8][33];
     for (int i = warp; i < nq; i += 4) {
         const uint16_t *my = ent + (size_t)i * S;
         const int li = __shfl_sync(0xffffffffu, len, i);
         const int64_t bi = __shfl_sync(0xffffffffu, rbase, i);
-        const int32_t qi = __shfl_sync(0xffffffffu, qid, i);
         const double qx = __shfl_sync(0xffffffffu, qxl, i), qy = __shfl_sync(0xffffffffu, qyl, i);
         const double qz = (DIM == 3) ? __shfl_sync(0xffffffffu, qzl, i) : 0.0;
         const bool longrow = li > S - 2;
@@ -867,9 +870,21 @@ __global__ void __launch_bounds__(128) k_cl_fill4(SortedPtsView P, Grid g, const
                 done += __shfl_sync(0xffffffffu, inc, 31);
             }
         }
+        s_hs[warp][i >> 2][lane] = hsum;
+    }
+    __syncwarp();
+    {
+        // lane = (row j of this warp, quarter): 8 partials in lane order, then the four quarters
+        const int j = lane >> 2, part = lane & 3, i = warp + 4 * j;
+        double t = 0.0;
+        if (i < nq) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
-        if (lane == 0) hs[qi] = hsum;
+            for (int k = 0; k < 8; ++k) t += s_hs[warp][j][8 * part + k];
+        }
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        const int32_t qi = __shfl_sync(0xffffffffu, qid, min(i, 31));
+        if (part == 0 && i < nq) hs[qi] = t;
     }
 }
 
