@@ -507,6 +507,9 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_cl_count(SortedPtsView P, 
 #define TF_CL_FILL3_WARPS 4
 #endif
 constexpr int kFill3Warps = TF_CL_FILL3_WARPS;  // warps per block: consecutive groups, i.e. neighbours along x
+#ifndef TF_CL_FILL3_PREFETCH
+#define TF_CL_FILL3_PREFETCH 1
+#endif
 #ifndef TF_CL_FILL3_MINB
 #define TF_CL_FILL3_MINB (32 / TF_CL_FILL3_WARPS)
 #endif
@@ -554,6 +557,14 @@ __global__ void __launch_bounds__(kFill3Warps * 32, TF_CL_FILL3_MINB)
         rbase = rowptr[qid];
         len = (int)(rowptr[qid + 1] - rbase);
     }
+#if TF_CL_FILL3_PREFETCH
+    // the group's mask block ([word][query], 128 bytes per word) comes from DRAM: touch every word
+    // line now, all in flight at once, instead of meeting the misses one by one along the walk
+    for (int k = lane; k < nw; k += 32)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(mask + kHalves * base + (size_t)WS * k + 32 * half));
+    for (int t = 64 * lane; t < L; t += 64 * 32)  // and the union's code list (128 bytes = 64 codes per line)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(ul + t));
+#endif
     {
         // branch-free walk: every step either emits up to two set bits of the current word or moves
         // to the next word (loaded one step ahead)
@@ -723,6 +734,7 @@ __global__ void __launch_bounds__(128) k_cl_fill4(SortedPtsView P, Grid g, const
         rbase = rowptr[qid];
         len = (int)(rowptr[qid + 1] - rbase);
     }
+    for (int k = tid; k < nw; k += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(mask + base + 32 * k));
     // (2) staging loads first (they overlap the walk)
     constexpr int SU = 3;
     PtRec sp[SU];
