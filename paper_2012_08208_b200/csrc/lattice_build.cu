@@ -1117,6 +1117,11 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
         const int LP = (std::max(1024, ntab_) + 1) & ~1;
         int LW = (ntab_ + LP + 2 + 1) & ~1;
         if ((size_t)2 * LW * sizeof(double) > (size_t)96 * 1024) LW = 0;
+        // the replica must fit beside the cycle table and the class masks (found by tools/lattice_soak.py:
+        // large tables passed the 160 KB check above and then overflowed the block's shared memory)
+        if ((size_t)2 * LW * sizeof(double) + (size_t)4 * SP * (sizeof(int32_t) + sizeof(double)) +
+                LatClasses::smem_bytes((int)ncls, Wc) + 4096 > di.smem_optin)
+            LW = 0;
 #ifdef TF_LAT_NO_BULK
         LW = 0;
 #endif
@@ -1260,6 +1265,9 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     const int LP = (std::max(1024, (int)ntab) + 1) & ~1;
     int LW = ((int)ntab + LP + 2 + 1) & ~1;
     if (!exact || (size_t)2 * LW * sizeof(double) > (size_t)96 * 1024) LW = 0;
+    if (exact && (size_t)2 * LW * sizeof(double) + (size_t)4 * SP * (sizeof(int32_t) + sizeof(double)) +
+                         LatClasses::smem_bytes((int)ncls, Wc) + 4096 > di.smem_optin)
+        LW = 0;
 #ifdef TF_LAT_NO_BULK
     LW = 0;
 #endif

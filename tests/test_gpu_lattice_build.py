@@ -55,6 +55,10 @@ def _lattice_cases():
     yield "kuhn_spec_6x4x2", synth.kuhn_tets(6, 4, 2), 1.5, "lattice_exact"
     yield "kuhn_e02_60x20x4", synth.kuhn_tets(60, 20, 4), 1.5, "lattice_exact"
     yield "kuhn_rmin2.7_downgraded", synth.kuhn_tets(14, 11, 9), 2.7, "lattice_tested"  # classes beyond smem
+    # tables large enough that the cycle table + class masks fit shared memory only without the weight
+    # replica of the bulk stores (found by tools/lattice_soak.py: the launch asked for > 227 KB)
+    yield "kuhn_13x3x2_rmin2.6_large_tables", synth.kuhn_tets(13, 3, 2), 2.6, "lattice_exact"
+    yield "kuhn_13x2x2_rmin2.6_large_tables", synth.kuhn_tets(13, 2, 2), 2.6, "lattice_exact"
     yield "hex_aniso", synth.hex_grid(30, 24, 18) * np.array([1.0, 0.75, 1.25]), 1.6, "lattice_exact"
     yield "kuhn_shift_dyadic", synth.kuhn_tets(12, 10, 8) - 37.5, 1.5, "lattice_exact"
     yield "kuhn_shift_thirds", synth.kuhn_tets(12, 10, 8) + (1.0e3 + 1.0 / 3.0), 1.5, "lattice_tested"
