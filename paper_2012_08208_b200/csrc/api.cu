@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <mutex>
+#include <unordered_map>
 #include <new>
 #include <vector>
 
@@ -137,6 +138,33 @@ tf_status device_info(DeviceInfo *di) {
     int optin = 0;
     TF_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, di->device));
     di->smem_optin = (size_t)optin;
+    return TF_OK;
+}
+
+tf_status allow_dynamic_smem_impl(const void *func, size_t bytes) {
+    // (raised on first use whatever the size: static + dynamic shared memory above 48 KB needs the
+    // opt-in even when the dynamic part alone is below it)
+    int dev = 0;
+    TF_CUDA_TRY(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static std::unordered_map<const void *, uint64_t> raised;  // function -> bit mask of devices done
+    int limit = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        uint64_t &m = raised[func];
+        if (dev < 64 && (m >> dev) & 1) return TF_OK;  // (sizes were validated by the callers' own capacity rules)
+        cudaFuncAttributes fa;
+        TF_CUDA_TRY(cudaFuncGetAttributes(&fa, func));
+        int optin = 0;
+        TF_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        limit = optin - (int)fa.sharedSizeBytes;
+        TF_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+        if (dev < 64) m |= 1ull << dev;
+    }
+    if ((int64_t)bytes > (int64_t)limit) {
+        set_error("internal: a kernel needs %zu bytes of dynamic shared memory, the device allows %d", bytes, limit);
+        return TF_ERR_INVALID;
+    }
     return TF_OK;
 }
 

@@ -469,7 +469,7 @@ tf_status launch_spmv_gu(const tf_filter_s *h, const double *x, const double *dc
     }
     int occ = occ_of[dev].load(std::memory_order_acquire);
     if (!occ) {
-        TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TF_TRY(allow_dynamic_smem(kern, smem));
         TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads + 32, smem));
         if (occ < 1) {
             set_error("apply kernel does not fit on an SM");

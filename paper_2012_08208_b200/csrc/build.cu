@@ -884,7 +884,7 @@ tf_status launch_count(const SortedPts &P, const Grid &g, int cap, int32_t *coun
     const size_t smem = (size_t)cap * (3 * sizeof(float) + sizeof(int32_t));
     auto kern = k_count<DIM, WARPS>;
     // always set: dynamic + static shared memory above 48 KB needs the opt-in attribute
-    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TF_TRY(allow_dynamic_smem(kern, smem));
     kern<<<(unsigned)g.nbins, WARPS * 32, smem, s>>>(P, g, cap, counts, maxrow);
     TF_LAUNCH_CHECK();
     return TF_OK;
@@ -894,7 +894,7 @@ template <int DIM, int WARPS>
 tf_status launch_fill(const SortedPts &P, const Grid &g, tf_filter_s *h, int cap, int32_t *large_rows,
                       int32_t *stats, cudaStream_t s) {
     const size_t smem = (size_t)cap * FillSmem::bytes_per();
-    TF_CUDA_TRY(cudaFuncSetAttribute(k_fill<DIM, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TF_TRY(allow_dynamic_smem(k_fill<DIM, WARPS>, smem));
 #ifdef TF_FILL_CARVEOUT
     TF_CUDA_TRY(cudaFuncSetAttribute(k_fill<DIM, WARPS>, cudaFuncAttributePreferredSharedMemoryCarveout, TF_FILL_CARVEOUT));
 #endif
@@ -1117,7 +1117,7 @@ tf_status build_filter_device(const double *c, int64_t n, int dim, double rmin, 
     if (fill_kind == 0 && maxC > cap) {
         const int scap = 8192;
         const size_t smem = (size_t)scap * (sizeof(double) + sizeof(int32_t));
-        TF_CUDA_TRY(cudaFuncSetAttribute(k_rowsort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TF_TRY(allow_dynamic_smem(k_rowsort, smem));
         k_rowsort<<<(unsigned)di.sms * 2, kSortThreads, smem, s>>>(large_rows.p, stats.p, h->rowptr, h->cols,
                                                                     h->vals, scap);
         TF_LAUNCH_CHECK();

@@ -676,7 +676,7 @@ tf_status launch_cl_fill3(const SortedPtsView &P, const Grid &g, const GroupRec 
                           cudaStream_t s) {
     const size_t smem = (size_t)kFill3Warps * 32 * S * sizeof(uint16_t);
     auto kern = k_cl_fill3<DIM, ROUNDS>;
-    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TF_TRY(allow_dynamic_smem(kern, smem));
     kern<<<(unsigned)(((int64_t)G * kHalves + kFill3Warps - 1) / kFill3Warps), kFill3Warps * 32, smem, s>>>(
         P, g, rec, loff, G, S, list, mask, h->rowptr, h->cols, h->vals, h->hs, stats);
     TF_LAUNCH_CHECK();
@@ -906,7 +906,7 @@ tf_status launch_cl_fill4(const SortedPtsView &P, const Grid &g, const GroupRec 
                           cudaStream_t s) {
     const size_t smem = (size_t)LPmax * ((DIM == 3 ? 24 : 16) + 4) + (size_t)32 * S * sizeof(uint16_t);
     auto kern = k_cl_fill4<DIM, ROUNDS>;
-    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TF_TRY(allow_dynamic_smem(kern, smem));
     kern<<<(unsigned)G, 128, smem, s>>>(P, g, rec, loff, LPmax, S, list, mask, h->rowptr, h->cols, h->vals, h->hs,
                                         stats);
     TF_LAUNCH_CHECK();
@@ -918,7 +918,7 @@ tf_status launch_cl_count(const SortedPtsView &P, const Grid &g, const GroupRec 
                           int LPmax, uint16_t *list, uint32_t *mask, int32_t *counts, int32_t *stats, cudaStream_t s) {
     const size_t smem = (size_t)5 * LPmax * sizeof(uint32_t);
     auto kern = k_cl_count<DIM>;
-    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TF_TRY(allow_dynamic_smem(kern, smem));
     kern<<<(unsigned)G, kCountWarps * 32, smem, s>>>(P, g, rec, loff, LPmax, list, mask, counts, stats);
     TF_LAUNCH_CHECK();
     return TF_OK;

@@ -1192,7 +1192,7 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
             const size_t smem_cyc = (size_t)2 * LW * sizeof(double) + (size_t)4 * SP * (sizeof(int32_t) + sizeof(double)) +
                                     LatClasses::smem_bytes((int)ncls, Wc);
             auto kern = (dim == 3) ? k_lat_fill_exact<3> : k_lat_fill_exact<2>;
-            TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cyc));
+            TF_TRY(allow_dynamic_smem(kern, smem_cyc));
             int per_sm = 0;
             TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem_cyc));
             const int64_t warps_needed = (n + 31) / 32;
@@ -1285,7 +1285,7 @@ tf_status build_lattice_csr(const double *c, int64_t n, int dim, double rmin, cu
     TF_TRY(flag.alloc(1, s, "lattice fill flag"));
     TF_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int32_t), s));
     auto grid_for = [&](auto kern, size_t smem, unsigned *grid) -> tf_status {
-        TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TF_TRY(allow_dynamic_smem(kern, smem));
         int per_sm = 0;
         TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
         const int64_t warps_needed = (n + 31) / 32;

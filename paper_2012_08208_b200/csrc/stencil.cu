@@ -406,7 +406,7 @@ static tf_status launch_lattice(const tf_filter_s *f, const double *x, const dou
     dim3 grid((unsigned)((sg.nx + kTX - 1) / kTX), (unsigned)((sg.ny + TY - 1) / TY),
               (unsigned)((sg.dim == 3) ? (sg.nz + TZ - 1) / TZ : 1));
     auto go = [&](auto kern) -> tf_status {
-        TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TF_TRY(allow_dynamic_smem(kern, smem));
         kern<<<grid, 256, smem, s>>>(sg, tab, f->hs, x, dc, out);
         TF_LAUNCH_CHECK();
         return TF_OK;
@@ -442,7 +442,7 @@ tf_status launch_stencil(const tf_filter_s *f, const double *x, const double *dc
     dim3 grid((unsigned)((sg.nx + kTX - 1) / kTX), (unsigned)((sg.ny + TY - 1) / TY),
               (unsigned)((sg.dim == 3) ? (sg.nz + TZ - 1) / TZ : 1));
     auto go = [&](auto kern) -> tf_status {
-        TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TF_TRY(allow_dynamic_smem(kern, smem));
         kern<<<grid, 256, smem, s>>>(sg, f->stencil_off, f->stencil_w, f->hs, x, dc, out);
         TF_LAUNCH_CHECK();
         return TF_OK;

@@ -151,6 +151,16 @@ struct DeviceInfo {
     size_t smem_optin = 227 * 1024;
 };
 tf_status device_info(DeviceInfo *di);
+// Allow `bytes` of dynamic shared memory for launches of `func` on the current device. The limit is a
+// per-function, process-wide attribute: it is only ever RAISED, and to one value (the device's opt-in
+// maximum minus the kernel's static shared memory), once per (function, device). Setting the exact size
+// before every launch -- as this library did -- lets concurrent builds on different host threads lower
+// the limit under each other's launches ("invalid argument"; found by tools/soak_all.py).
+tf_status allow_dynamic_smem_impl(const void *func, size_t bytes);
+template <class K>
+inline tf_status allow_dynamic_smem(K kern, size_t bytes) {
+    return allow_dynamic_smem_impl(reinterpret_cast<const void *>(kern), bytes);
+}
 // TF_ERR_INVALID unless p is a non-NULL device (or managed) pointer
 tf_status require_device(const void *p, const char *name);
 // TF_ERR_INVALID unless the current CUDA device is `device` (a handle's build device)
