@@ -143,6 +143,11 @@ def soak_sharded(seed, rng):
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
     rng = np.random.default_rng(777)
+    if len(sys.argv) > 2 and sys.argv[2] == "sharded":  # sharded runs only
+        for seed in range(cases):
+            soak_sharded(5000 + seed, rng)
+        print(f"soak: {cases} sharded runs, {len(BAD)} mismatches")
+        sys.exit(1 if BAD else 0)
     for seed in range(cases):
         soak_applies(seed, rng)
         soak_matrix_free(seed, rng)
